@@ -1,0 +1,344 @@
+"""Benchmark: surface fixation density-map generation on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+One step = one full density-map generation (all fixations of the workload)
+over the resident scene.  Workload (BASELINE.json configs[1]):
+C2 room, 98,080 triangles / 20 objects, k = 10,000 samples/m^2 (N = 2.19 M
+samples), 100,000 fixations, 4-sigma filtering on, 512^2 z-buffer.  Under
+torchrun (N > 1) every rank generates its own 100,000-fixation shard of an
+N x 100,000 stream (weak scaling) and the partial maps are combined with one
+NCCL sum all-reduce, followed by the global max.
+
+metric: sample-fixation pairs per second (N_samples * F / t), the same
+numerator for CPU and GPU, filtered or not.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "sample-fixation pairs/s (density-map generation)"
+UNIT = "pairs/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c2off", "c5"])
+    ap.add_argument("--fixations", type=int, default=0, help="override fixations per rank")
+    ap.add_argument("--batch", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-fixations", type=int, default=0)
+    return ap.parse_args()
+
+
+def workload(name: str, n_fix: int, rank: int):
+    import workloads as W
+
+    filtering = True
+    if name == "c1":
+        scene, k, fx = W.c1()
+    elif name in ("c2", "c2off"):
+        scene = W.room_scene()
+        k = 10_000.0
+        fx = W.room_fixations(n_fix or 100_000, seed=1 + 1000 * rank, scene=scene)
+        filtering = name == "c2"
+    elif name == "c5":
+        scene = W.shells_scene()
+        k = 20_000.0
+        fx = W.orbit_fixations(n_fix or 50_000, 4 + 1000 * rank, 4.5, 6.0, jitter=0.3)
+    else:
+        raise ValueError(name)
+    if n_fix:
+        fx = fx[:n_fix]
+    desc = {"c1": "C1 icosphere(3), k=1e3, 200 fixations",
+            "c2": "C2 room 98,080 tris/20 objects, k=1e4, 100k fixations, filtering on",
+            "c2off": "C2 room 98,080 tris/20 objects, k=1e4, 100k fixations, filtering off",
+            "c5": "C5 12 nested icosphere(6) shells 983,040 tris, k=2e4, 50k fixations"}[name]
+    return scene, k, np.ascontiguousarray(fx), filtering, desc
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int = 0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_port_pairs_per_s(scene, k, fx, filtering, n_fix, threads):
+    """The oracle port (oracle/gm_oracle.c: the reference algorithm restated in
+    C, numba's prange -> OpenMP over samples) on a bounded fixation prefix."""
+    from oracle import oracle as O
+
+    lay = O.build_layouts(scene, k)
+    N = sum(v[3] for v in lay.values())
+    rows = O.rows_as_fixations(fx[:n_fix])
+    O.generate(scene, rows[:2], k=k, filtering_enabled=filtering, threads=threads, layouts=lay)  # warm
+    t0 = time.perf_counter()
+    O.generate(scene, rows, k=k, filtering_enabled=filtering, threads=threads, layouts=lay)
+    dt = time.perf_counter() - t0
+    return N * len(rows) / dt, dt, N
+
+
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    scene, k, fx, filtering, desc = workload(args.config, args.fixations, 0)
+    threads = host_threads()
+    per_step = args.cpu_fixations or (100 if args.config != "c1" else 200)
+    from oracle import oracle as O
+
+    lay = O.build_layouts(scene, k)
+    N = sum(v[3] for v in lay.values())
+    rows = O.rows_as_fixations(fx)
+    for i in range(args.warmup):
+        O.generate(scene, rows[:max(2, per_step // 10)], k=k, filtering_enabled=filtering, threads=threads, layouts=lay)
+    times = []
+    for s in range(args.steps):
+        sl = rows[(s * per_step) % len(rows):][:per_step]
+        t0 = time.perf_counter()
+        O.generate(scene, sl, k=k, filtering_enabled=filtering, threads=threads, layouts=lay)
+        times.append(time.perf_counter() - t0)
+    t = sum(times) / len(times)
+    v = N * per_step / t
+    print(json.dumps({
+        "metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": desc, "samples": int(N), "fixations_per_step": per_step,
+                   "note": "CPU port of the reference algorithm (oracle/gm_oracle.c), bounded prefix per step"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{per_step} fixations of the workload per step, {N} samples"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+class _CudaArray:
+    def __init__(self, ptr, n):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (ptr, False), "version": 3}
+
+
+def run_ours(args, rank, world):
+    import paper_2601_07571_b200 as gm
+    from paper_2601_07571_b200 import _native
+
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
+        dist.init_process_group("nccl")
+    device = int(os.environ.get("LOCAL_RANK", 0)) if world > 1 else 0
+    if world > 1:
+
+    scene, k, fx, filtering, desc = workload(args.config, args.fixations, rank)
+    cfg = gm.GenerationConfig(k=k, filtering_enabled=filtering)
+    sampled = gm.build_sampled_meshes(scene, k, device=device)
+    plan = gm.ScenePlan(scene, sampled, scene.object_ids, device=device)
+    lib = _native.load()
+    N = plan.n_samples
+    F = len(fx)
+    ccfg = _native.GmConfig(cfg.theta, cfg.epsilon_abs, cfg.epsilon_rel, cfg.zbuffer_resolution,
+                            int(filtering), args.batch, 0)
+    bad = np.zeros(1, np.int64)
+    _native.check(lib.gm_plan_prepare(plan._h, _native.dptr(fx), F, ctypes.byref(ccfg), _native.iptr(bad)))
+
+    reduce_t = None
+    if world > 1:
+        import torch
+
+        vals_t = torch.as_tensor(_CudaArray(plan.values_device_ptr(), N), device=f"cuda:{device}")
+
+    def one_step(timed_stats=None):
+        tm = _native.GmTimings()
+        ms = ctypes.c_float(0.0)
+        _native.check(lib.gm_plan_run(plan._h, 1, ctypes.byref(tm), ctypes.byref(ms)), "gm_plan_run")
+        extra = 0.0
+        if world > 1:
+            import torch
+
+            ev0 = torch.cuda.Event(enable_timing=True)
+            ev1 = torch.cuda.Event(enable_timing=True)
+            ev0.record()
+            dist.all_reduce(vals_t)
+            ev1.record()
+            torch.cuda.synchronize()
+            extra = ev0.elapsed_time(ev1)
+        gmax = plan.global_max()
+        return ms.value + extra, tm, gmax
+
+    for _ in range(args.warmup):
+        one_step()
+    times, tms = [], []
+    with ClockSampler(device) as clk:
+        for _ in range(args.steps):
+            _native.check(lib.gm_plan_flush_l2(plan._h, 512 << 20))
+            plan.sync()
+            if world > 1:
+                dist.barrier()
+            t, tm, gmax = one_step()
+            times.append(t)
+            tms.append(tm)
+    step_ms = float(np.mean(times))
+    if world > 1:
+        import torch
+
+        tt = torch.tensor([step_ms], device=f"cuda:{device}", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        step_ms = float(tt.item())
+    value = world * N * F / (step_ms / 1e3)
+    tm = tms[-1]
+    acc_ms = tm.accumulate_ms
+    launches = int(tm.batches) * 6 + 1
+
+    # ---- e2e through the public API (host table in, host values out) -----
+    e2e = None
+    if not args.no_e2e:
+        pinned_vals = None
+        t0 = time.perf_counter()
+        e_times = []
+        for _ in range(max(1, min(args.steps, 2))):
+            t0 = time.perf_counter()
+            dm = gm.generate(scene, sampled, fx, cfg, device=device)
+            e_times.append(time.perf_counter() - t0)
+        e_t = float(np.mean(e_times))
+        e2e = {"value": world * N * F / e_t if world == 1 else None, "unit": UNIT,
+               "h2d_bytes_per_step": int(F * (224 + 80)), "d2h_bytes_per_step": int(N * 8),
+               "ms_per_step": e_t * 1e3, "path": "paper_2601_07571_b200.generate (fixation table -> values dict)"}
+        if world > 1:
+            import torch
+
+            tt = torch.tensor([e_t], device=f"cuda:{device}", dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e2e["value"] = world * N * F / float(tt.item())
+
+    peaks_path = ROOT / "MEASURED_PEAKS.json"
+    peaks = json.loads(peaks_path.read_text()) if peaks_path.exists() else {}
+    # FP32 SIMT peak: 148 SMs x 128 lanes x 2 flop x max SM clock (nominal; no measured FP32 figure exists)
+    fp32_peak = 148 * 128 * 2 * (peaks.get("sm_max_mhz", 1965.0) * 1e6) / 1e12
+    # reference-algorithmic work: 26 FP32-equivalent flops per nominal pair
+    alg_flops = 26.0 * N * F
+    roof = {"bound": "fp32", "achieved": alg_flops / (acc_ms / 1e3) / 1e12 if acc_ms else None,
+            "peak": fp32_peak, "unit": "TFLOP/s", "frac": None, "traffic": None,
+            "kernel": "k_accumulate", "kernel_ms_per_step": acc_ms,
+            "note": "reference-algorithmic 26 flop/pair over the whole step's k_accumulate time; "
+                    "peak = nominal FP32 SIMT at max SM clock"}
+    if roof["achieved"]:
+        roof["frac"] = roof["achieved"] / fp32_peak
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            n_cpu = args.cpu_fixations or (200 if args.config == "c1" else 100)
+            v, dt, _ = cpu_port_pairs_per_s(scene, k, fx, filtering, n_cpu, host_threads())
+            cpu = {"value": v, "unit": UNIT, "cores": host_threads(), "kind": "port",
+                   "sample": f"first {n_cpu} fixations of the workload ({dt:.1f} s), oracle/gm_oracle.c with OpenMP"}
+        except Exception as e:  # the baseline is reported, never required
+            cpu = {"value": None, "unit": UNIT, "cores": host_threads(), "kind": "port", "sample": f"failed: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": desc, "samples": int(N), "triangles": int(plan._lib.gm_plan_num_triangles(plan._h)),
+                       "fixations_per_gpu": int(F), "zbuffer": cfg.zbuffer_resolution, "filtering": filtering,
+                       "parallelism": f"fixation-sharded x{world}, NCCL sum all-reduce" if world > 1 else "single GPU",
+                       "l2": "flushed (512 MiB write) before every timed step",
+                       "timing": "CUDA events on the plan stream around each full generation (+ all-reduce)"},
+            "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "clocks": clk.summary(), "gpu_launches": launches,
+            "phases_ms": {"cull": tm.cull_ms, "bin": tm.rasterize_ms, "accumulate": tm.accumulate_ms,
+                          "batches": tm.batches, "screen_tris": tm.screen_tris, "bin_items": tm.bin_items},
+            "global_max": gmax,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", args.gpus if args.gpus == 1 else 1))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world)
+
+
+if __name__ == "__main__":
+    main()

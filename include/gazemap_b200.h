@@ -1,0 +1,149 @@
+/*
+ * gazemap_b200.h -- C ABI of the B200-native density-map generation path.
+ *
+ * Library: paper_2601_07571_b200/_gazemap_b200.so (sm_100a kernels, static
+ * cudart, host OpenMP).  Plain pointers and sizes only; every entry point
+ * returns an int status (0 = GM_OK) and never throws; gm_last_error() gives
+ * the message of the calling thread's last failure.  All host buffers are
+ * owned by the caller; the library allocates only device memory it owns.
+ *
+ * Reference interface replaced (paths under /root/reference/pkg/src/gazemap):
+ * the reference has no FFI; its hot path sits behind numba kernels called from
+ * Python (kernels.py) and the Python functions of geometry.py / density.py.
+ * Each entry point below names the function(s) it replaces.
+ */
+#ifndef GAZEMAP_B200_H
+#define GAZEMAP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    GM_OK = 0,
+    GM_ERR_CUDA = 1,             /* CUDA runtime failure */
+    GM_ERR_ARG = 2,              /* invalid argument -> ConfigError */
+    GM_ERR_INVALID_FRUSTUM = 3,  /* perspective_matrix bounds -> InvalidFrustumError (gaze.py:325-328) */
+    GM_ERR_NO_DEVICE = 4,        /* no CUDA device: there is no CPU fallback */
+    GM_ERR_OOM = 5,
+    GM_ERR_UNSUPPORTED = 6
+};
+
+/* Fixation table: F rows x 18 float64 in the fixation-log column order
+ * (gaze.py:133-136): start_time, duration, camera position xyz, camera
+ * rotation quaternion xyzw, frustum l r t b n f, gaze direction xyz
+ * (unit, as Fixation.__post_init__ leaves it, gaze.py:91-95). */
+#define GM_FIX_STRIDE 18
+
+/* GenerationConfig (density.py:44-71); k is consumed by gm_layout. */
+typedef struct GmConfig {
+    double theta;               /* 1-sigma gaze angle, radians (0, pi/2) */
+    double eps_abs;             /* depth tolerance, meters (raster.py:30) */
+    double eps_rel;             /* relative depth tolerance (raster.py:31) */
+    int32_t zbuffer_resolution; /* square z-buffer side, 1..65535 */
+    int32_t filtering;          /* 1: 4-sigma crop frustum, 0: full frustum */
+    int32_t batch;              /* fixations per GPU batch, 0 = auto */
+    int32_t flags;              /* reserved, 0 */
+} GmConfig;
+
+/* Timings.phases (density.py:94-103), measured with CUDA events. */
+typedef struct GmTimings {
+    double setup_ms, cull_ms, rasterize_ms, accumulate_ms, total_ms;
+    int64_t screen_tris, bin_items, batches;
+} GmTimings;
+
+typedef struct gm_plan gm_plan;
+typedef void (*gm_progress_fn)(int64_t done, int64_t total, void* user);
+
+const char* gm_last_error(void);
+int gm_abi_version(void);
+int gm_device_count(void);
+
+/* ---- stage 1: sampling -------------------------------------------------- */
+
+/* build_sampled_mesh (geometry.py:305-320): triangle_areas :169-176,
+ * adaptive_resolutions :202-210, counts, exclusive-prefix offsets, total.
+ * tri_local: T x 3 x 3 corner positions.  Outputs may be NULL except total. */
+int gm_layout(int device, const double* tri_local, int64_t T, double k, int64_t* res, int64_t* counts,
+              int64_t* offsets, int64_t* total);
+
+/* sample_positions_local (geometry.py:331-346), then Transform.apply
+ * (geometry.py:86-89) when xform = [t(3), q xyzw(4), s(3)] is non-NULL.
+ * out: N x 3. */
+int gm_sample_positions(int device, const double* tri_local, int64_t T, const int64_t* res,
+                        const int64_t* offsets, int64_t N, const double* xform, double* out);
+
+/* normalize (density.py:230-244) of n values by gmax > 0. */
+int gm_normalize(int device, const double* values, int64_t n, double gmax, double* out);
+
+/* ---- per-fixation setup (host, bit-exact with CPython + glibc) ---------- */
+
+/* Fixation.view_matrix (gaze.py:114-122), build_crop_frustum (gaze.py:372-381)
+ * with the GazeOutsideFrustumError fallback of density.py:152-158,
+ * frustum_from_matrix (gaze.py:345-356).  ex: F x 28 float64 (GmFixExact in
+ * csrc/gm_types.h), cull: F x 20 float32 or NULL. */
+int gm_fixation_setup(const double* fixations, int64_t F, double theta, int filtering, int res, double* ex,
+                      void* cull, int64_t* bad_fixation);
+
+/* ---- scene plan: occluders + samples resident on one GPU ---------------- */
+
+int gm_plan_create(int device, gm_plan** out);
+void gm_plan_destroy(gm_plan* plan);
+int gm_plan_set_host_threads(gm_plan* plan, int n);
+
+/* _SampleCache (density.py:106-121) + scene_world_triangles (raster.py:68-78):
+ * n_obj objects with tri_counts[o] triangles, local corners tri_local
+ * (sum T x 9, object order), transforms xforms (n_obj x [t, q, s]), the
+ * SampledMesh resolutions res (sum T) and include flags (object_include_list,
+ * density.py:130-133).  Occluders are all objects; samples are the included
+ * objects' samples concatenated in object order. */
+int gm_plan_set_scene(gm_plan* plan, int n_obj, const int64_t* tri_counts, const double* tri_local,
+                      const double* xforms, const int64_t* res, const uint8_t* include);
+int64_t gm_plan_num_samples(gm_plan* plan);
+int64_t gm_plan_num_triangles(gm_plan* plan);
+double* gm_plan_values_device(gm_plan* plan); /* device pointer to the N accumulators */
+
+/* generate / accumulate_fixation (density.py:136-227): add the F fixations, in
+ * log order, into the plan's device values (zeroed first if reset).  One
+ * fused pass per batch replaces cull_mask + rasterize + accumulate
+ * (kernels.py:140-340).  progress(done, total) is called as batches complete. */
+int gm_plan_accumulate(gm_plan* plan, const double* fixations, int64_t F, const GmConfig* cfg, int reset,
+                       GmTimings* timings, gm_progress_fn progress, void* user, int64_t* bad_fixation);
+
+/* Device-resident replay (bench): compute the F fixations' setup records once
+ * into HBM, then gm_plan_run repeats the whole generation from them;
+ * device_ms = CUDA-event time of the pass on the plan's stream. */
+int gm_plan_prepare(gm_plan* plan, const double* fixations, int64_t F, const GmConfig* cfg, int64_t* bad_fixation);
+int gm_plan_run(gm_plan* plan, int reset, GmTimings* timings, float* device_ms);
+/* Write `bytes` of scratch on the plan's stream to evict L2 between repetitions. */
+int gm_plan_flush_l2(gm_plan* plan, int64_t bytes);
+
+/* Running global max (density.py:192) of the plan's values. */
+int gm_plan_max(gm_plan* plan, double* gmax);
+/* Copy values to host: raw (may be NULL) and/or normalized = raw / gmax. */
+int gm_plan_read(gm_plan* plan, double* raw, double* normalized, double gmax);
+int gm_plan_write(gm_plan* plan, const double* raw);
+int gm_plan_sync(gm_plan* plan);
+
+/* ---- kernel-seam ports (parity instruments) ----------------------------- */
+
+/* kernels.rasterize (kernels.py:140-192) via raster.rasterize_triangles
+ * (raster.py:99-124): res x res depth (+inf where empty) of the plan's
+ * occluders for one fixation row; no_cull = 1 projects every triangle. */
+int gm_plan_depth_buffer(gm_plan* plan, const double* fixation, double theta, int filtering, int res,
+                         int no_cull, double* depth);
+
+/* The NDC crop filter (kernels.py:302-319) as per-fixation candidate lists
+ * (warp-ballot compaction): out F x cap (unsorted per row), counts F. */
+int gm_plan_candidates(gm_plan* plan, const double* fixations, int64_t F, double theta, int filtering, int res,
+                       int64_t* out, int64_t cap, int64_t* counts);
+
+/* World sample positions of the plan (N x 3), _SampleCache.base_world. */
+int gm_plan_positions(gm_plan* plan, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GAZEMAP_B200_H */

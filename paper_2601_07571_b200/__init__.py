@@ -1,0 +1,20 @@
+"""B200-native generation stage of surface-based fixation density maps
+(arXiv 2601.07571), a drop-in for the reference package's Python API.
+
+The compute runs in hand-written sm_100a CUDA kernels (csrc/) reached through
+a C ABI (include/gazemap_b200.h) loaded with ctypes; there is no CPU fallback.
+"""
+
+from .density import (DEFAULT_EPS_ABS, DEFAULT_EPS_REL, DEFAULT_K, DEFAULT_RESOLUTION, DensityMap, GenerationConfig,
+                      ScenePlan, Timings, accumulate_fixation, generate, normalize)
+from .errors import (ConfigError, GazemapError, GazeOutsideFrustumError, InvalidFrustumError, LayoutMismatchError,
+                     ParseError)
+from .estimator import FixationDensityMapper
+from .gaze import (DEFAULT_THETA, SQRT_TWO_PI, Fixation, GazeCone, fixation_setup, fixation_table,
+                   frustum_from_matrix, gaussian_weight, perspective_matrix)
+from .geometry import (Mesh, SampledMesh, Scene, SceneObject, Transform, TriangleSampling, adaptive_resolution,
+                       build_sampled_mesh, build_sampled_meshes, quat_to_matrix, rowcol_to_barycentric,
+                       sample_count, sample_index_to_rowcol, sample_positions_local, sample_world_position,
+                       triangle_area)
+
+__version__ = "0.1.0"

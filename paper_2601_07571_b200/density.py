@@ -1,0 +1,352 @@
+"""Density-map generation on the B200 (drop-in for the reference's
+density.py: GenerationConfig :44-71, DensityMap :74-91, Timings :94-103,
+accumulate_fixation :136-200, generate :203-227, normalize :230-244).
+
+`generate` uploads the scene once into a `ScenePlan` (occluder triangles and
+sample positions resident in HBM), streams the fixation table through the
+extension in batches (host setup of batch i+1 overlaps the GPU work of batch
+i) and reads the per-sample values back.  Per-sample accumulation order is the
+fixation log order, so results are deterministic run to run.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native
+from .errors import ConfigError
+from .gaze import DEFAULT_THETA, GazeCone, fixation_table
+
+__all__ = ["GenerationConfig", "DensityMap", "Timings", "ScenePlan", "accumulate_fixation", "generate",
+           "normalize", "DEFAULT_K", "DEFAULT_EPS_ABS", "DEFAULT_EPS_REL", "DEFAULT_RESOLUTION"]
+
+DEFAULT_K = 40000.0
+DEFAULT_EPS_ABS = 1e-3
+DEFAULT_EPS_REL = 1e-3
+DEFAULT_RESOLUTION = 512
+
+
+@dataclass
+class GenerationConfig:
+    k: float = DEFAULT_K
+    theta: float = DEFAULT_THETA
+    zbuffer_resolution: int = DEFAULT_RESOLUTION
+    epsilon_abs: float = DEFAULT_EPS_ABS
+    epsilon_rel: float = DEFAULT_EPS_REL
+    time_window: tuple | None = None
+    filtering_enabled: bool = True
+    object_include_list: set | None = None
+
+    def validate(self) -> "GenerationConfig":
+        if self.k <= 0:
+            raise ConfigError(f"k must be > 0, got {self.k}")
+        if not 0 < self.theta < math.pi / 2:
+            raise ConfigError(f"theta must be in (0, pi/2), got {self.theta}")
+        if self.zbuffer_resolution < 1:
+            raise ConfigError(f"zbuffer_resolution must be >= 1, got {self.zbuffer_resolution}")
+        if self.epsilon_abs < 0 or self.epsilon_rel < 0:
+            raise ConfigError("epsilon values must be >= 0")
+        if self.time_window is not None and self.time_window[0] > self.time_window[1]:
+            raise ConfigError(f"empty time window {self.time_window}")
+        return self
+
+    def cone(self) -> GazeCone:
+        return GazeCone.from_theta(self.theta)
+
+
+@dataclass
+class DensityMap:
+    values: dict
+    global_max: float = 0.0
+    normalized: bool = False
+
+    @classmethod
+    def zeros(cls, sampled_meshes: dict) -> "DensityMap":
+        return cls({oid: np.zeros(sm.total_samples) for oid, sm in sampled_meshes.items()})
+
+    @property
+    def total_samples(self) -> int:
+        return sum(len(v) for v in self.values.values())
+
+    def copy(self) -> "DensityMap":
+        return DensityMap({k: v.copy() for k, v in self.values.items()}, self.global_max, self.normalized)
+
+
+@dataclass
+class Timings:
+    """Seconds per phase.  cull = occluder cone cull + clip + projection
+    (device), rasterize = screen binning (device), accumulate = filter +
+    visibility + Gaussian (device), setup = host fixation setup."""
+
+    phases: dict = field(default_factory=lambda: {"cull": 0.0, "rasterize": 0.0, "accumulate": 0.0,
+                                                  "normalize": 0.0})
+
+    def add(self, phase: str, seconds: float) -> None:
+        self.phases[phase] = self.phases.get(phase, 0.0) + seconds
+
+
+def _included_ids(scene, config) -> list:
+    ids = [o.object_id for o in scene.objects]
+    if config.object_include_list is None:
+        return ids
+    return [oid for oid in ids if oid in config.object_include_list]
+
+
+class ScenePlan:
+    """A scene resident on one GPU: all objects' world triangles (occluders)
+    and the included objects' world sample positions + value slots."""
+
+    def __init__(self, scene, sampled_meshes: dict, included: list, device: int = 0):
+        lib = _native.load()
+        self.device = device
+        self.scene = scene
+        self.sampled_meshes = sampled_meshes
+        h = ctypes.c_void_p()
+        _native.check(lib.gm_plan_create(device, ctypes.byref(h)), "gm_plan_create")
+        self._h = h
+        self._lib = lib
+        objs = list(scene.objects)
+        inc = set(included)
+        tri_counts, tris, xforms, res, flags = [], [], [], [], []
+        self.slices = {}
+        base = 0
+        for o in objs:
+            v = np.asarray(o.mesh.vertices, dtype=np.float64).reshape(-1, 3)
+            f = np.asarray(o.mesh.faces, dtype=np.int64).reshape(-1, 3)
+            tri_counts.append(len(f))
+            tris.append(v[f].reshape(-1, 9))
+            tr = o.transform
+            xforms.append(np.concatenate([np.asarray(tr.translation, np.float64), np.asarray(tr.rotation, np.float64),
+                                          np.asarray(tr.scale, np.float64)]))
+            sm = sampled_meshes.get(o.object_id)
+            take = o.object_id in inc and sm is not None and sm.total_samples > 0
+            if sm is not None and len(sm.resolutions) == len(f):
+                res.append(np.asarray(sm.resolutions, np.int64))
+            else:
+                res.append(np.ones(len(f), np.int64))
+                take = False
+            flags.append(1 if take else 0)
+            if take:
+                self.slices[o.object_id] = (base, base + int(sm.total_samples))
+                base += int(sm.total_samples)
+        self.n_samples = base
+        self._keep = (np.ascontiguousarray(np.asarray(tri_counts, np.int64)),
+                      np.ascontiguousarray(np.concatenate(tris) if tris else np.zeros((0, 9))),
+                      np.ascontiguousarray(np.stack(xforms) if xforms else np.zeros((0, 10))),
+                      np.ascontiguousarray(np.concatenate(res) if res else np.zeros(0, np.int64)),
+                      np.ascontiguousarray(np.asarray(flags, np.uint8)))
+        tc, tl, xf, rs, fl = self._keep
+        _native.check(lib.gm_plan_set_scene(h, len(objs), _native.iptr(tc), _native.dptr(tl), _native.dptr(xf),
+                                            _native.iptr(rs), _native.u8ptr(fl)), "gm_plan_set_scene")
+        n = int(lib.gm_plan_num_samples(h))
+        if n != self.n_samples:
+            raise RuntimeError(f"plan sample count {n} != layout total {self.n_samples}")
+        self._keep = None
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                self._lib.gm_plan_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    # ----------------------------------------------------------------- ops
+    def accumulate(self, fixations, config: GenerationConfig, reset: bool = True, progress=None,
+                   timers: Timings | None = None, batch: int = 0) -> None:
+        """Add the fixations' contributions to the device values."""
+        table = fixation_table(fixations)
+        F = len(table)
+        cfg = _native.GmConfig(float(config.theta), float(config.epsilon_abs), float(config.epsilon_rel),
+                               int(config.zbuffer_resolution), int(bool(config.filtering_enabled)), int(batch), 0)
+        tm = _native.GmTimings()
+        bad = np.zeros(1, np.int64)
+        cb = _native.PROGRESS_FN(0)
+        if progress is not None:
+            state = {"n": 0}
+
+            def _cb(done, total, _user):
+                while state["n"] < done:
+                    state["n"] += 1
+                    progress(state["n"], total)
+
+            cb = _native.PROGRESS_FN(_cb)
+        rc = self._lib.gm_plan_accumulate(self._h, _native.dptr(table), F, ctypes.byref(cfg), int(bool(reset)),
+                                          ctypes.byref(tm), cb, None, _native.iptr(bad))
+        _native.check(rc, f"fixation {int(bad[0])}" if rc == _native.GM_ERR_INVALID_FRUSTUM else "gm_plan_accumulate")
+        self.last_timings = tm
+        if timers is not None:
+            timers.add("cull", tm.cull_ms / 1e3)
+            timers.add("rasterize", tm.rasterize_ms / 1e3)
+            timers.add("accumulate", tm.accumulate_ms / 1e3)
+            timers.add("setup", tm.setup_ms / 1e3)
+
+    def global_max(self) -> float:
+        out = np.zeros(1)
+        _native.check(self._lib.gm_plan_max(self._h, _native.dptr(out)), "gm_plan_max")
+        return float(out[0])
+
+    def read(self, normalized_by: float | None = None) -> np.ndarray:
+        out = np.empty(self.n_samples)
+        if normalized_by is None:
+            _native.check(self._lib.gm_plan_read(self._h, _native.dptr(out), None, 0.0), "gm_plan_read")
+        else:
+            _native.check(self._lib.gm_plan_read(self._h, None, _native.dptr(out), float(normalized_by)),
+                          "gm_plan_read")
+        return out
+
+    def write(self, values: np.ndarray) -> None:
+        v = np.ascontiguousarray(values, dtype=np.float64)
+        _native.check(self._lib.gm_plan_write(self._h, _native.dptr(v)), "gm_plan_write")
+
+    def values_device_ptr(self) -> int:
+        return int(self._lib.gm_plan_values_device(self._h) or 0)
+
+    def sync(self) -> None:
+        _native.check(self._lib.gm_plan_sync(self._h), "gm_plan_sync")
+
+    def split(self, flat: np.ndarray, sampled_meshes: dict) -> dict:
+        out = {}
+        for oid, sm in sampled_meshes.items():
+            if oid in self.slices:
+                a, b = self.slices[oid]
+                out[oid] = flat[a:b].copy()
+            else:
+                out[oid] = np.zeros(sm.total_samples)
+        return out
+
+    def gather(self, values: dict) -> np.ndarray:
+        flat = np.zeros(self.n_samples)
+        for oid, (a, b) in self.slices.items():
+            flat[a:b] = values[oid]
+        return flat
+
+    # ------------------------------------------------------- seam ports
+    def depth_buffer(self, fixation, config: GenerationConfig, cull: bool = False) -> np.ndarray:
+        """The (res, res) z-buffer kernels.rasterize produces for this fixation
+        (crop frustum when filtering, else full), evaluated on the GPU."""
+        row = fixation_table([fixation] if not isinstance(fixation, np.ndarray) else fixation[None, :])[0]
+        res = int(config.zbuffer_resolution)
+        out = np.empty((res, res))
+        _native.check(self._lib.gm_plan_depth_buffer(self._h, _native.dptr(np.ascontiguousarray(row)),
+                                                     float(config.theta), int(bool(config.filtering_enabled)), res,
+                                                     int(not cull), _native.dptr(out)), "gm_plan_depth_buffer")
+        return out
+
+    def candidates(self, fixations, config: GenerationConfig, cap: int | None = None) -> list:
+        """Per fixation, the sorted sample indices passing the NDC crop filter
+        (kernels.py:302-319), computed by warp-ballot compaction on the GPU."""
+        table = fixation_table(fixations)
+        F = len(table)
+        cap = self.n_samples if cap is None else cap
+        out = np.zeros((max(F, 1), max(cap, 1)), np.int64)
+        counts = np.zeros(max(F, 1), np.int64)
+        _native.check(self._lib.gm_plan_candidates(self._h, _native.dptr(table), F, float(config.theta),
+                                                   int(bool(config.filtering_enabled)),
+                                                   int(config.zbuffer_resolution), _native.iptr(out), max(cap, 1),
+                                                   _native.iptr(counts)), "gm_plan_candidates")
+        return [np.sort(out[f, :min(int(counts[f]), cap)]) for f in range(F)]
+
+    def positions(self) -> np.ndarray:
+        out = np.empty((self.n_samples, 3))
+        _native.check(self._lib.gm_plan_positions(self._h, _native.dptr(out)), "gm_plan_positions")
+        return out
+
+
+_PLANS: dict = {}
+_PLAN_LIMIT = 4
+
+
+def get_plan(scene, sampled_meshes: dict, config: GenerationConfig, device: int = 0) -> ScenePlan:
+    """Cached ScenePlan for (scene, layout, include list, device)."""
+    included = _included_ids(scene, config)
+    for oid in included:
+        if oid not in sampled_meshes:
+            raise KeyError(oid)
+    key = (id(scene), id(sampled_meshes), tuple(included), device,
+           tuple((oid, int(sm.total_samples)) for oid, sm in sampled_meshes.items()))
+    plan = _PLANS.get(key)
+    if plan is not None and plan.scene is scene and plan.sampled_meshes is sampled_meshes:
+        return plan
+    plan = ScenePlan(scene, sampled_meshes, included, device)
+    if len(_PLANS) >= _PLAN_LIMIT:
+        _PLANS.pop(next(iter(_PLANS)))
+    _PLANS[key] = plan
+    return plan
+
+
+def _reject_overrides(fixations) -> None:
+    if isinstance(fixations, np.ndarray):
+        return
+    for f in fixations:
+        if getattr(f, "overrides", None):
+            raise NotImplementedError(
+                "per-fixation pose overrides (dynamic scenes) are not supported by the B200 path yet; "
+                "there is no CPU fallback")
+
+
+def generate(scene, sampled_meshes: dict, fixations, config: GenerationConfig, workers: int | None = None,
+             progress=None, timers: Timings | None = None, device: int = 0, batch: int = 0) -> DensityMap:
+    """All fixations, in log order, into a fresh un-normalized map.
+
+    `fixations` is a list of Fixation objects (this package's or the
+    reference's) or an (F, 18) table in fixation-log column order.  `workers`
+    is accepted for API compatibility; the GPU result does not depend on it.
+    """
+    config.validate()
+    _reject_overrides(fixations)
+    plan = get_plan(scene, sampled_meshes, config, device)
+    table = fixation_table(fixations)
+    plan.accumulate(table, config, reset=True, progress=progress, timers=timers, batch=batch)
+    gmax = plan.global_max() if len(table) else 0.0
+    values = plan.split(plan.read(), sampled_meshes)
+    return DensityMap(values, global_max=gmax, normalized=False)
+
+
+def accumulate_fixation(dmap: DensityMap, scene, sampled_meshes: dict, fixation, config: GenerationConfig,
+                        cache=None, timers: Timings | None = None, device: int = 0) -> DensityMap:
+    """Add one fixation to `dmap` in place (running max updated), return it."""
+    _reject_overrides([fixation])
+    plan = cache if isinstance(cache, ScenePlan) else get_plan(scene, sampled_meshes, config, device)
+    plan.write(plan.gather(dmap.values))
+    plan.accumulate([fixation], config, reset=False, timers=timers)
+    flat = plan.read()
+    running = dmap.global_max
+    for oid, (a, b) in plan.slices.items():
+        dmap.values[oid][...] = flat[a:b]
+        if b > a:
+            running = max(running, float(flat[a:b].max()))
+    dmap.global_max = running
+    return dmap
+
+
+def normalize(dmap: DensityMap, timers: Timings | None = None, device: int = 0) -> DensityMap:
+    """values / global_max on the GPU into a new map; idempotent, zero-safe."""
+    t0 = time.perf_counter()
+    if dmap.normalized or dmap.global_max <= 0.0:
+        out = dmap.copy()
+        out.normalized = True
+    else:
+        keys = list(dmap.values)
+        flat = np.ascontiguousarray(np.concatenate([np.asarray(dmap.values[k], np.float64) for k in keys])
+                                    if keys else np.zeros(0))
+        res = np.empty_like(flat)
+        if len(flat):
+            lib = _native.load()
+            _native.check(lib.gm_normalize(device, _native.dptr(flat), len(flat), float(dmap.global_max),
+                                           _native.dptr(res)), "gm_normalize")
+        vals, o = {}, 0
+        for k in keys:
+            n = len(dmap.values[k])
+            vals[k] = res[o:o + n]
+            o += n
+        out = DensityMap(vals, global_max=1.0, normalized=True)
+    if timers is not None:
+        timers.add("normalize", time.perf_counter() - t0)
+    return out

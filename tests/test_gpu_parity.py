@@ -1,0 +1,182 @@
+"""CUDA path vs the reference's golden outputs and vs the CPU oracle.
+
+Bar (north_star): sample layout, per-fixation setup, z-buffers and filter
+index sets bit-exact; density values within 1e-5 relative / 1e-7 absolute
+(we assert the much tighter rtol 1e-12: the only non-bit-exact operation is
+CUDA's exp() vs glibc's, <= 1 ulp) with the set of contributing samples
+identical.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+import paper_2601_07571_b200 as gm
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-12  # assert_allclose(rtol) on density values; the spec bar is 1e-5 / 1e-7
+
+
+def _assert_values(got, want):
+    assert got.shape == want.shape
+    np.testing.assert_array_equal(got != 0.0, want != 0.0)  # identical contributing set
+    np.testing.assert_allclose(got, want, rtol=RTOL, atol=0.0)
+
+
+# ------------------------------------------------------------- stage 1
+
+@pytest.mark.parametrize("k", [1000, 6000])
+def test_layout_positions_vs_golden(golden, k):
+    scene = golden.scene("lay_")
+    sm = gm.build_sampled_meshes(scene, float(k))
+    for i, obj in enumerate(scene.objects):
+        tag = f"lay_k{k}_{i}_"
+        s = sm[obj.object_id]
+        np.testing.assert_array_equal(s.resolutions, golden[tag + "res"])
+        np.testing.assert_array_equal(s.offsets, golden[tag + "off"])
+        np.testing.assert_array_equal(s.counts, np.diff(np.append(s.offsets, s.total_samples)))
+        assert s.total_samples == int(golden[tag + "total"])
+        world = gm.sample_positions_local(obj.mesh, s, transform=obj.transform)
+        np.testing.assert_array_equal(world, golden[tag + "world"])
+
+
+def test_layout_random_triangles_vs_oracle():
+    rng = np.random.default_rng(7)
+    tris = rng.normal(size=(50_000, 3, 3)) * rng.uniform(1e-3, 0.8, size=(50_000, 1, 1))
+    tris[:5] = 0.0  # degenerate triangles -> r = 1
+    mesh = gm.Mesh(tris.reshape(-1, 3), np.arange(150_000).reshape(-1, 3))
+    for k in (1.0, 1000.0, 40000.0, 123456.7):
+        s = gm.build_sampled_mesh(mesh, k)
+        res, cnt, off, total = O.layout(tris, k)
+        np.testing.assert_array_equal(s.resolutions, res)
+        np.testing.assert_array_equal(s.offsets, off)
+        assert s.total_samples == total
+    s = gm.build_sampled_mesh(mesh, 3000.0)
+    loc = gm.sample_positions_local(mesh, s)
+    res, cnt, off, total = O.layout(tris, 3000.0)
+    np.testing.assert_array_equal(loc, O.positions_local(tris, res, cnt, off, total))
+
+
+def test_layout_edge_cases():
+    empty = gm.build_sampled_mesh(gm.Mesh(np.zeros((0, 3)), np.zeros((0, 3))), 10.0)
+    assert empty.total_samples == 0 and len(empty.offsets) == 0
+    tiny = gm.build_sampled_mesh(gm.Mesh(np.eye(3) * 1e-3, [[0, 1, 2]]), 1.0)
+    assert tiny.total_samples == 3
+    import workloads as W
+
+    cube = gm.build_sampled_mesh(W.box(0.001), 1.0)
+    assert cube.total_samples == 36
+    # (0.5, 6) -> 1 ; (0.01, 10000) -> 13 (reference KATs, test_geometry.py:47-57)
+    a = np.array([[0, 0, 0], [1.0, 0, 0], [0, 1.0, 0]])  # area 0.5
+    assert gm.build_sampled_mesh(gm.Mesh(a, [[0, 1, 2]]), 6.0).resolutions[0] == 1
+    s = math.sqrt(0.02)
+    b = np.array([[0, 0, 0], [s, 0, 0], [0, s, 0]])  # area 0.01
+    assert gm.build_sampled_mesh(gm.Mesh(b, [[0, 1, 2]]), 10000.0).resolutions[0] == 13
+    with pytest.raises(gm.ConfigError):
+        gm.build_sampled_mesh(gm.Mesh(a, [[0, 1, 2]]), 0.0)
+
+
+# ------------------------------------------------------- per-fixation setup
+
+def test_fixation_setup_vs_golden(golden):
+    S = gm.gaze.SETUP_FIELDS
+    out = gm.fixation_setup(golden["setup_fix"], float(golden["setup_theta"]), True)
+    want = golden["setup_out"]
+    got = np.column_stack([out[:, S["rot"]], out[:, S["trans"]], out[:, S["p00"]], out[:, S["p11"]],
+                           out[:, S["p02"]], out[:, S["p12"]], out[:, S["near"]], out[:, S["far"]],
+                           out[:, S["cropped"]], out[:, S["amp"]]])
+    np.testing.assert_array_equal(got, want)
+
+
+def test_invalid_frustum_raises():
+    row = np.array([0, 1, 0, 0, 0, 0, 0, 0, 1, 0.1, -0.1, 0.1, -0.1, 0.1, 100, 0, 0, -1.0])  # l > r
+    with pytest.raises(gm.InvalidFrustumError):
+        gm.fixation_setup(row[None, :], math.radians(1.0), False)
+
+
+# ------------------------------------------------------------- z-buffer
+
+def test_depth_buffers_vs_golden(golden):
+    for i in range(int(golden["ras_count"])):
+        scene = golden.scene(f"ras_{golden[f'ras{i}_scene']}_")
+        want = golden[f"ras{i}_depth"]
+        cfg = gm.GenerationConfig(k=100.0, zbuffer_resolution=want.shape[0],
+                                  filtering_enabled=bool(golden[f"ras{i}_crop"]))
+        plan = gm.ScenePlan(scene, gm.build_sampled_meshes(scene, 100.0), scene.object_ids)
+        got = plan.depth_buffer(golden[f"ras{i}_fix"], cfg)
+        np.testing.assert_array_equal(got, want)
+
+
+def test_depth_buffers_vs_oracle_random():
+    import workloads as W
+
+    scene = W.rotated_object_scene()
+    plan = gm.ScenePlan(scene, gm.build_sampled_meshes(scene, 100.0), scene.object_ids)
+    tris = O.scene_world_triangles(scene)
+    fx = W.orbit_fixations(12, 21, 1.5, 4.0, jitter=0.4, max_tilt=0.6)
+    for j, row in enumerate(fx):
+        for crop, res in ((True, 64 + 37 * j), (False, 128)):
+            cfg = gm.GenerationConfig(zbuffer_resolution=res, filtering_enabled=crop)
+            s = O.fixation_setup(row, cfg.theta, crop)
+            want = O.rasterize(tris, s[O.FS_ROT:O.FS_ROT + 9], s[O.FS_TRANS:O.FS_TRANS + 3], s[O.FS_P00],
+                               s[O.FS_P11], s[O.FS_P02], s[O.FS_P12], res, res, s[O.FS_NEAR], s[O.FS_FAR])
+            np.testing.assert_array_equal(plan.depth_buffer(row, cfg), want)
+
+
+# ----------------------------------------------------------------- filter
+
+def test_candidates_vs_golden(golden):
+    scene = golden.scene("fil_")
+    k = float(golden["fil_k"])
+    plan = gm.ScenePlan(scene, gm.build_sampled_meshes(scene, k), scene.object_ids)
+    got = plan.candidates(golden["fil_fix"], gm.GenerationConfig(k=k))
+    for j, idx in enumerate(got):
+        np.testing.assert_array_equal(idx, golden[f"fil{j}_idx"])
+
+
+def test_candidates_vs_oracle_unfiltered():
+    import workloads as W
+
+    scene, k, fx = W.c1()
+    plan = gm.ScenePlan(scene, gm.build_sampled_meshes(scene, k), scene.object_ids)
+    pos = plan.positions()
+    cfg = gm.GenerationConfig(k=k, filtering_enabled=False)
+    got = plan.candidates(fx[:20], cfg)
+    for row, idx in zip(fx[:20], got):
+        np.testing.assert_array_equal(idx, O.candidates(pos, O.fixation_setup(row, cfg.theta, False)))
+
+
+# ------------------------------------------------------------- generate
+
+@pytest.mark.parametrize("case", ["c1", "sib_off", "chal_on", "quads_incl"])
+def test_generate_vs_golden(golden, case):
+    p = f"gen_{case}_"
+    scene = golden.scene(p)
+    incl = [str(x) for x in golden[p + "incl"]] or None
+    cfg = gm.GenerationConfig(k=float(golden[p + "k"]), zbuffer_resolution=int(golden[p + "res"]),
+                              filtering_enabled=bool(golden[p + "filt"]),
+                              object_include_list=set(incl) if incl else None)
+    sm = gm.build_sampled_meshes(scene, cfg.k)
+    dm = gm.generate(scene, sm, golden[p + "fix"], cfg)
+    assert dm.global_max == pytest.approx(float(golden[p + "gmax"]), rel=RTOL)
+    for i, obj in enumerate(scene.objects):
+        _assert_values(dm.values[obj.object_id], golden[f"{p}val{i}"])
+
+
+@pytest.mark.parametrize("filtering,res,batch", [(True, 512, 0), (False, 512, 7), (True, 77, 3), (False, 1, 0)])
+def test_generate_vs_oracle(filtering, res, batch):
+    import workloads as W
+
+    scene = W.rotated_object_scene()
+    fx = W.orbit_fixations(40, 5, 1.2, 4.0, jitter=0.5, max_tilt=0.3)
+    cfg = gm.GenerationConfig(k=3000.0, filtering_enabled=filtering, zbuffer_resolution=res)
+    sm = gm.build_sampled_meshes(scene, cfg.k)
+    dm = gm.generate(scene, sm, fx, cfg, batch=batch)
+    vals, gmax = O.generate(scene, O.rows_as_fixations(fx), k=cfg.k, zbuffer_resolution=res, filtering_enabled=filtering)
+    assert dm.global_max == pytest.approx(gmax, rel=RTOL)
+    for oid in vals:
+        _assert_values(dm.values[oid], vals[oid])
+    assert gmax > 0
