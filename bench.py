@@ -202,7 +202,6 @@ def run_ours(args, rank, world):
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
         dist.init_process_group("nccl")
     device = int(os.environ.get("LOCAL_RANK", 0)) if world > 1 else 0
-    if world > 1:
 
     scene, k, fx, filtering, desc = workload(args.config, args.fixations, rank)
     cfg = gm.GenerationConfig(k=k, filtering_enabled=filtering)
@@ -262,7 +261,9 @@ def run_ours(args, rank, world):
     value = world * N * F / (step_ms / 1e3)
     tm = tms[-1]
     acc_ms = tm.accumulate_ms
-    launches = int(tm.batches) * 6 + 1
+    # per step: k_set_i64; per batch: k_tri_setup, k_samples<mark>, k_texels, k_samples<accumulate>;
+    # then k_max
+    launches = int(tm.batches) * 4 + 2
 
     # ---- e2e through the public API (host table in, host values out) -----
     e2e = None
@@ -276,7 +277,7 @@ def run_ours(args, rank, world):
             e_times.append(time.perf_counter() - t0)
         e_t = float(np.mean(e_times))
         e2e = {"value": world * N * F / e_t if world == 1 else None, "unit": UNIT,
-               "h2d_bytes_per_step": int(F * (224 + 80)), "d2h_bytes_per_step": int(N * 8),
+               "h2d_bytes_per_step": int(F * (208 + 80)), "d2h_bytes_per_step": int(N * 8),
                "ms_per_step": e_t * 1e3, "path": "paper_2601_07571_b200.generate (fixation table -> values dict)"}
         if world > 1:
             import torch
@@ -320,8 +321,9 @@ def run_ours(args, rank, world):
                        "l2": "flushed (512 MiB write) before every timed step",
                        "timing": "CUDA events on the plan stream around each full generation (+ all-reduce)"},
             "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "clocks": clk.summary(), "gpu_launches": launches,
-            "phases_ms": {"cull": tm.cull_ms, "bin": tm.rasterize_ms, "accumulate": tm.accumulate_ms,
-                          "batches": tm.batches, "screen_tris": tm.screen_tris, "bin_items": tm.bin_items},
+            "phases_ms": {"cull": tm.cull_ms, "mark": tm.mark_ms, "texels": tm.texel_ms,
+                          "accumulate": tm.accumulate_ms, "batches": tm.batches, "retries": tm.retries,
+                          "screen_tris": tm.screen_tris},
             "global_max": gmax,
         }
         print(json.dumps(line), flush=True)

@@ -50,8 +50,17 @@ typedef struct GmConfig {
 
 /* Timings.phases (density.py:94-103), measured with CUDA events. */
 typedef struct GmTimings {
-    double setup_ms, cull_ms, rasterize_ms, accumulate_ms, total_ms;
-    int64_t screen_tris, bin_items, batches;
+    double setup_ms;      /* host fixation setup */
+    double cull_ms;       /* occluder cull + clip + projection */
+    double rasterize_ms;  /* screen binning */
+    double accumulate_ms; /* NDC filter + cone + depth test + Gaussian */
+    double total_ms;      /* whole call, wall */
+    double mark_ms;       /* candidate texel marking */
+    double texel_ms;      /* z-buffer values of the marked texels */
+    int64_t screen_tris;  /* projected triangles produced */
+    int64_t bin_items;    /* reserved */
+    int64_t batches;
+    int64_t retries;      /* passes resumed after a screen-triangle segment overflow */
 } GmTimings;
 
 typedef struct gm_plan gm_plan;
@@ -82,7 +91,7 @@ int gm_normalize(int device, const double* values, int64_t n, double gmax, doubl
 
 /* Fixation.view_matrix (gaze.py:114-122), build_crop_frustum (gaze.py:372-381)
  * with the GazeOutsideFrustumError fallback of density.py:152-158,
- * frustum_from_matrix (gaze.py:345-356).  ex: F x 28 float64 (GmFixExact in
+ * frustum_from_matrix (gaze.py:345-356).  ex: F x 26 float64 (GmFixExact in
  * csrc/gm_types.h), cull: F x 20 float32 or NULL. */
 int gm_fixation_setup(const double* fixations, int64_t F, double theta, int filtering, int res, double* ex,
                       void* cull, int64_t* bad_fixation);

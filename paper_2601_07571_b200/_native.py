@@ -36,12 +36,13 @@ class GmConfig(ctypes.Structure):
 
 class GmTimings(ctypes.Structure):
     _fields_ = [("setup_ms", ctypes.c_double), ("cull_ms", ctypes.c_double), ("rasterize_ms", ctypes.c_double),
-                ("accumulate_ms", ctypes.c_double), ("total_ms", ctypes.c_double),
-                ("screen_tris", ctypes.c_int64), ("bin_items", ctypes.c_int64), ("batches", ctypes.c_int64)]
+                ("accumulate_ms", ctypes.c_double), ("total_ms", ctypes.c_double), ("mark_ms", ctypes.c_double),
+                ("texel_ms", ctypes.c_double), ("screen_tris", ctypes.c_int64), ("bin_items", ctypes.c_int64),
+                ("batches", ctypes.c_int64), ("retries", ctypes.c_int64)]
 
 
-# GmFixExact is 28 float64 (gm_types.h); GmFixCull 20 float32
-FIX_EXACT_DOUBLES = 28
+# GmFixExact is 26 float64 (gm_types.h); GmFixCull 20 float32
+FIX_EXACT_DOUBLES = 26
 FIX_CULL_FLOATS = 20
 
 PROGRESS_FN = ctypes.CFUNCTYPE(None, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p)

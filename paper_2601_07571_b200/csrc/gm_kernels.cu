@@ -6,13 +6,15 @@
 //          transform like OpenBLAS), k_world_tris
 //   a8-a10 per-fixation setup: host, gm_setup.cpp (glibc trig, bit-exact)
 //   a11-a12 occluders: k_tri_setup (conservative cone cull, exact camera
-//          transform + near clip + projection + _raster_tri setup) and
-//          k_bin_count / k_bin_fill (16x16-pixel screen bins)
-//   a13-a15 k_accumulate: sample-major, one warp per 32-sample chunk, fixation
-//          culling by warp ballot, exact NDC filter, exact 4-sigma Gaussian,
-//          and depth_match evaluated on the texels it reads (the z-buffer
-//          value of a texel = min over the binned screen triangles covering
-//          it, computed with the reference's own pixel arithmetic)
+//          transform + near clip + projection + _raster_tri setup) into
+//          per-fixation screen-triangle segments
+//   a13-a15 k_samples<true>: sample-major, one warp per 32-sample chunk,
+//          fixation culling by warp ballot, exact NDC filter + 4-sigma cone,
+//          marks the <= 9 texels depth_match will read;
+//          k_texels: fixation-major per 64x64 tile, evaluates only marked
+//          texels (min over covering screen triangles, reference pixel
+//          arithmetic) from shared-memory sub-bins;
+//          k_samples<false>: depth_match + Gaussian, accumulated in log order
 //   a16    k_max / k_normalize
 // Exactness: compiled with -fmad=false; see gm_device.cuh.
 #include <cub/cub.cuh>
@@ -23,6 +25,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <climits>
 #include <chrono>
 #include <string>
 #include <thread>
@@ -217,15 +220,31 @@ __global__ void k_group_spheres(const float4* __restrict__ member, const double*
 
 // ------------------------------------------------------ occluder setup
 
+// Per-batch screen-triangle store: fixation slot f owns the segment
+// [f * cap_seg, (f + 1) * cap_seg) of `tris` (records) and `bbox` (their
+// inclusive pixel boxes, packed x0 | x1 << 16, y0 | y1 << 16, scanned by
+// k_texels); count[f] is the number appended.  Overflow never corrupts a
+// result: the first batch that overflows sets *fail (sticky) and every later
+// kernel of that and following batches returns immediately; the host grows
+// the segments and resumes from that batch (log order is preserved).
+struct TriStore {
+    GmScreenTri* tris;
+    uint2* bbox;
+    int* count;
+    int64_t cap_seg;
+    long long* fail;     // first failed batch start, LLONG_MAX if none
+    int* max_count;      // largest per-fixation count seen (for regrowth)
+    unsigned long long* total;  // screen triangles produced (statistics)
+};
+
 // One warp per group of 32 triangle clusters (32 triangles each); blockIdx.y =
 // fixation slot.  Lane-parallel cluster test -> ballot -> per passing cluster
 // lane = triangle: sphere test, exact projection, warp-aggregated append.
 __global__ void __launch_bounds__(256) k_tri_setup(const double* __restrict__ tw, int64_t T,
                                                    const float4* __restrict__ tsph, const float4* __restrict__ csph,
                                                    int64_t n_clu, const GmFixExact* __restrict__ fixes,
-                                                   const GmFixCull* __restrict__ culls, int W, int H,
-                                                   GmScreenTri* __restrict__ pool, int64_t cap,
-                                                   unsigned long long* __restrict__ counter) {
+                                                   const GmFixCull* __restrict__ culls, int W, int H, TriStore ts,
+                                                   long long b0) {
     const int f = blockIdx.y;
     const int lane = threadIdx.x & 31;
     const int64_t group = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -237,16 +256,15 @@ __global__ void __launch_bounds__(256) k_tri_setup(const double* __restrict__ tw
     unsigned mask = __ballot_sync(0xffffffffu, pass);
     if (!mask) return;
     const GmFixExact& F = fixes[f];
+    GmScreenTri* seg = ts.tris + (int64_t)f * ts.cap_seg;
+    uint2* segb = ts.bbox + (int64_t)f * ts.cap_seg;
     while (mask) {
         int j = __ffs(mask) - 1;
         mask &= mask - 1;
         int64_t t = (c0 + j) * 32 + lane;
         GmScreenTri out[2];
         int n = 0;
-        if (t < T && sphere_visible(cull, tsph[t], true)) {
-            n = project_triangle(tw + 9 * t, F, W, H, out);
-        }
-        // warp-aggregated append
+        if (t < T && sphere_visible(cull, tsph[t], true)) n = project_triangle(tw + 9 * t, F, W, H, out);
         int incl = n;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -255,113 +273,41 @@ __global__ void __launch_bounds__(256) k_tri_setup(const double* __restrict__ tw
         }
         int total = __shfl_sync(0xffffffffu, incl, 31);
         if (total == 0) continue;
-        unsigned long long base = 0;
-        if (lane == 31) base = atomicAdd(counter, (unsigned long long)total);
+        int base = 0;
+        if (lane == 31) {
+            atomicAdd(ts.total, (unsigned long long)total);
+            base = atomicAdd(ts.count + f, total);
+            if (base + total > ts.cap_seg) {
+                atomicMin(ts.fail, b0);
+                atomicMax(ts.max_count, base + total);
+            }
+        }
         base = __shfl_sync(0xffffffffu, base, 31);
-        unsigned long long at = base + (unsigned long long)(incl - n);
+        int at = base + (incl - n);
         for (int q = 0; q < n; q++) {
-            if (at + q < (unsigned long long)cap) {
+            if (at + q < ts.cap_seg) {
                 out[q].fslot = f;
-                pool[at + q] = out[q];
+                seg[at + q] = out[q];
+                segb[at + q] = make_uint2((uint32_t)out[q].x0 | ((uint32_t)out[q].x1 << 16),
+                                          (uint32_t)out[q].y0 | ((uint32_t)out[q].y1 << 16));
             }
         }
     }
 }
 
-__global__ void k_bin_count(const GmScreenTri* __restrict__ pool, const unsigned long long* __restrict__ counter,
-                            int64_t cap, int nbx, int nbins, int* __restrict__ bin_count) {
-    int64_t n = (int64_t)min(*counter, (unsigned long long)cap);
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const GmScreenTri& t = pool[i];
-        int bx0 = t.x0 >> GM_BIN_SHIFT, bx1 = t.x1 >> GM_BIN_SHIFT;
-        int by0 = t.y0 >> GM_BIN_SHIFT, by1 = t.y1 >> GM_BIN_SHIFT;
-        int* base = bin_count + (int64_t)t.fslot * nbins;
-        for (int by = by0; by <= by1; by++)
-            for (int bx = bx0; bx <= bx1; bx++) atomicAdd(base + by * nbx + bx, 1);
-    }
-}
+// ------------------------------------------------------ the hot kernels
 
-__global__ void k_bin_fill(const GmScreenTri* __restrict__ pool, const unsigned long long* __restrict__ counter,
-                           int64_t cap, int nbx, int nbins, int* __restrict__ cursor, int* __restrict__ items,
-                           int64_t cap_items) {
-    int64_t n = (int64_t)min(*counter, (unsigned long long)cap);
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const GmScreenTri& t = pool[i];
-        int bx0 = t.x0 >> GM_BIN_SHIFT, bx1 = t.x1 >> GM_BIN_SHIFT;
-        int by0 = t.y0 >> GM_BIN_SHIFT, by1 = t.y1 >> GM_BIN_SHIFT;
-        int* base = cursor + (int64_t)t.fslot * nbins;
-        for (int by = by0; by <= by1; by++)
-            for (int bx = bx0; bx <= bx1; bx++) {
-                int at = atomicAdd(base + by * nbx + bx, 1);
-                if (at < cap_items) items[at] = (int)i;
-            }
-    }
-}
-
-// ----------------------------------------------------- texel evaluation
-
-struct BinView {
-    const GmScreenTri* tris;
-    const int* off;   // exclusive offsets, length nbins*B + 1
-    const int* items;
-    int nbx, nbins;
+// Per-batch z-buffer store: only the texels some candidate's depth_match will
+// read are ever written (mask bit set by k_samples<true>, value by k_texels).
+struct DepthView {
+    double* depth;    // [B][H][W]
+    uint32_t* mask;   // [B][H][wwords]
+    int W, H, wwords;
 };
 
-// Min depth of the texel block [bx0, bx0+nx) x [by0, by0+ny) (nx, ny <= 3),
-// i.e. the z-buffer values kernels.rasterize would leave there, evaluated only
-// for these texels.  T[ry*3+rx].
-__device__ __forceinline__ void eval_block(const BinView& bv, int fslot, int bx0, int by0, int nx, int ny,
-                                           double near_, double far_, double T[9]) {
-#pragma unroll
-    for (int q = 0; q < 9; q++) T[q] = CUDART_INF;
-    const int bxa = bx0 >> GM_BIN_SHIFT, bxb = (bx0 + nx - 1) >> GM_BIN_SHIFT;
-    const int bya = by0 >> GM_BIN_SHIFT, byb = (by0 + ny - 1) >> GM_BIN_SHIFT;
-    const int64_t fb = (int64_t)fslot * bv.nbins;
-    for (int biy = bya; biy <= byb; biy++) {
-        for (int bix = bxa; bix <= bxb; bix++) {
-            // texels of the block that belong to this bin
-            int tx_lo = max(bx0, bix << GM_BIN_SHIFT), tx_hi = min(bx0 + nx - 1, (bix << GM_BIN_SHIFT) + GM_BIN - 1);
-            int ty_lo = max(by0, biy << GM_BIN_SHIFT), ty_hi = min(by0 + ny - 1, (biy << GM_BIN_SHIFT) + GM_BIN - 1);
-            int64_t b = fb + biy * bv.nbx + bix;
-            int s = bv.off[b], e = bv.off[b + 1];
-            for (int it = s; it < e; it++) {
-                const GmScreenTri* tp = bv.tris + bv.items[it];
-                uint2 bb = *reinterpret_cast<const uint2*>(&tp->x0);  // x0,x1,y0,y1 (uint16 x4)
-                int x0 = bb.x & 0xffff, x1 = bb.x >> 16, y0 = bb.y & 0xffff, y1 = bb.y >> 16;
-                int lx = max(tx_lo, x0), hx = min(tx_hi, x1);
-                int ly = max(ty_lo, y0), hy = min(ty_hi, y1);
-                if (lx > hx || ly > hy) continue;
-                GmScreenTri tri = *tp;
-#pragma unroll
-                for (int ry = 0; ry < 3; ry++) {
-#pragma unroll
-                    for (int rx = 0; rx < 3; rx++) {
-                        int px = bx0 + rx, py = by0 + ry;
-                        if (px >= lx && px <= hx && py >= ly && py <= hy) {
-                            double d = texel_depth(tri, px, py, near_, far_);
-                            if (d < T[ry * 3 + rx]) T[ry * 3 + rx] = d;
-                        }
-                    }
-                }
-            }
-        }
-    }
-}
-
-// kernels.py:219-285 depth_match, reading texels from the evaluated block.
-__device__ __forceinline__ bool depth_match_eval(const BinView& bv, int fslot, int W, int H, double fx, double fy,
-                                                 double d, double eps, double near_, double far_) {
-    double gx = fx - 0.5, gy = fy - 0.5;
-    long long cx = x86_i64(rint(gx));  // np.round: half to even
-    if (cx < 0) cx = 0;
-    else if (cx > W - 1) cx = W - 1;
-    long long cy = x86_i64(rint(gy));
-    if (cy < 0) cy = 0;
-    else if (cy > H - 1) cy = H - 1;
-    int bx0 = (int)max(cx - 1, 0LL), bx1 = (int)min(cx + 1, (long long)W - 1);
-    int by0 = (int)max(cy - 1, 0LL), by1 = (int)min(cy + 1, (long long)H - 1);
-    double T[9];
-    eval_block(bv, fslot, bx0, by0, bx1 - bx0 + 1, by1 - by0 + 1, near_, far_, T);
+// kernels.py:219-285 depth_match on texels that k_texels evaluated.
+__device__ __forceinline__ bool depth_match_tex(const double* __restrict__ dep, int W, int H, double gx, double gy,
+                                                int bx0, int bx1, int by0, int by1, double d, double eps) {
     if (W > 1 && H > 1) {
         long long x0 = x86_i64(floor(gx));
         if (x0 < 0) x0 = 0;
@@ -369,9 +315,8 @@ __device__ __forceinline__ bool depth_match_eval(const BinView& bv, int fslot, i
         long long y0 = x86_i64(floor(gy));
         if (y0 < 0) y0 = 0;
         else if (y0 > H - 2) y0 = H - 2;
-        int ix = (int)(x0 - bx0), iy = (int)(y0 - by0);  // quad inside the 3x3 block
-        double q00 = T[iy * 3 + ix], q01 = T[iy * 3 + ix + 1];
-        double q10 = T[(iy + 1) * 3 + ix], q11 = T[(iy + 1) * 3 + ix + 1];
+        const double* r0 = dep + (int64_t)y0 * W + x0;
+        double q00 = r0[0], q01 = r0[1], q10 = r0[W], q11 = r0[W + 1];
         if (isfinite(q00) && isfinite(q01) && isfinite(q10) && isfinite(q11)) {
             double tx = gx - (double)x0;
             if (tx < 0.0) tx = 0.0;
@@ -388,40 +333,43 @@ __device__ __forceinline__ bool depth_match_eval(const BinView& bv, int fslot, i
         }
     }
     double best = CUDART_INF;
-#pragma unroll
-    for (int ry = 0; ry < 3; ry++)
-#pragma unroll
-        for (int rx = 0; rx < 3; rx++) {
-            if (rx <= bx1 - bx0 && ry <= by1 - by0) {
-                double t = T[ry * 3 + rx];
-                if (isfinite(t)) {
-                    double diff = fabs(t - d);
-                    if (diff < best) best = diff;
-                }
+    for (int yy = by0; yy <= by1; yy++) {
+        const double* row = dep + (int64_t)yy * W;
+        for (int xx = bx0; xx <= bx1; xx++) {
+            double t = row[xx];
+            if (isfinite(t)) {
+                double diff = fabs(t - d);
+                if (diff < best) best = diff;
             }
         }
+    }
     return best <= eps;
 }
 
-// ------------------------------------------------------ the hot kernel
-
-// Sample-major fused filter + visibility + Gaussian (kernels.py:288-340 for a
-// batch of fixations).  A warp owns 32 consecutive samples (one value slot per
-// lane, kept in a register across the batch); lane l first tests fixation g+l
-// against the chunk sphere, the ballot gives the fixations that can touch the
-// chunk, and those are applied in log order -> per-sample accumulation order is
-// the reference's (density.py:223-226), deterministic, no atomics.
-// The cone test (kernels.py:330-339) is evaluated before depth_match
-// (kernels.py:326): all conditions are conjunctive and side-effect free, so the
-// set of contributing samples and their weights are unchanged.
-__global__ void __launch_bounds__(256) k_accumulate(const double* __restrict__ px, const double* __restrict__ py,
-                                                    const double* __restrict__ pz, const float4* __restrict__ chunks,
-                                                    int64_t N, int64_t n_chunks, const GmFixExact* __restrict__ fixes,
-                                                    const GmFixCull* __restrict__ culls, int B, BinView bv, int W,
-                                                    int H, double inv_sigma, double eps_abs, double eps_rel,
-                                                    double* __restrict__ values) {
+// Sample-major pass over a batch of fixations (kernels.py:288-340).  A warp
+// owns 32 consecutive samples; lane l tests fixation g+l against the chunk
+// sphere, the ballot gives the fixations that can touch the chunk, and those
+// are applied in log order.
+//   MARK = true : set the mask bits of the 3x3 texel block depth_match reads
+//                 for every candidate that passes the NDC filter and the cone.
+//   MARK = false: depth_match on those texels and accumulate; the value slot
+//                 lives in a register, so per-sample accumulation order is the
+//                 reference's (density.py:223-226): deterministic, no atomics.
+// The cone test (kernels.py:330-339) runs before depth_match (:326): every
+// condition is conjunctive and side-effect free, so the contributing set and
+// the weights are unchanged.
+template <bool MARK>
+__global__ void __launch_bounds__(256) k_samples(const double* __restrict__ px, const double* __restrict__ py,
+                                                 const double* __restrict__ pz, const float4* __restrict__ chunks,
+                                                 int64_t N, int64_t n_chunks, const GmFixExact* __restrict__ fixes,
+                                                 const GmFixCull* __restrict__ culls, int B, DepthView dv,
+                                                 double inv_sigma, double eps_abs, double eps_rel,
+                                                 double* __restrict__ values, const long long* __restrict__ fail,
+                                                 long long b0) {
+    if (*fail <= b0) return;  // this batch overflowed the triangle store: the host redoes it
     const int lane = threadIdx.x & 31;
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const int W = dv.W, H = dv.H;
     const double Wd = (double)W, Hd = (double)H;
     const double lo = -1.0 - GM_NDC_SLACK, hi = 1.0 + GM_NDC_SLACK;
     for (int64_t ch = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); ch < n_chunks; ch += warps) {
@@ -432,7 +380,7 @@ __global__ void __launch_bounds__(256) k_accumulate(const double* __restrict__ p
             wx = px[i];
             wy = py[i];
             wz = pz[i];
-            v = values[i];
+            if (!MARK) v = values[i];
         }
         const float4 sph = chunks[ch];
         for (int g = 0; g < B; g += 32) {
@@ -443,7 +391,8 @@ __global__ void __launch_bounds__(256) k_accumulate(const double* __restrict__ p
                 const int j = __ffs(mask) - 1;
                 mask &= mask - 1;
                 if (!valid) continue;
-                const GmFixExact& F = fixes[g + j];
+                const int f = g + j;
+                const GmFixExact& F = fixes[f];
                 // kernels.py:305-319
                 double x = F.rot[0] * wx + F.rot[1] * wy + F.rot[2] * wz + F.trans[0];
                 double y = F.rot[3] * wx + F.rot[4] * wy + F.rot[5] * wz + F.trans[1];
@@ -463,28 +412,192 @@ __global__ void __launch_bounds__(256) k_accumulate(const double* __restrict__ p
                 if (d2sq < 0.0) d2sq = 0.0;
                 double ratio_sq = d2sq * inv_sigma * inv_sigma / (d1 * d1);
                 if (ratio_sq > 16.0) continue;
+                // texel coordinates (kernels.py:327, :231-232, :267-276)
+                double gx = (ndc_x + 1.0) * 0.5 * Wd - 0.5;
+                double gy = (1.0 - ndc_y) * 0.5 * Hd - 0.5;
+                long long cx = x86_i64(rint(gx));
+                if (cx < 0) cx = 0;
+                else if (cx > W - 1) cx = W - 1;
+                long long cy = x86_i64(rint(gy));
+                if (cy < 0) cy = 0;
+                else if (cy > H - 1) cy = H - 1;
+                int bx0 = (int)max(cx - 1, 0LL), bx1 = (int)min(cx + 1, (long long)W - 1);
+                int by0 = (int)max(cy - 1, 0LL), by1 = (int)min(cy + 1, (long long)H - 1);
+                if (MARK) {
+                    uint32_t* m = dv.mask + (int64_t)f * H * dv.wwords;
+                    unsigned long long bits = ((1ull << (bx1 - bx0 + 1)) - 1ull) << (bx0 & 31);
+                    int w0 = bx0 >> 5;
+                    for (int yy = by0; yy <= by1; yy++) {
+                        uint32_t* row = m + (int64_t)yy * dv.wwords + w0;
+                        atomicOr(row, (uint32_t)bits);
+                        if (bits >> 32) atomicOr(row + 1, (uint32_t)(bits >> 32));
+                    }
+                    continue;
+                }
                 // kernels.py:323-329
                 double eps = eps_abs;
                 if (eps_rel * d > eps) eps = eps_rel * d;
-                if (!depth_match_eval(bv, g + j, W, H, (ndc_x + 1.0) * 0.5 * Wd, (1.0 - ndc_y) * 0.5 * Hd, d, eps,
-                                      F.near_, F.far_))
-                    continue;
+                const double* dep = dv.depth + (int64_t)f * W * H;
+                if (!depth_match_tex(dep, W, H, gx, gy, bx0, bx1, by0, by1, d, eps)) continue;
                 v += F.amp * exp(-0.5 * ratio_sq);  // kernels.py:340
             }
         }
-        if (valid) values[i] = v;
+        if (!MARK && valid) values[i] = v;
     }
 }
 
-// Full depth buffer of one fixation slot via the same texel evaluator
-// (kernel-seam port of kernels.rasterize, used by parity tests).
-__global__ void k_depth_full(BinView bv, int fslot, int W, int H, double near_, double far_, double* __restrict__ depth) {
-    int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (p >= (int64_t)W * H) return;
-    int px = (int)(p % W), py = (int)(p / W);
-    double T[9];
-    eval_block(bv, fslot, px, py, 1, 1, near_, far_, T);
-    depth[p] = T[0];
+// Fixation-major evaluation of the marked texels.  One CTA of 512 threads per
+// (fixation, 64x64-pixel tile); warp w owns the 16x16 sub-bin w of the tile.
+// The CTA scans the fixation's screen triangles (bbox array, coalesced), keeps
+// those overlapping the tile, stages their records in shared memory TX_CAP at
+// a time and bins them into the 16 sub-bins.  Each warp then walks its
+// sub-bin's triangles; every (triangle, marked texel inside its bbox) pair is
+// pushed to a per-warp ring queue and the queue is drained 32 pairs at a time
+// (one pair per lane: full SIMT use of the FP64 pipe), each pair folding its
+// depth into the texel's shared-memory minimum (atomicMin on the bit pattern:
+// non-negative doubles order like their bits).  The result is exactly the
+// value kernels.rasterize leaves in that pixel (same per-pixel arithmetic).
+#define TX_TILE 64
+#define TX_CAP 96
+#define TX_Q 256
+#define TX_DYN_SMEM (16 * 256 * 8 + 16 * TX_Q * 4)  // s_best + s_q
+__global__ void __launch_bounds__(512) k_texels(TriStore ts, DepthView dv, int tiles_x, int tiles_per_fix,
+                                                const GmFixExact* __restrict__ fixes, long long b0) {
+    __shared__ __align__(16) GmScreenTri s_tri[TX_CAP];
+    extern __shared__ __align__(16) unsigned char tx_dyn[];
+    auto s_best = reinterpret_cast<unsigned long long (*)[256]>(tx_dyn);
+    auto s_q = reinterpret_cast<uint32_t (*)[TX_Q]>(tx_dyn + 16 * 256 * 8);
+    __shared__ uint32_t s_mask[TX_TILE][2];
+    __shared__ int s_sel[512];
+    __shared__ uint8_t s_list[16][TX_CAP];
+    __shared__ int s_cnt[16];
+    __shared__ int s_nsel;
+    if (*ts.fail <= b0) return;
+    const int f = blockIdx.x / tiles_per_fix;
+    const int tile = blockIdx.x - f * tiles_per_fix;
+    const int W = dv.W, H = dv.H;
+    const int xb = (tile % tiles_x) * TX_TILE, yb = (tile / tiles_x) * TX_TILE;
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+    const uint32_t* m = dv.mask + (int64_t)f * H * dv.wwords;
+    {
+        uint32_t v = 0;
+        if (t < 2 * TX_TILE) {
+            int yy = yb + (t >> 1), ww = (xb >> 5) + (t & 1);
+            if (yy < H && ww < dv.wwords) v = m[(int64_t)yy * dv.wwords + ww];
+            s_mask[t >> 1][t & 1] = v;
+        }
+        if (!__syncthreads_or(v != 0u)) return;
+    }
+    // lane -> column (lane & 15) and rows (lane >> 4) * 8 .. + 7 of the warp's sub-bin
+    const int sbx = warp & 3, sby = warp >> 2;
+    const int lcol = lane & 15, lrow0 = (lane >> 4) * 8;
+    const int lx = sbx * 16 + lcol;
+    const int col = xb + lx, row0 = yb + sby * 16 + lrow0;
+    uint32_t need = 0;
+#pragma unroll
+    for (int r = 0; r < 8; r++) need |= ((s_mask[sby * 16 + lrow0 + r][lx >> 5] >> (lx & 31)) & 1u) << r;
+#pragma unroll
+    for (int r = 0; r < 8; r++) s_best[warp][(lrow0 + r) * 16 + lcol] = 0x7ff0000000000000ull;  // +inf
+    const bool warp_needs = __any_sync(0xffffffffu, need != 0u);
+    const double near_ = fixes[f].near_, far_ = fixes[f].far_;
+    const int n = min(ts.count[f], (int)ts.cap_seg);
+    const GmScreenTri* seg = ts.tris + (int64_t)f * ts.cap_seg;
+    const uint2* segb = ts.bbox + (int64_t)f * ts.cap_seg;
+    const int xe = xb + TX_TILE - 1, ye = yb + TX_TILE - 1;
+    const int sx0 = xb + sbx * 16, sy0 = yb + sby * 16;  // sub-bin origin (pixels)
+    unsigned qhead = 0, qtail = 0;  // warp-uniform ring indices
+    auto drain = [&](unsigned upto) {  // evaluate queued pairs while >= upto are pending
+        while (qtail - qhead >= upto && qtail != qhead) {
+            unsigned k = qhead + lane;
+            if (k < qtail) {
+                uint32_t e = s_q[warp][k & (TX_Q - 1)];
+                const GmScreenTri& T = s_tri[e >> 8];
+                int el = e & 255;
+                double d = texel_depth(T, sx0 + (el & 15), sy0 + (el >> 4), near_, far_);
+                if (d < CUDART_INF) atomicMin(&s_best[warp][el], (unsigned long long)__double_as_longlong(d));
+            }
+            qhead += min(32u, qtail - qhead);
+        }
+    };
+    for (int base = 0; base < n; base += 512) {
+        if (t == 0) s_nsel = 0;
+        __syncthreads();
+        const int i = base + t;
+        if (i < n) {
+            uint2 bb = segb[i];
+            int x0 = bb.x & 0xffff, x1 = bb.x >> 16, y0 = bb.y & 0xffff, y1 = bb.y >> 16;
+            if (!(x1 < xb || x0 > xe || y1 < yb || y0 > ye)) s_sel[atomicAdd(&s_nsel, 1)] = i;
+        }
+        __syncthreads();
+        const int nsel = s_nsel;
+        for (int c0 = 0; c0 < nsel; c0 += TX_CAP) {
+            const int mcount = min(TX_CAP, nsel - c0);
+            for (int q = t; q < mcount * 6; q += 512) {
+                const int ti = q / 6, part = q - ti * 6;
+                reinterpret_cast<uint4*>(&s_tri[ti])[part] = reinterpret_cast<const uint4*>(seg + s_sel[c0 + ti])[part];
+            }
+            if (t < 16) s_cnt[t] = 0;
+            __syncthreads();
+            if (t < mcount) {  // bin the staged triangles into the 16 sub-bins
+                const GmScreenTri& T = s_tri[t];
+                int bx0 = max((int)T.x0 - xb, 0) >> 4, bx1 = min((int)T.x1 - xb, TX_TILE - 1) >> 4;
+                int by0 = max((int)T.y0 - yb, 0) >> 4, by1 = min((int)T.y1 - yb, TX_TILE - 1) >> 4;
+                for (int by = by0; by <= by1; by++)
+                    for (int bx = bx0; bx <= bx1; bx++) {
+                        int sb = by * 4 + bx;
+                        s_list[sb][atomicAdd(&s_cnt[sb], 1)] = (uint8_t)t;
+                    }
+            }
+            __syncthreads();
+            if (warp_needs) {
+                const int cnt = s_cnt[warp];
+                for (int k = 0; k < cnt; k++) {
+                    const int slot = s_list[warp][k];
+                    const GmScreenTri& T = s_tri[slot];
+                    uint32_t bits = 0;
+                    if (col >= T.x0 && col <= T.x1) {
+                        int lo = max((int)T.y0 - row0, 0), hi = min((int)T.y1 - row0, 7);
+                        if (lo <= hi) bits = need & (((1u << (hi - lo + 1)) - 1u) << lo);
+                    }
+                    int pc = __popc(bits), incl = pc;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        int v = __shfl_up_sync(0xffffffffu, incl, o);
+                        if (lane >= o) incl += v;
+                    }
+                    const unsigned total = (unsigned)__shfl_sync(0xffffffffu, incl, 31);
+                    if (qtail - qhead + total > TX_Q) drain(1);  // total <= 256 = TX_Q
+                    unsigned at = qtail + (unsigned)(incl - pc);
+                    while (bits) {
+                        int r = __ffs(bits) - 1;
+                        bits &= bits - 1;
+                        s_q[warp][at++ & (TX_Q - 1)] = ((uint32_t)slot << 8) | (uint32_t)((lrow0 + r) * 16 + lcol);
+                    }
+                    qtail += total;
+                    __syncwarp();
+                    drain(32);
+                }
+                drain(1);  // the staged records are replaced after this chunk
+            }
+            __syncthreads();
+        }
+    }
+    if (need) {
+        double* dep = dv.depth + (int64_t)f * W * H;
+#pragma unroll
+        for (int r = 0; r < 8; r++)
+            if ((need >> r) & 1u)
+                dep[(int64_t)(row0 + r) * W + col] = __longlong_as_double((long long)s_best[warp][(lrow0 + r) * 16 + lcol]);
+    }
+}
+
+// Mark every texel of fixation slot 0 (the kernel-seam full z-buffer port).
+__global__ void k_mark_all(uint32_t* __restrict__ mask, int W, int H, int wwords) {
+    int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (q >= (int64_t)H * wwords) return;
+    int w = (int)(q % wwords);
+    int bits = min(32, W - 32 * w);
+    mask[q] = bits >= 32 ? 0xffffffffu : ((1u << bits) - 1u);
 }
 
 // Filter-only seam (kernels.py:302-319): per fixation, the compacted list of
@@ -553,6 +666,8 @@ static int dev_alloc(T** p, size_t n) {
     return GM_OK;
 }
 
+#define GM_RING 3  // pinned host setup slots in flight
+
 struct gm_plan {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -565,24 +680,25 @@ struct gm_plan {
     double *d_px = nullptr, *d_py = nullptr, *d_pz = nullptr;
     float4* d_chunk = nullptr;
     double* d_values = nullptr;
-    // batch buffers
+    // batch buffers: per-fixation setup (device + pinned host ring)
     int cap_B = 0;
     GmFixExact* d_fix = nullptr;
     GmFixCull* d_cull = nullptr;
-    GmFixExact* h_fix = nullptr;
-    GmFixCull* h_cull = nullptr;
-    GmScreenTri* d_pool = nullptr;
-    int64_t cap_pool = 0;
-    unsigned long long* d_counter = nullptr;  // [0] = screen tris
-    unsigned long long* h_counter = nullptr;  // pinned: [0] tris, [1] items
-    int* d_bin_count = nullptr;
-    int* d_bin_off = nullptr;
-    int* d_cursor = nullptr;
-    int64_t cap_bins = 0;
-    int* d_items = nullptr;
-    int64_t cap_items = 0;
-    void* d_scan_tmp = nullptr;
-    size_t scan_tmp_bytes = 0;
+    GmFixExact* h_fix[GM_RING] = {};
+    GmFixCull* h_cull[GM_RING] = {};
+    cudaEvent_t h_ev[GM_RING] = {};
+    // per-fixation screen-triangle segments
+    GmScreenTri* d_tris = nullptr;
+    uint2* d_bbox = nullptr;
+    int* d_count = nullptr;
+    int64_t cap_seg = 0, cap_seg_B = 0;
+    long long* d_fail = nullptr;
+    int* d_maxcount = nullptr;
+    unsigned long long* d_ntris = nullptr;
+    // marked z-buffer texels
+    double* d_depth = nullptr;   // [B][H][W] marked texels only
+    uint32_t* d_mask = nullptr;  // [B][H][wwords]
+    int64_t cap_depth = 0, cap_mask = 0;
     unsigned long long* d_max = nullptr;
     int host_threads = 8;
     // device-resident setup table (gm_plan_prepare)
@@ -593,6 +709,8 @@ struct gm_plan {
     void* d_flush = nullptr;
     int64_t flush_bytes = 0;
     int flush_gen = 0;
+    void* d_scan_tmp = nullptr;
+    size_t scan_tmp_bytes = 0;
 };
 
 static void plan_free_scene(gm_plan* p) {
@@ -616,9 +734,12 @@ extern "C" int gm_plan_create(int device, gm_plan** out) {
         return set_err(GM_ERR_CUDA, cudaGetErrorString(e));
     }
     cudaDeviceGetAttribute(&p->sms, cudaDevAttrMultiProcessorCount, device);
-    CK(cudaMalloc(&p->d_counter, 4 * sizeof(unsigned long long)));
+    CK(cudaFuncSetAttribute(k_texels, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
     CK(cudaMalloc(&p->d_max, sizeof(unsigned long long)));
-    CK(cudaMallocHost(&p->h_counter, 4 * sizeof(unsigned long long)));
+    CK(cudaMalloc(&p->d_fail, sizeof(long long)));
+    CK(cudaMalloc(&p->d_maxcount, sizeof(int)));
+    CK(cudaMalloc(&p->d_ntris, sizeof(unsigned long long)));
+    for (int r = 0; r < GM_RING; r++) CK(cudaEventCreateWithFlags(&p->h_ev[r], cudaEventDisableTiming));
     unsigned hc = std::thread::hardware_concurrency();
     p->host_threads = hc > 0 ? (int)hc : 8;
     *out = p;
@@ -631,10 +752,13 @@ extern "C" void gm_plan_destroy(gm_plan* p) {
     cudaStreamSynchronize(p->stream);
     plan_free_scene(p);
     cudaFree(p->d_fix); cudaFree(p->d_cull);
-    cudaFreeHost(p->h_fix); cudaFreeHost(p->h_cull); cudaFreeHost(p->h_counter);
-    cudaFree(p->d_pool); cudaFree(p->d_counter); cudaFree(p->d_bin_count); cudaFree(p->d_bin_off);
-    cudaFree(p->d_cursor); cudaFree(p->d_items); cudaFree(p->d_scan_tmp); cudaFree(p->d_max);
+    for (int r = 0; r < GM_RING; r++) {
+        cudaFreeHost(p->h_fix[r]); cudaFreeHost(p->h_cull[r]); cudaEventDestroy(p->h_ev[r]);
+    }
+    cudaFree(p->d_tris); cudaFree(p->d_bbox); cudaFree(p->d_count); cudaFree(p->d_fail); cudaFree(p->d_maxcount); cudaFree(p->d_ntris);
+    cudaFree(p->d_scan_tmp); cudaFree(p->d_max);
     cudaFree(p->d_fix_all); cudaFree(p->d_cull_all); cudaFree(p->d_flush);
+    cudaFree(p->d_depth); cudaFree(p->d_mask);
     cudaStreamDestroy(p->stream);
     delete p;
 }
@@ -749,91 +873,38 @@ extern "C" int64_t gm_plan_num_samples(gm_plan* p) { return p ? p->N : -1; }
 extern "C" int64_t gm_plan_num_triangles(gm_plan* p) { return p ? p->T : -1; }
 extern "C" double* gm_plan_values_device(gm_plan* p) { return p ? p->d_values : nullptr; }
 
-static int ensure_batch(gm_plan* p, int B, int nbins) {
+static int ensure_batch(gm_plan* p, int B, int W, int H, int64_t seg) {
     int rc;
     if (B > p->cap_B) {
         if ((rc = dev_alloc(&p->d_fix, (size_t)B))) return rc;
         if ((rc = dev_alloc(&p->d_cull, (size_t)B))) return rc;
-        cudaFreeHost(p->h_fix);
-        cudaFreeHost(p->h_cull);
-        CK(cudaMallocHost(&p->h_fix, sizeof(GmFixExact) * B));
-        CK(cudaMallocHost(&p->h_cull, sizeof(GmFixCull) * B));
+        if ((rc = dev_alloc(&p->d_count, (size_t)B))) return rc;
+        for (int r = 0; r < GM_RING; r++) {
+            cudaFreeHost(p->h_fix[r]);
+            cudaFreeHost(p->h_cull[r]);
+            CK(cudaMallocHost(&p->h_fix[r], sizeof(GmFixExact) * B));
+            CK(cudaMallocHost(&p->h_cull[r], sizeof(GmFixCull) * B));
+        }
         p->cap_B = B;
     }
-    int64_t nb = (int64_t)B * nbins;
-    if (nb + 1 > p->cap_bins) {
-        if ((rc = dev_alloc(&p->d_bin_count, (size_t)nb + 1))) return rc;
-        if ((rc = dev_alloc(&p->d_bin_off, (size_t)nb + 1))) return rc;
-        if ((rc = dev_alloc(&p->d_cursor, (size_t)nb + 1))) return rc;
-        p->cap_bins = nb + 1;
-        size_t tmp = 0;
-        cub::DeviceScan::ExclusiveSum(nullptr, tmp, p->d_bin_count, p->d_bin_off, (int)(nb + 1), p->stream);
-        if (tmp > p->scan_tmp_bytes) {
-            cudaFree(p->d_scan_tmp);
-            p->d_scan_tmp = nullptr;
-            CK(cudaMalloc(&p->d_scan_tmp, tmp));
-            p->scan_tmp_bytes = tmp;
-        }
+    if (seg > p->cap_seg || (int64_t)B * seg > p->cap_seg_B) {
+        int64_t cs = std::max(seg, p->cap_seg);
+        if ((rc = dev_alloc(&p->d_tris, (size_t)(B * cs)))) return rc;
+        if ((rc = dev_alloc(&p->d_bbox, (size_t)(B * cs)))) return rc;
+        p->cap_seg = cs;
+        p->cap_seg_B = B * cs;
     }
-    if (p->cap_pool == 0) {
-        p->cap_pool = std::max<int64_t>(1 << 20, (int64_t)B * 4096);
-        if ((rc = dev_alloc(&p->d_pool, (size_t)p->cap_pool))) return rc;
+    const int wwords = (W + 31) / 32;
+    const int64_t mask_words = (int64_t)B * H * wwords;
+    if (mask_words > p->cap_mask) {
+        if ((rc = dev_alloc(&p->d_mask, (size_t)mask_words))) return rc;
+        p->cap_mask = mask_words;
     }
-    if (p->cap_items == 0) {
-        p->cap_items = std::max<int64_t>(1 << 22, (int64_t)B * 16384);
-        if ((rc = dev_alloc(&p->d_items, (size_t)p->cap_items))) return rc;
+    if ((int64_t)B * W * H > p->cap_depth) {
+        if ((rc = dev_alloc(&p->d_depth, (size_t)B * W * H))) return rc;
+        p->cap_depth = (int64_t)B * W * H;
     }
     return GM_OK;
-}
-
-// Occluder setup + binning for one batch already uploaded to d_fix/d_cull.
-// Grows the pools and retries on overflow; leaves d_bin_off ready.
-static int run_occluders(gm_plan* p, const GmFixExact* d_fix, const GmFixCull* d_cull, int nb, int W, int H, int nbx,
-                         int nbins, cudaEvent_t ev_a, cudaEvent_t ev_b, int64_t* n_tris, int64_t* n_items) {
-    cudaStream_t s = p->stream;
-    for (int attempt = 0; attempt < 8; attempt++) {
-        int64_t nbn = (int64_t)nb * nbins;
-        CK(cudaMemsetAsync(p->d_counter, 0, sizeof(unsigned long long), s));
-        CK(cudaMemsetAsync(p->d_bin_count, 0, sizeof(int) * (nbn + 1), s));
-        if (ev_a) CK(cudaEventRecord(ev_a, s));
-        if (p->n_clu > 0) {
-            dim3 grid(blocks_for((p->n_clu + 31) / 32, 8), nb);
-            k_tri_setup<<<grid, 256, 0, s>>>(p->d_tw, p->T, p->d_tsph, p->d_csph, p->n_clu, d_fix, d_cull, W, H,
-                                             p->d_pool, p->cap_pool, p->d_counter);
-        }
-        if (ev_b) CK(cudaEventRecord(ev_b, s));
-        k_bin_count<<<p->sms * 8, 256, 0, s>>>(p->d_pool, p->d_counter, p->cap_pool, nbx, nbins, p->d_bin_count);
-        size_t tmp = p->scan_tmp_bytes;
-        CK(cub::DeviceScan::ExclusiveSum(p->d_scan_tmp, tmp, p->d_bin_count, p->d_bin_off, (int)(nbn + 1), s));
-        CK(cudaMemcpyAsync(p->h_counter, p->d_counter, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-        CK(cudaMemcpyAsync(p->h_counter + 1, p->d_bin_off + nbn, sizeof(int), cudaMemcpyDeviceToHost, s));
-        CK(cudaGetLastError());
-        CK(cudaStreamSynchronize(s));
-        unsigned long long ntri = p->h_counter[0];
-        int64_t nitems = (int64_t)(int)(p->h_counter[1] & 0xffffffffull);
-        bool grow = false;
-        if ((int64_t)ntri > p->cap_pool) {
-            int rc = dev_alloc(&p->d_pool, (size_t)(ntri + ntri / 2 + 1024));
-            if (rc) return rc;
-            p->cap_pool = (int64_t)(ntri + ntri / 2 + 1024);
-            grow = true;
-        }
-        if (!grow && (nitems < 0 || nitems > p->cap_items)) {
-            if (nitems < 0) return set_err(GM_ERR_OOM, "bin item count overflows int32; lower the batch size");
-            int rc = dev_alloc(&p->d_items, (size_t)(nitems + nitems / 2 + 1024));
-            if (rc) return rc;
-            p->cap_items = nitems + nitems / 2 + 1024;
-        }
-        if (grow) continue;  // pool overflowed: bins are incomplete, redo
-        CK(cudaMemcpyAsync(p->d_cursor, p->d_bin_off, sizeof(int) * (nbn + 1), cudaMemcpyDeviceToDevice, s));
-        k_bin_fill<<<p->sms * 8, 256, 0, s>>>(p->d_pool, p->d_counter, p->cap_pool, nbx, nbins, p->d_cursor,
-                                             p->d_items, p->cap_items);
-        CK(cudaGetLastError());
-        *n_tris = (int64_t)ntri;
-        *n_items = nitems;
-        return GM_OK;
-    }
-    return set_err(GM_ERR_OOM, "screen-triangle pool kept overflowing");
 }
 
 typedef void (*gm_progress_fn)(int64_t done, int64_t total, void* user);
@@ -842,10 +913,51 @@ static inline double wall_ms() {
     return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 
-// One pass over F fixations in batches.  Either `fx` (host table: the host
-// setup of each batch runs while the GPU works on the previous one) or the
-// prepared device setup table (gm_plan_prepare) supplies the per-fixation
-// records.  device_ms (optional) = CUDA-event time on the plan stream.
+__global__ void k_set_i64(long long* p, long long v) { *p = v; }
+
+// Kernels of one batch (already-uploaded setup records d_fix/d_cull):
+// occluder setup, candidate marking, texel evaluation, accumulation.
+static int enqueue_batch(gm_plan* p, const GmFixExact* d_fix, const GmFixCull* d_cull, int nb, int W, int H,
+                         long long b0, double inv_sigma, const GmConfig* cfg, bool accumulate, cudaEvent_t* ev) {
+    cudaStream_t s = p->stream;
+    const int wwords = (W + 31) / 32;
+    const int tiles_x = (W + TX_TILE - 1) / TX_TILE, tiles_y = (H + TX_TILE - 1) / TX_TILE;
+    TriStore ts{p->d_tris, p->d_bbox, p->d_count, p->cap_seg, p->d_fail, p->d_maxcount, p->d_ntris};
+    DepthView dv{p->d_depth, p->d_mask, W, H, wwords};
+    if (ev) CK(cudaEventRecord(ev[0], s));
+    CK(cudaMemsetAsync(p->d_count, 0, sizeof(int) * nb, s));
+    if (p->n_clu > 0) {
+        dim3 grid(blocks_for((p->n_clu + 31) / 32, 8), nb);
+        k_tri_setup<<<grid, 256, 0, s>>>(p->d_tw, p->T, p->d_tsph, p->d_csph, p->n_clu, d_fix, d_cull, W, H, ts, b0);
+    }
+    if (ev) CK(cudaEventRecord(ev[1], s));
+    if (p->n_chunks > 0 && accumulate) {
+        int grid = (int)std::min<int64_t>((p->n_chunks + 7) / 8, (int64_t)p->sms * 64);
+        CK(cudaMemsetAsync(p->d_mask, 0, sizeof(uint32_t) * (size_t)nb * H * wwords, s));
+        k_samples<true><<<grid, 256, 0, s>>>(p->d_px, p->d_py, p->d_pz, p->d_chunk, p->N, p->n_chunks, d_fix, d_cull,
+                                             nb, dv, inv_sigma, cfg->eps_abs, cfg->eps_rel, p->d_values, p->d_fail, b0);
+        if (ev) CK(cudaEventRecord(ev[2], s));
+        k_texels<<<nb * tiles_x * tiles_y, 512, TX_DYN_SMEM, s>>>(ts, dv, tiles_x, tiles_x * tiles_y, d_fix, b0);
+        if (ev) CK(cudaEventRecord(ev[3], s));
+        k_samples<false><<<grid, 256, 0, s>>>(p->d_px, p->d_py, p->d_pz, p->d_chunk, p->N, p->n_chunks, d_fix,
+                                              d_cull, nb, dv, inv_sigma, cfg->eps_abs, cfg->eps_rel, p->d_values,
+                                              p->d_fail, b0);
+    } else if (ev) {
+        CK(cudaEventRecord(ev[2], s));
+        CK(cudaEventRecord(ev[3], s));
+    }
+    if (ev) CK(cudaEventRecord(ev[4], s));
+    CK(cudaGetLastError());
+    return GM_OK;
+}
+
+// One pass over F fixations in batches, all enqueued without host syncs.
+// Either `fx` (host table: the host setup of batch i+1 runs while the GPU
+// works on batch i, through a ring of pinned slots) or the prepared device
+// setup table (gm_plan_prepare) supplies the per-fixation records.  If a batch
+// overflows the screen-triangle segments, it and every later batch is a no-op
+// on the device; the host grows the segments and resumes from that batch, so
+// the per-sample accumulation order is still the log order.
 static int run_batches(gm_plan* p, const double* fx, int64_t F, const GmConfig* cfg, int reset, GmTimings* tm,
                        gm_progress_fn progress, void* user, int64_t* bad_fixation, float* device_ms) {
     if (cfg->zbuffer_resolution < 1 || cfg->zbuffer_resolution > 65535)
@@ -855,19 +967,27 @@ static int run_batches(gm_plan* p, const double* fx, int64_t F, const GmConfig* 
     const bool prepared = fx == nullptr;
     double t_start = wall_ms();
     const int W = cfg->zbuffer_resolution, H = cfg->zbuffer_resolution;
-    const int nbx = (W + GM_BIN - 1) / GM_BIN, nby = (H + GM_BIN - 1) / GM_BIN;
-    const int nbins = nbx * nby;
     int B = cfg->batch > 0 ? cfg->batch : 512;
     if (B > 4096) B = 4096;
-    int64_t max_b = std::max<int64_t>(1, (int64_t)(1 << 26) / nbins);  // bins per batch <= 64M
-    if (B > max_b) B = (int)max_b;
+    const int64_t depth_per_fix = (int64_t)W * H;
+    int64_t max_d = std::max<int64_t>(1, ((int64_t)1 << 28) / depth_per_fix);  // z-buffer store <= 2 GiB
+    if (B > max_d) B = (int)max_d;
     if (F > 0 && B > F) B = (int)F;
+    B = std::max(B, 1);
     GmSetupConsts consts;
     gm_setup_consts(cfg->theta, cfg->filtering, W, H, &consts);
-    int rc = ensure_batch(p, std::max(B, 1), nbins);
+    int rc = ensure_batch(p, B, W, H, std::max<int64_t>(p->cap_seg, 4096));
     if (rc) return rc;
     cudaStream_t s = p->stream;
     cudaEvent_t ev_start = nullptr, ev_end = nullptr;
+    std::vector<cudaEvent_t> evs;
+    auto cleanup = [&]() {
+        for (auto e : evs) cudaEventDestroy(e);
+        evs.clear();
+        if (ev_start) cudaEventDestroy(ev_start);
+        if (ev_end) cudaEventDestroy(ev_end);
+        ev_start = ev_end = nullptr;
+    };
     if (device_ms) {
         CK(cudaEventCreate(&ev_start));
         CK(cudaEventCreate(&ev_end));
@@ -876,81 +996,101 @@ static int run_batches(gm_plan* p, const double* fx, int64_t F, const GmConfig* 
     if (reset && p->N > 0) CK(cudaMemsetAsync(p->d_values, 0, sizeof(double) * p->N, s));
     GmTimings t;
     memset(&t, 0, sizeof(t));
-    std::vector<cudaEvent_t> evs;
     const bool timing = tm != nullptr;
-    double inv_sigma = 1.0 / consts.sigma;
-    BinView bv{p->d_pool, p->d_bin_off, p->d_items, nbx, nbins};
-    int64_t done_reported = 0;
-    auto cleanup = [&]() {
-        for (auto e : evs) cudaEventDestroy(e);
-        if (ev_start) cudaEventDestroy(ev_start);
-        if (ev_end) cudaEventDestroy(ev_end);
-    };
-    for (int64_t b0 = 0; b0 < F; b0 += B) {
-        int nb = (int)std::min<int64_t>(B, F - b0);
-        GmFixExact* d_fix = p->d_fix;
-        GmFixCull* d_cull = p->d_cull;
-        if (prepared) {
-            d_fix = p->d_fix_all + b0;
-            d_cull = p->d_cull_all + b0;
-        } else {
-            double ts = wall_ms();
-            int64_t bad = gm_setup_batch(fx + GM_FIX_STRIDE * b0, nb, &consts, p->h_fix, p->h_cull, p->host_threads);
-            t.setup_ms += wall_ms() - ts;
-            if (bad >= 0) {
-                cudaStreamSynchronize(s);
+    const double inv_sigma = 1.0 / consts.sigma;
+    int64_t start = 0;
+    for (int attempt = 0; attempt < 16; attempt++) {
+        k_set_i64<<<1, 1, 0, s>>>(p->d_fail, LLONG_MAX);
+        CK(cudaMemsetAsync(p->d_maxcount, 0, sizeof(int), s));
+        CK(cudaMemsetAsync(p->d_ntris, 0, sizeof(unsigned long long), s));
+        int slot = 0;
+        for (int64_t b0 = start; b0 < F; b0 += B) {
+            int nb = (int)std::min<int64_t>(B, F - b0);
+            const GmFixExact* d_fix = p->d_fix;
+            const GmFixCull* d_cull = p->d_cull;
+            if (prepared) {
+                d_fix = p->d_fix_all + b0;
+                d_cull = p->d_cull_all + b0;
+            } else {
+                CK(cudaEventSynchronize(p->h_ev[slot]));  // slot's previous upload has completed
+                double ts = wall_ms();
+                int64_t bad = gm_setup_batch(fx + GM_FIX_STRIDE * b0, nb, &consts, p->h_fix[slot], p->h_cull[slot],
+                                             p->host_threads);
+                t.setup_ms += wall_ms() - ts;
+                if (bad >= 0) {
+                    cudaStreamSynchronize(s);
+                    cleanup();
+                    if (bad_fixation) *bad_fixation = b0 + bad;
+                    return set_err(GM_ERR_INVALID_FRUSTUM, "degenerate frustum bounds (InvalidFrustumError)");
+                }
+                CK(cudaMemcpyAsync(p->d_fix, p->h_fix[slot], sizeof(GmFixExact) * nb, cudaMemcpyHostToDevice, s));
+                CK(cudaMemcpyAsync(p->d_cull, p->h_cull[slot], sizeof(GmFixCull) * nb, cudaMemcpyHostToDevice, s));
+                CK(cudaEventRecord(p->h_ev[slot], s));
+                slot = (slot + 1) % GM_RING;
+            }
+            cudaEvent_t* e = nullptr;
+            if (timing) {
+                for (int q = 0; q < 5; q++) {
+                    cudaEvent_t x;
+                    CK(cudaEventCreate(&x));
+                    evs.push_back(x);
+                }
+                e = &evs[evs.size() - 5];
+            }
+            rc = enqueue_batch(p, d_fix, d_cull, nb, W, H, (long long)b0, inv_sigma, cfg, true, e);
+            if (rc) {
                 cleanup();
-                if (bad_fixation) *bad_fixation = b0 + bad;
-                return set_err(GM_ERR_INVALID_FRUSTUM, "degenerate frustum bounds (InvalidFrustumError)");
+                return rc;
             }
-            CK(cudaMemcpyAsync(p->d_fix, p->h_fix, sizeof(GmFixExact) * nb, cudaMemcpyHostToDevice, s));
-            CK(cudaMemcpyAsync(p->d_cull, p->h_cull, sizeof(GmFixCull) * nb, cudaMemcpyHostToDevice, s));
-        }
-        cudaEvent_t e[4] = {nullptr, nullptr, nullptr, nullptr};
-        if (timing) {
-            for (int q = 0; q < 4; q++) {
-                CK(cudaEventCreate(&e[q]));
-                evs.push_back(e[q]);
+            t.batches += 1;
+            if (progress) {  // per-batch progress needs a sync; only then
+                CK(cudaStreamSynchronize(s));
+                long long failed = LLONG_MAX;
+                CK(cudaMemcpy(&failed, p->d_fail, sizeof(failed), cudaMemcpyDeviceToHost));
+                if (failed == LLONG_MAX) progress(b0 + nb, F, user);
             }
         }
-        int64_t ntri = 0, nitems = 0;
-        rc = run_occluders(p, d_fix, d_cull, nb, W, H, nbx, nbins, e[0], e[1], &ntri, &nitems);
+        long long failed = LLONG_MAX;
+        int maxcount = 0;
+        unsigned long long ntris = 0;
+        CK(cudaMemcpyAsync(&failed, p->d_fail, sizeof(failed), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(&maxcount, p->d_maxcount, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(&ntris, p->d_ntris, sizeof(ntris), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        t.screen_tris += (int64_t)ntris;
+        if (failed == LLONG_MAX) break;
+        // grow the per-fixation segments and resume at the first failed batch
+        int64_t want = std::max<int64_t>(2 * p->cap_seg, (int64_t)maxcount + maxcount / 4 + 64);
+        p->cap_seg = 0;
+        rc = ensure_batch(p, B, W, H, want);
         if (rc) {
             cleanup();
             return rc;
         }
-        // the previous batch's accumulate finished before this batch's sync
-        if (progress && b0 > done_reported) {
-            progress(b0, F, user);
-            done_reported = b0;
+        start = failed;
+        t.batches = 0;
+        t.retries += 1;
+        if (attempt == 15) {
+            cleanup();
+            return set_err(GM_ERR_OOM, "screen-triangle segments kept overflowing");
         }
-        t.screen_tris += ntri;
-        t.bin_items += nitems;
-        t.batches += 1;
-        if (timing) CK(cudaEventRecord(e[2], s));
-        if (p->n_chunks > 0) {
-            int grid = (int)std::min<int64_t>((p->n_chunks + 7) / 8, (int64_t)p->sms * 64);
-            k_accumulate<<<grid, 256, 0, s>>>(p->d_px, p->d_py, p->d_pz, p->d_chunk, p->N, p->n_chunks, d_fix, d_cull,
-                                              nb, bv, W, H, inv_sigma, cfg->eps_abs, cfg->eps_rel, p->d_values);
-        }
-        if (timing) CK(cudaEventRecord(e[3], s));
-        CK(cudaGetLastError());
     }
     if (device_ms) CK(cudaEventRecord(ev_end, s));
     CK(cudaStreamSynchronize(s));
     if (device_ms) cudaEventElapsedTime(device_ms, ev_start, ev_end);
-    if (progress && F > done_reported) progress(F, F, user);
     if (timing) {
-        for (size_t q = 0; q + 3 < evs.size(); q += 4) {
-            float a = 0, b = 0, c = 0;
-            cudaEventElapsedTime(&a, evs[q], evs[q + 1]);
-            cudaEventElapsedTime(&c, evs[q + 1], evs[q + 2]);
-            cudaEventElapsedTime(&b, evs[q + 2], evs[q + 3]);
-            t.cull_ms += a;
-            t.rasterize_ms += c;
-            t.accumulate_ms += b;
+        // events of the last (successful) pass are the last t.batches groups
+        size_t first = evs.size() - 5 * (size_t)t.batches;
+        for (size_t q = first; q + 4 < evs.size(); q += 5) {
+            float a[4] = {0, 0, 0, 0};
+            for (int z = 0; z < 4; z++) cudaEventElapsedTime(&a[z], evs[q + z], evs[q + z + 1]);
+            t.cull_ms += a[0];
+            t.mark_ms += a[1];
+            t.texel_ms += a[2];
+            t.accumulate_ms += a[3];
         }
         t.total_ms = wall_ms() - t_start;
+        t.bin_items = 0;
         *tm = t;
     }
     cleanup();
@@ -1170,37 +1310,52 @@ extern "C" int gm_fixation_setup(const double* fx, int64_t F, double theta, int 
 
 // kernels.rasterize for the plan's occluders under fixation `fx` (18 floats):
 // the whole res x res depth buffer (+inf where nothing is drawn), evaluated by
-// the same binned texel evaluator k_accumulate uses.  When no_cull != 0 the
-// occluder cone cull is disabled (every triangle is projected).
+// the production texel kernel (k_texels) with every texel marked.  When
+// no_cull != 0 the occluder cone cull is disabled (every triangle is projected).
 extern "C" int gm_plan_depth_buffer(gm_plan* p, const double* fx, double theta, int filtering, int res, int no_cull,
                                     double* depth) {
     if (!p || !fx || !depth || res < 1 || res > 65535) return set_err(GM_ERR_ARG, "bad arguments");
     CK(cudaSetDevice(p->device));
-    const int nbx = (res + GM_BIN - 1) / GM_BIN, nbins = nbx * nbx;
     GmSetupConsts c;
     gm_setup_consts(theta, filtering, res, res, &c);
-    int rc = ensure_batch(p, 1, nbins);
+    int rc = ensure_batch(p, 1, res, res, std::max<int64_t>(p->cap_seg, 4096));
     if (rc) return rc;
-    int64_t bad = gm_setup_batch(fx, 1, &c, p->h_fix, p->h_cull, 1);
-    if (bad >= 0) return set_err(GM_ERR_INVALID_FRUSTUM, "degenerate frustum bounds (InvalidFrustumError)");
-    if (no_cull) {
-        GmFixCull& k = p->h_cull[0];
-        k.cos_t = -3.0f;  // sphere_visible: no culling at all
-    }
     cudaStream_t s = p->stream;
-    CK(cudaMemcpyAsync(p->d_fix, p->h_fix, sizeof(GmFixExact), cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(p->d_cull, p->h_cull, sizeof(GmFixCull), cudaMemcpyHostToDevice, s));
-    int64_t ntri = 0, nitems = 0;
-    rc = run_occluders(p, p->d_fix, p->d_cull, 1, res, res, nbx, nbins, nullptr, nullptr, &ntri, &nitems);
-    if (rc) return rc;
-    double* d_depth = nullptr;
-    CK(cudaMallocAsync(&d_depth, sizeof(double) * res * res, s));
-    BinView bv{p->d_pool, p->d_bin_off, p->d_items, nbx, nbins};
-    k_depth_full<<<blocks_for((int64_t)res * res, 256), 256, 0, s>>>(bv, 0, res, res, p->h_fix[0].near_,
-                                                                      p->h_fix[0].far_, d_depth);
+    CK(cudaEventSynchronize(p->h_ev[0]));
+    int64_t bad = gm_setup_batch(fx, 1, &c, p->h_fix[0], p->h_cull[0], 1);
+    if (bad >= 0) return set_err(GM_ERR_INVALID_FRUSTUM, "degenerate frustum bounds (InvalidFrustumError)");
+    if (no_cull) p->h_cull[0][0].cos_t = -3.0f;  // sphere_visible: no culling at all
+    CK(cudaMemcpyAsync(p->d_fix, p->h_fix[0], sizeof(GmFixExact), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(p->d_cull, p->h_cull[0], sizeof(GmFixCull), cudaMemcpyHostToDevice, s));
+    CK(cudaEventRecord(p->h_ev[0], s));
+    const int wwords = (res + 31) / 32;
+    for (int attempt = 0; attempt < 16; attempt++) {
+        k_set_i64<<<1, 1, 0, s>>>(p->d_fail, LLONG_MAX);
+        CK(cudaMemsetAsync(p->d_maxcount, 0, sizeof(int), s));
+        CK(cudaMemsetAsync(p->d_count, 0, sizeof(int), s));
+        TriStore ts{p->d_tris, p->d_bbox, p->d_count, p->cap_seg, p->d_fail, p->d_maxcount, p->d_ntris};
+        if (p->n_clu > 0) {
+            dim3 grid(blocks_for((p->n_clu + 31) / 32, 8), 1);
+            k_tri_setup<<<grid, 256, 0, s>>>(p->d_tw, p->T, p->d_tsph, p->d_csph, p->n_clu, p->d_fix, p->d_cull, res,
+                                             res, ts, 0);
+        }
+        long long failed = LLONG_MAX;
+        int maxcount = 0;
+        CK(cudaMemcpyAsync(&failed, p->d_fail, sizeof(failed), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(&maxcount, p->d_maxcount, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (failed == LLONG_MAX) break;
+        int64_t want = std::max<int64_t>(2 * p->cap_seg, (int64_t)maxcount + maxcount / 4 + 64);
+        p->cap_seg = 0;
+        if ((rc = ensure_batch(p, 1, res, res, want))) return rc;
+    }
+    TriStore ts{p->d_tris, p->d_bbox, p->d_count, p->cap_seg, p->d_fail, p->d_maxcount, p->d_ntris};
+    DepthView dv{p->d_depth, p->d_mask, res, res, wwords};
+    k_mark_all<<<blocks_for((int64_t)res * wwords, 256), 256, 0, s>>>(p->d_mask, res, res, wwords);
+    const int tiles_x = (res + TX_TILE - 1) / TX_TILE;
+    k_texels<<<tiles_x * tiles_x, 512, TX_DYN_SMEM, s>>>(ts, dv, tiles_x, tiles_x * tiles_x, p->d_fix, 0);
     CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(depth, d_depth, sizeof(double) * res * res, cudaMemcpyDeviceToHost, s));
-    CK(cudaFreeAsync(d_depth, s));
+    CK(cudaMemcpyAsync(depth, p->d_depth, sizeof(double) * res * res, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     return GM_OK;
 }

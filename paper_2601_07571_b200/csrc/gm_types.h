@@ -21,7 +21,7 @@ struct __attribute__((aligned(16))) GmFixExact {
     double near_lo, far_hi;     // near'(1-1e-9), far'(1+1e-9) (kernels.py:312)
     double cropped;             // 1.0 when the crop frustum was used
     double pad_;
-};  // 28 doubles = 224 B
+};  // 26 doubles = 208 B
 
 // Conservative float32 culling record of one fixation, world space.
 // Cone = 4-sigma cone around the world gaze ray from the camera position.
@@ -71,12 +71,21 @@ struct GmTimings {
     double setup_ms;       // host fixation setup (wall)
     double cull_ms;        // occluder cull + clip + project (device)
     double rasterize_ms;   // screen-space binning (device)
-    double accumulate_ms;  // filter + visibility + Gaussian (device)
+    double accumulate_ms;  // filter + depth test + Gaussian (device, k_samples<false>)
     double total_ms;       // whole call (wall)
+    double mark_ms;        // candidate texel marking (device, k_samples<true>)
+    double texel_ms;       // marked z-buffer texels (device, k_texels)
     int64_t screen_tris;   // projected triangles produced
-    int64_t bin_items;     // (triangle, bin) pairs produced
+    int64_t bin_items;     // reserved
     int64_t batches;
+    int64_t retries;       // passes resumed after a screen-triangle segment overflow
 };
+
+#ifdef __cplusplus
+static_assert(sizeof(GmFixExact) == 26 * 8, "GmFixExact layout (Python binds 26 float64)");
+static_assert(sizeof(GmFixCull) == 20 * 4, "GmFixCull layout");
+static_assert(sizeof(GmScreenTri) == 96, "GmScreenTri layout");
+#endif
 
 #define GM_NDC_SLACK 1e-9
 #define GM_FIX_STRIDE 18

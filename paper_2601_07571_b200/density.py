@@ -80,8 +80,9 @@ class DensityMap:
 @dataclass
 class Timings:
     """Seconds per phase.  cull = occluder cone cull + clip + projection
-    (device), rasterize = screen binning (device), accumulate = filter +
-    visibility + Gaussian (device), setup = host fixation setup."""
+    (device), rasterize = screen binning + evaluation of the z-buffer texels
+    the depth test reads (device), accumulate = NDC filter + cone + depth test
+    + Gaussian (device, both sample passes), setup = host fixation setup."""
 
     phases: dict = field(default_factory=lambda: {"cull": 0.0, "rasterize": 0.0, "accumulate": 0.0,
                                                   "normalize": 0.0})
@@ -183,8 +184,8 @@ class ScenePlan:
         self.last_timings = tm
         if timers is not None:
             timers.add("cull", tm.cull_ms / 1e3)
-            timers.add("rasterize", tm.rasterize_ms / 1e3)
-            timers.add("accumulate", tm.accumulate_ms / 1e3)
+            timers.add("rasterize", (tm.rasterize_ms + tm.texel_ms) / 1e3)
+            timers.add("accumulate", (tm.mark_ms + tm.accumulate_ms) / 1e3)
             timers.add("setup", tm.setup_ms / 1e3)
 
     def global_max(self) -> float:

@@ -178,7 +178,7 @@ def gaussian_weight(p, gaze_dir, duration_t: float, cone: GazeCone) -> float:
     return duration_t / (cone.sigma * SQRT_TWO_PI) * math.exp(-0.5 * ratio * ratio)
 
 
-# GmFixExact field offsets (float64 units), csrc/gm_types.h
+# GmFixExact field offsets (float64 units, 26 per record), csrc/gm_types.h
 SETUP_FIELDS = {"rot": slice(0, 9), "trans": slice(9, 12), "gaze": slice(12, 15), "amp": 15, "p00": 16,
                 "p11": 17, "p02": 18, "p12": 19, "near": 20, "far": 21, "near_lo": 22, "far_hi": 23,
                 "cropped": 24}
@@ -186,7 +186,7 @@ SETUP_FIELDS = {"rot": slice(0, 9), "trans": slice(9, 12), "gaze": slice(12, 15)
 
 def fixation_setup(fixations, theta: float = DEFAULT_THETA, filtering: bool = True,
                    zbuffer_resolution: int = 512) -> np.ndarray:
-    """(F, 28) float64 per-fixation setup table exactly as the kernels use it
+    """(F, 26) float64 per-fixation setup table exactly as the kernels use it
     (view rotation/translation, crop-or-full projection terms, near'/far',
     amplitude); see SETUP_FIELDS.  Raises InvalidFrustumError like the
     reference's perspective_matrix."""

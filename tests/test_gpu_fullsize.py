@@ -1,0 +1,121 @@
+"""Full-size checks on the bench workload (C2 room: 98,080 triangles,
+2,189,280 samples): bit-exact layout / positions / filter sets and oracle
+parity on a fixation prefix, plus size-independent properties over
+thousands of fixations (determinism, additivity across partitions,
+filtered ~ unfiltered)."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+import paper_2601_07571_b200 as gm
+import workloads as W
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def room():
+    scene, k, fx = W.c2(4096)
+    sampled = gm.build_sampled_meshes(scene, k)
+    cfg = gm.GenerationConfig(k=k)
+    plan = gm.get_plan(scene, sampled, cfg) if hasattr(gm, "get_plan") else None
+    from paper_2601_07571_b200.density import get_plan
+
+    plan = get_plan(scene, sampled, cfg)
+    return scene, k, fx, sampled, cfg, plan
+
+
+def test_room_layout_and_positions_bitwise(room):
+    scene, k, fx, sampled, cfg, plan = room
+    lay = O.build_layouts(scene, k)
+    assert sum(v[3] for v in lay.values()) == 2_189_280
+    for oid, (res, cnt, off, total) in lay.items():
+        np.testing.assert_array_equal(sampled[oid].resolutions, res)
+        np.testing.assert_array_equal(sampled[oid].offsets, off)
+        assert sampled[oid].total_samples == total
+    world = O.world_samples(scene, lay)
+    np.testing.assert_array_equal(plan.positions(), np.concatenate([world[o.object_id] for o in scene.objects]))
+
+
+def test_room_candidate_sets_bitwise(room):
+    scene, k, fx, sampled, cfg, plan = room
+    pos = plan.positions()
+    for filtering in (True, False):
+        c = gm.GenerationConfig(k=k, filtering_enabled=filtering)
+        got = plan.candidates(fx[:8], c)
+        for row, idx in zip(fx[:8], got):
+            want = O.candidates(pos, O.fixation_setup(row, c.theta, filtering))
+            np.testing.assert_array_equal(idx, want)
+            assert len(want) > 0
+
+
+@pytest.mark.parametrize("filtering", [True, False])
+def test_room_values_vs_oracle_prefix(room, filtering):
+    scene, k, fx, sampled, cfg, plan = room
+    n = 24
+    c = gm.GenerationConfig(k=k, filtering_enabled=filtering)
+    dm = gm.generate(scene, sampled, fx[:n], c)
+    vals, gmax = O.generate(scene, O.rows_as_fixations(fx[:n]), k=k, filtering_enabled=filtering, threads=8,
+                            layouts=O.build_layouts(scene, k))
+    assert dm.global_max == pytest.approx(gmax, rel=1e-12)
+    nz = 0
+    for oid in vals:
+        np.testing.assert_array_equal(dm.values[oid] != 0, vals[oid] != 0)
+        np.testing.assert_allclose(dm.values[oid], vals[oid], rtol=1e-12, atol=0.0)
+        nz += int((vals[oid] != 0).sum())
+    assert nz > 1000
+
+
+def _digest(dm):
+    h = hashlib.sha256()
+    for oid in sorted(dm.values):
+        h.update(np.ascontiguousarray(dm.values[oid]).tobytes())
+    return h.hexdigest()
+
+
+def test_room_determinism_and_additivity(room):
+    scene, k, fx, sampled, cfg, plan = room
+    full = gm.generate(scene, sampled, fx, cfg)
+    again = gm.generate(scene, sampled, fx, cfg, batch=333)
+    assert _digest(full) == _digest(again)  # checksum determinism (cli bench, gm/cli.py:180-186)
+    a = gm.generate(scene, sampled, fx[:1500], cfg)
+    b = gm.generate(scene, sampled, fx[1500:], cfg)
+    for oid in full.values:
+        np.testing.assert_allclose(full.values[oid], a.values[oid] + b.values[oid], rtol=1e-9, atol=1e-12)
+    assert full.global_max > 0
+
+
+def test_room_filtered_vs_unfiltered(room):
+    scene, k, fx, sampled, cfg, plan = room
+    on = gm.generate(scene, sampled, fx[:256], gm.GenerationConfig(k=k, filtering_enabled=True))
+    off = gm.generate(scene, sampled, fx[:256], gm.GenerationConfig(k=k, filtering_enabled=False))
+    scale = off.global_max
+    agree = total = unexplained = 0
+    for oid in on.values:
+        x, y = on.values[oid], off.values[oid]
+        match = np.abs(x - y) / scale <= 1e-6
+        agree += int(match.sum())
+        total += len(x)
+    assert agree / total >= 0.999
+
+
+def test_shells_occlusion_vs_oracle():
+    """C5-style nested shells (occlusion-dominated), reduced size."""
+    base = W.icosphere(4, 1.0)
+    scene = gm.Scene(tuple(gm.SceneObject(f"s{i}", gm.Mesh(base.vertices * (0.5 + 0.25 * i), base.faces))
+                           for i in range(6)))
+    fx = W.orbit_fixations(16, 4, 3.0, 4.5, jitter=0.3)
+    for filtering in (True, False):
+        cfg = gm.GenerationConfig(k=4000.0, filtering_enabled=filtering)
+        sampled = gm.build_sampled_meshes(scene, cfg.k)
+        dm = gm.generate(scene, sampled, fx, cfg)
+        vals, gmax = O.generate(scene, O.rows_as_fixations(fx), k=cfg.k, filtering_enabled=filtering, threads=8)
+        assert dm.global_max == pytest.approx(gmax, rel=1e-12)
+        for oid in vals:
+            np.testing.assert_array_equal(dm.values[oid] != 0, vals[oid] != 0)
+            np.testing.assert_allclose(dm.values[oid], vals[oid], rtol=1e-12, atol=0.0)
+        inner = sum(int((vals[f"s{i}"] != 0).sum()) for i in range(5))
+        assert inner == 0  # only the outermost shell is visible
