@@ -224,7 +224,7 @@ def run_ours(args, rank, world):
     def one_step(timed_stats=None):
         tm = _native.GmTimings()
         ms = ctypes.c_float(0.0)
-        _native.check(lib.gm_plan_run(plan._h, 1, ctypes.byref(tm), ctypes.byref(ms)), "gm_plan_run")
+        _native.check(lib.gm_plan_run(plan._h, 1, 0, ctypes.byref(tm), ctypes.byref(ms)), "gm_plan_run")
         extra = 0.0
         if world > 1:
             import torch
@@ -260,46 +260,78 @@ def run_ours(args, rank, world):
         step_ms = float(tt.item())
     value = world * N * F / (step_ms / 1e3)
     tm = tms[-1]
-    acc_ms = tm.accumulate_ms
     # per step: k_set_i64; per batch: k_tri_setup, k_samples<mark>, k_texels, k_samples<accumulate>;
     # then k_max
     launches = int(tm.batches) * 4 + 2
 
     # ---- e2e through the public API (host table in, host values out) -----
+    # Every step: fixation table (host) -> host setup -> H2D -> kernels -> D2H of
+    # the values.  N > 1: sharding.generate_sharded over the concatenated
+    # N x F stream (each rank's contiguous shard is its own F fixations) with
+    # the NCCL all-reduce inside the timed region.
     e2e = None
     if not args.no_e2e:
-        pinned_vals = None
-        t0 = time.perf_counter()
+        if world > 1:
+            from paper_2601_07571_b200.sharding import generate_sharded
+
+            full = np.concatenate([workload(args.config, args.fixations, r)[2] for r in range(world)])
+
+            def e2e_call():
+                return generate_sharded(scene, sampled, full, cfg, device=device)
+        else:
+            def e2e_call():
+                return gm.generate(scene, sampled, fx, cfg, device=device)
+        e2e_call()  # plan upload + warm
         e_times = []
-        for _ in range(max(1, min(args.steps, 2))):
+        for _ in range(max(1, min(args.steps, 3))):
+            if world > 1:
+                dist.barrier()
             t0 = time.perf_counter()
-            dm = gm.generate(scene, sampled, fx, cfg, device=device)
+            e2e_call()
             e_times.append(time.perf_counter() - t0)
         e_t = float(np.mean(e_times))
-        e2e = {"value": world * N * F / e_t if world == 1 else None, "unit": UNIT,
-               "h2d_bytes_per_step": int(F * (208 + 80)), "d2h_bytes_per_step": int(N * 8),
-               "ms_per_step": e_t * 1e3, "path": "paper_2601_07571_b200.generate (fixation table -> values dict)"}
         if world > 1:
             import torch
 
             tt = torch.tensor([e_t], device=f"cuda:{device}", dtype=torch.float64)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            e2e["value"] = world * N * F / float(tt.item())
+            e_t = float(tt.item())
+        e2e = {"value": world * N * F / e_t, "unit": UNIT, "h2d_bytes_per_step": int(F * (208 + 80)),
+               "d2h_bytes_per_step": int(N * 8), "ms_per_step": e_t * 1e3,
+               "path": "paper_2601_07571_b200.generate (fixation table in host memory -> values dict)"
+               if world == 1 else "paper_2601_07571_b200.sharding.generate_sharded (NCCL all-reduce)",
+               "timing": "host wall clock around the API call"}
 
+    # ---- algorithmic work of this step (one instrumented, untimed pass) ----
+    stats = (ctypes.c_uint64 * 16)()
+    tm_s = _native.GmTimings()
+    ms_s = ctypes.c_float(0.0)
+    _native.check(lib.gm_plan_run(plan._h, 1, _native.GM_FLAG_STATS, ctypes.byref(tm_s), ctypes.byref(ms_s)))
+    _native.check(lib.gm_plan_stats(plan._h, stats))
+    st = dict(zip(_native.STAT_NAMES, [int(x) for x in stats]))
     peaks_path = ROOT / "MEASURED_PEAKS.json"
     peaks = json.loads(peaks_path.read_text()) if peaks_path.exists() else {}
-    # FP32 SIMT peak: 148 SMs x 128 lanes x 2 flop x max SM clock (nominal; no measured FP32 figure exists)
-    fp32_peak = 148 * 128 * 2 * (peaks.get("sm_max_mhz", 1965.0) * 1e6) / 1e12
-    # reference-algorithmic work: 26 FP32-equivalent flops per nominal pair
-    alg_flops = 26.0 * N * F
-    roof = {"bound": "fp32", "achieved": alg_flops / (acc_ms / 1e3) / 1e12 if acc_ms else None,
-            "peak": fp32_peak, "unit": "TFLOP/s", "frac": None, "traffic": None,
-            "kernel": "k_accumulate", "kernel_ms_per_step": acc_ms,
-            "note": "reference-algorithmic 26 flop/pair over the whole step's k_accumulate time; "
-                    "peak = nominal FP32 SIMT at max SM clock"}
-    if roof["achieved"]:
-        roof["frac"] = roof["achieved"] / fp32_peak
-
+    clk_ghz = peaks.get("sm_max_mhz", 1965.0) / 1e3
+    # FP64 SIMT peak (nominal, no measured FP64 figure exists): 148 SM x 64 FP64 lanes x 2 (FMA) x max clock
+    fp64_peak = 148 * 64 * 2 * clk_ghz / 1e3
+    # algorithmic FP64 flops per unit, counted from the reference source (kernels.py):
+    #   exact sample evaluation (camera transform :305-307 + NDC projection :314-315) 26
+    #   cone test (:330-337) 14, depth test (:323-327 + bilinear :231-261) 24
+    #   texel pair (3 edge functions :107-109, 23) + covered texel (l, inv_w, 1/inv_w :119-125, 9)
+    fl = {"k_samples<mark>": 26 * st["exact_evals"] + 14 * st["ndc_candidates"],
+          "k_texels": 23 * st["texel_pairs"] + 9 * st["covered_pairs"],
+          "k_samples<accumulate>": 26 * st["exact_evals"] + 14 * st["ndc_candidates"] + 24 * st["cone_candidates"]}
+    times = {"k_samples<mark>": tm.mark_ms, "k_texels": tm.texel_ms, "k_samples<accumulate>": tm.accumulate_ms,
+             "k_tri_setup": tm.cull_ms}
+    dom = max(times, key=times.get)
+    dom_flops = fl.get(dom, 0)
+    ach = dom_flops / (times[dom] / 1e3) / 1e12 if times[dom] else None
+    roof = {"bound": "fp64", "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s",
+            "frac": (ach / fp64_peak) if ach else None, "traffic": None, "kernel": dom,
+            "kernel_ms_per_step": times[dom], "kernel_share": times[dom] / step_ms,
+            "algorithmic_flops_per_step": dom_flops,
+            "peak_kind": "nominal FP64 FMA peak at max SM clock (MEASURED_PEAKS.json has no FP64 figure)",
+            "work": st}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:

@@ -122,12 +122,19 @@ int gm_plan_accumulate(gm_plan* plan, const double* fixations, int64_t F, const 
                        GmTimings* timings, gm_progress_fn progress, void* user, int64_t* bad_fixation);
 
 /* Device-resident replay (bench): compute the F fixations' setup records once
- * into HBM, then gm_plan_run repeats the whole generation from them;
- * device_ms = CUDA-event time of the pass on the plan's stream. */
+ * into HBM, then gm_plan_run repeats the whole generation from them (flags
+ * as GmConfig.flags); device_ms = CUDA-event time of the pass on the plan's
+ * stream. */
 int gm_plan_prepare(gm_plan* plan, const double* fixations, int64_t F, const GmConfig* cfg, int64_t* bad_fixation);
-int gm_plan_run(gm_plan* plan, int reset, GmTimings* timings, float* device_ms);
+int gm_plan_run(gm_plan* plan, int reset, int flags, GmTimings* timings, float* device_ms);
 /* Write `bytes` of scratch on the plan's stream to evict L2 between repetitions. */
 int gm_plan_flush_l2(gm_plan* plan, int64_t bytes);
+
+/* Work counters of the last pass run with GmConfig.flags & 1: 16 x uint64 =
+ * super-chunk tests, chunk tests, exact sample evaluations, NDC-filtered
+ * samples, in-cone candidates, visible contributions, marked texels, exact
+ * (texel, triangle) evaluations, covered pairs, reserved. */
+int gm_plan_stats(gm_plan* plan, unsigned long long* out);
 
 /* Running global max (density.py:192) of the plan's values. */
 int gm_plan_max(gm_plan* plan, double* gmax);

@@ -45,6 +45,10 @@ class GmTimings(ctypes.Structure):
 FIX_EXACT_DOUBLES = 26
 FIX_CULL_FLOATS = 20
 
+GM_FLAG_STATS = 1
+STAT_NAMES = ["l1_tests", "l2_tests", "exact_evals", "ndc_candidates", "cone_candidates", "visible",
+              "texels", "texel_pairs", "covered_pairs"]
+
 PROGRESS_FN = ctypes.CFUNCTYPE(None, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p)
 
 # every C-ABI entry point (include/gazemap_b200.h) -> (restype, argtypes)
@@ -67,8 +71,10 @@ SIGNATURES = {
     "gm_plan_accumulate": (ctypes.c_int, [_VP, _D, ctypes.c_int64, ctypes.POINTER(GmConfig), ctypes.c_int,
                                           ctypes.POINTER(GmTimings), PROGRESS_FN, ctypes.c_void_p, _I64]),
     "gm_plan_prepare": (ctypes.c_int, [_VP, _D, ctypes.c_int64, ctypes.POINTER(GmConfig), _I64]),
-    "gm_plan_run": (ctypes.c_int, [_VP, ctypes.c_int, ctypes.POINTER(GmTimings), ctypes.POINTER(ctypes.c_float)]),
+    "gm_plan_run": (ctypes.c_int, [_VP, ctypes.c_int, ctypes.c_int, ctypes.POINTER(GmTimings),
+                                   ctypes.POINTER(ctypes.c_float)]),
     "gm_plan_flush_l2": (ctypes.c_int, [_VP, ctypes.c_int64]),
+    "gm_plan_stats": (ctypes.c_int, [_VP, ctypes.POINTER(ctypes.c_uint64)]),
     "gm_plan_max": (ctypes.c_int, [_VP, _D]),
     "gm_plan_read": (ctypes.c_int, [_VP, _D, _D, ctypes.c_double]),
     "gm_plan_write": (ctypes.c_int, [_VP, _D]),

@@ -150,7 +150,13 @@ __device__ __forceinline__ int project_triangle(const double* tw, const GmFixExa
             sy[m] = (1.0 - ndc_y) * half_h;
             iw[m] = 1.0 / w;
         }
-        if (ok && make_screen_tri(sx, sy, iw, W, H, &out[n_out])) n_out++;
+        if (ok && make_screen_tri(sx, sy, iw, W, H, &out[n_out])) {
+            // depth written at any covered pixel = 1 / (convex combination of 1/w) >= min w
+            // (up to a few ulps, far inside the 1e-9 margin k_texels applies)
+            const double w0 = -vout[0][2], w1 = -vout[k + 1][2], w2 = -vout[k + 2][2];
+            out[n_out].minw = __double2float_rd(fmin(w0, fmin(w1, w2)));
+            n_out++;
+        }
     }
     return n_out;
 }

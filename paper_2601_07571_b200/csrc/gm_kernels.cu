@@ -34,6 +34,8 @@
 #include "gm_device.cuh"
 #include "gm_types.h"
 
+#define GM_MAX_BATCH 1024
+
 extern "C" void gm_setup_consts(double theta, int filtering, int width, int height, GmSetupConsts* c);
 extern "C" int64_t gm_setup_batch(const double* fx, int64_t F, const GmSetupConsts* c, GmFixExact* ex,
                                   GmFixCull* cull, int threads);
@@ -181,11 +183,11 @@ __global__ void k_tri_spheres(const double* __restrict__ tw, int64_t T, float4* 
 // 32 consecutive samples (sample chunks).
 __global__ void k_group_spheres(const float4* __restrict__ member, const double* __restrict__ px,
                                 const double* __restrict__ py, const double* __restrict__ pz, int64_t n,
-                                float4* __restrict__ out) {
+                                float4* __restrict__ out, int group) {
     int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    int64_t first = g * 32;
+    int64_t first = g * group;
     if (first >= n) return;
-    int64_t last = first + 32 < n ? first + 32 : n;
+    int64_t last = first + group < n ? first + group : n;
     double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
     for (int64_t i = first; i < last; i++) {
         double p[3], r;
@@ -286,7 +288,6 @@ __global__ void __launch_bounds__(256) k_tri_setup(const double* __restrict__ tw
         int at = base + (incl - n);
         for (int q = 0; q < n; q++) {
             if (at + q < ts.cap_seg) {
-                out[q].fslot = f;
                 seg[at + q] = out[q];
                 segb[at + q] = make_uint2((uint32_t)out[q].x0 | ((uint32_t)out[q].x1 << 16),
                                           (uint32_t)out[q].y0 | ((uint32_t)out[q].y1 << 16));
@@ -299,15 +300,111 @@ __global__ void __launch_bounds__(256) k_tri_setup(const double* __restrict__ tw
 
 // Per-batch z-buffer store: only the texels some candidate's depth_match will
 // read are ever written (mask bit set by k_samples<true>, value by k_texels).
-struct DepthView {
-    double* depth;    // [B][H][W]
-    uint32_t* mask;   // [B][H][wwords]
-    int W, H, wwords;
+// Coarse screen bins (cb x cb pixels, cb a power of two >= 64) of every
+// fixation's screen triangles, so a k_texels tile scans only the triangles of
+// its coarse bin.  One CTA per fixation slot: count per bin in shared memory,
+// scan, fill.  Per-fixation CSR in citems[f * cap_items ...]; if the items do
+// not fit, covf[f] = 1 and k_texels scans the fixation's whole list instead.
+#define GM_MAX_CBINS 1024
+struct CoarseBins {
+    int* items;   // [B][cap_items]
+    int* off;     // [B][GM_MAX_CBINS + 1]
+    int* ovf;     // [B]
+    int64_t cap_items;
+    int shift, ncx, ncy;
 };
 
-// kernels.py:219-285 depth_match on texels that k_texels evaluated.
-__device__ __forceinline__ bool depth_match_tex(const double* __restrict__ dep, int W, int H, double gx, double gy,
-                                                int bx0, int bx1, int by0, int by1, double d, double eps) {
+__global__ void __launch_bounds__(256) k_coarse(TriStore ts, CoarseBins cb, const long long* __restrict__ fail,
+                                                long long b0) {
+    __shared__ int s_cnt[GM_MAX_CBINS];
+    __shared__ int s_off[GM_MAX_CBINS + 1];
+    if (*fail <= b0) return;
+    const int f = blockIdx.x;
+    const int nbins = cb.ncx * cb.ncy;
+    const int n = min(ts.count[f], (int)ts.cap_seg);
+    const uint2* segb = ts.bbox + (int64_t)f * ts.cap_seg;
+    for (int b = threadIdx.x; b < nbins; b += blockDim.x) s_cnt[b] = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const uint2 bb = segb[i];
+        const int bx0 = (bb.x & 0xffff) >> cb.shift, bx1 = (bb.x >> 16) >> cb.shift;
+        const int by0 = (bb.y & 0xffff) >> cb.shift, by1 = (bb.y >> 16) >> cb.shift;
+        for (int by = by0; by <= by1; by++)
+            for (int bx = bx0; bx <= bx1; bx++) atomicAdd(&s_cnt[by * cb.ncx + bx], 1);
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {  // warp scan over <= 1024 bins
+        const int lane = threadIdx.x;
+        int carry = 0;
+        for (int b0s = 0; b0s < nbins; b0s += 32) {
+            const int b = b0s + lane;
+            const int v = b < nbins ? s_cnt[b] : 0;
+            int incl = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += t;
+            }
+            if (b < nbins) s_off[b] = carry + incl - v;
+            carry += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        if (lane == 0) s_off[nbins] = carry;
+    }
+    __syncthreads();
+    const int total = s_off[nbins];
+    int* off = cb.off + (int64_t)f * (GM_MAX_CBINS + 1);
+    for (int b = threadIdx.x; b <= nbins; b += blockDim.x) off[b] = s_off[b];
+    if (total > cb.cap_items) {
+        if (threadIdx.x == 0) cb.ovf[f] = 1;
+        return;
+    }
+    if (threadIdx.x == 0) cb.ovf[f] = 0;
+    for (int b = threadIdx.x; b < nbins; b += blockDim.x) s_cnt[b] = 0;
+    __syncthreads();
+    int* items = cb.items + (int64_t)f * cb.cap_items;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const uint2 bb = segb[i];
+        const int bx0 = (bb.x & 0xffff) >> cb.shift, bx1 = (bb.x >> 16) >> cb.shift;
+        const int by0 = (bb.y & 0xffff) >> cb.shift, by1 = (bb.y >> 16) >> cb.shift;
+        for (int by = by0; by <= by1; by++)
+            for (int bx = bx0; bx <= bx1; bx++) {
+                const int b = by * cb.ncx + bx;
+                items[s_off[b] + atomicAdd(&s_cnt[b], 1)] = i;
+            }
+    }
+}
+
+#define TW 32      // k_texels tile width (pixels) = warp lanes
+#define TH 16      // k_texels tile height (pixels)
+
+struct DepthView {
+    double* depth;    // [B][H][W]: marked texels only
+    uint32_t* mask;   // [B][H][wwords]: texels the depth tests will read
+    int W, H, wwords;
+    unsigned long long* stats;  // optional work counters (GM_STAT_*), nullptr = off
+};
+
+// Work counters filled when GmConfig.flags & GM_FLAG_STATS (bench roofline).
+enum {
+    GM_STAT_L1_TESTS = 0,    // super-chunk x fixation sphere tests (warp ballots x 32)
+    GM_STAT_L2_TESTS = 1,    // chunk x fixation sphere tests
+    GM_STAT_EXACT = 2,       // exact per-sample camera transform + NDC filter evaluations
+    GM_STAT_NDC = 3,         // samples passing the NDC filter (the reference's filtered set)
+    GM_STAT_CANDIDATES = 4,  // NDC and in the 4-sigma cone (depth test performed)
+    GM_STAT_VISIBLE = 5,     // depth test passed (contributions added)
+    GM_STAT_TEXELS = 6,      // marked texels evaluated
+    GM_STAT_PAIRS = 7,       // (texel, screen triangle) exact evaluations
+    GM_STAT_COVERED = 8,     // pairs where the triangle covers the texel
+    GM_STAT_N = 16
+};
+#define GM_FLAG_STATS 1
+
+// kernels.py:219-285 depth_match, reading the texels k_texels evaluated
+// (the 3x3 block around rint(g), which contains the bilinear quad).
+__device__ __forceinline__ bool depth_test(const DepthView& dv, int f, double gx, double gy, int bx0, int bx1,
+                                           int by0, int by1, double d, double eps) {
+    const int W = dv.W, H = dv.H;
+    const double* dep = dv.depth + (int64_t)f * W * H;
     if (W > 1 && H > 1) {
         long long x0 = x86_i64(floor(gx));
         if (x0 < 0) x0 = 0;
@@ -336,7 +433,7 @@ __device__ __forceinline__ bool depth_match_tex(const double* __restrict__ dep, 
     for (int yy = by0; yy <= by1; yy++) {
         const double* row = dep + (int64_t)yy * W;
         for (int xx = bx0; xx <= bx1; xx++) {
-            double t = row[xx];
+            const double t = row[xx];
             if (isfinite(t)) {
                 double diff = fabs(t - d);
                 if (diff < best) best = diff;
@@ -358,21 +455,68 @@ __device__ __forceinline__ bool depth_match_tex(const double* __restrict__ dep, 
 // The cone test (kernels.py:330-339) runs before depth_match (:326): every
 // condition is conjunctive and side-effect free, so the contributing set and
 // the weights are unchanged.
+// Level 1 of the sample-side fixation cull, once per batch: warp per
+// super-chunk (8 chunks = 256 consecutive samples), lane-parallel sphere tests
+// against all fixations of the batch -> lvl1[sc][g] ballots and the number of
+// fixations that can touch the super-chunk (the work estimate used to order
+// the sample passes, heaviest first).
+__global__ void __launch_bounds__(256) k_level1(const float4* __restrict__ supers, int64_t n_supers,
+                                                const GmFixCull* __restrict__ culls, int B,
+                                                uint32_t* __restrict__ lvl1, int* __restrict__ count,
+                                                int* __restrict__ order, const long long* __restrict__ fail,
+                                                long long b0) {
+    const int lane = threadIdx.x & 31;
+    const int64_t sc = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (sc >= n_supers) return;
+    const int ngroups = (B + 31) >> 5;
+    int total = 0;
+    if (*fail > b0) {
+        const float4 ssph = supers[sc];
+        for (int g = 0; g < ngroups; g++) {
+            const int myf = g * 32 + lane;
+            const unsigned m = __ballot_sync(0xffffffffu, myf < B && sphere_visible(culls[myf], ssph, false));
+            if (lane == 0) lvl1[sc * ngroups + g] = m;
+            total += __popc(m);
+        }
+    }
+    if (lane == 0) {
+        count[sc] = total;
+        order[sc] = (int)sc;
+    }
+}
+
 template <bool MARK>
 __global__ void __launch_bounds__(256) k_samples(const double* __restrict__ px, const double* __restrict__ py,
                                                  const double* __restrict__ pz, const float4* __restrict__ chunks,
-                                                 int64_t N, int64_t n_chunks, const GmFixExact* __restrict__ fixes,
+                                                 const uint32_t* __restrict__ lvl1, const int* __restrict__ order,
+                                                 int* __restrict__ work, int64_t N, int64_t n_chunks,
+                                                 int64_t n_supers, const GmFixExact* __restrict__ fixes,
                                                  const GmFixCull* __restrict__ culls, int B, DepthView dv,
                                                  double inv_sigma, double eps_abs, double eps_rel,
                                                  double* __restrict__ values, const long long* __restrict__ fail,
                                                  long long b0) {
     if (*fail <= b0) return;  // this batch overflowed the triangle store: the host redoes it
     const int lane = threadIdx.x & 31;
-    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const int ngroups = (B + 31) >> 5;  // <= 32 (B <= GM_MAX_BATCH)
     const int W = dv.W, H = dv.H;
     const double Wd = (double)W, Hd = (double)H;
     const double lo = -1.0 - GM_NDC_SLACK, hi = 1.0 + GM_NDC_SLACK;
-    for (int64_t ch = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); ch < n_chunks; ch += warps) {
+    const int64_t n_items = n_supers * 8;
+    unsigned long long c_l1 = 0, c_l2 = 0, c_exact = 0, c_ndc = 0, c_cand = 0, c_vis = 0;
+    // persistent warps; items = chunks of the super-chunks in descending-work
+    // order (k_level1 + radix sort), claimed one at a time
+    for (;;) {
+        int item = 0;
+        if (lane == 0) item = atomicAdd(work, 1);
+        item = __shfl_sync(0xffffffffu, item, 0);
+        if (item >= n_items) break;
+        const int64_t sc = order[item >> 3];
+        const int64_t ch = sc * 8 + (item & 7);
+        if (ch >= n_chunks) continue;
+        const unsigned l1 = lane < ngroups ? lvl1[sc * ngroups + lane] : 0u;  // lane g: group g
+        c_l1 += 1;
+        if (!__any_sync(0xffffffffu, l1 != 0u)) continue;
+        {
         const int64_t i = ch * 32 + lane;
         const bool valid = i < N;
         double wx = 0.0, wy = 0.0, wz = 0.0, v = 0.0;
@@ -383,9 +527,13 @@ __global__ void __launch_bounds__(256) k_samples(const double* __restrict__ px, 
             if (!MARK) v = values[i];
         }
         const float4 sph = chunks[ch];
-        for (int g = 0; g < B; g += 32) {
-            const int myf = g + lane;
-            bool pass = myf < B && sphere_visible(culls[myf], sph, false);
+        for (int gi = 0; gi < ngroups; gi++) {
+            const unsigned sm = __shfl_sync(0xffffffffu, l1, gi);
+            if (!sm) continue;
+            const int g = gi * 32;
+            // level 2: this chunk's 32 samples against the fixations that passed level 1
+            bool pass = ((sm >> lane) & 1u) && sphere_visible(culls[g + lane], sph, false);
+            c_l2 += (sm >> lane) & 1u;
             unsigned mask = __ballot_sync(0xffffffffu, pass);
             while (mask) {
                 const int j = __ffs(mask) - 1;
@@ -393,6 +541,7 @@ __global__ void __launch_bounds__(256) k_samples(const double* __restrict__ px, 
                 if (!valid) continue;
                 const int f = g + j;
                 const GmFixExact& F = fixes[f];
+                c_exact++;
                 // kernels.py:305-319
                 double x = F.rot[0] * wx + F.rot[1] * wy + F.rot[2] * wz + F.trans[0];
                 double y = F.rot[3] * wx + F.rot[4] * wy + F.rot[5] * wz + F.trans[1];
@@ -405,6 +554,7 @@ __global__ void __launch_bounds__(256) k_samples(const double* __restrict__ px, 
                 double ndc_y = (F.p11 * y + F.p12 * z) / w;
                 if (ndc_x < lo || ndc_x > hi) continue;
                 if (ndc_y < lo || ndc_y > hi) continue;
+                c_ndc++;
                 // kernels.py:330-339 (moved before the depth test)
                 double d1 = x * F.gaze[0] + y * F.gaze[1] + z * F.gaze[2];
                 if (d1 <= 0.0) continue;
@@ -412,6 +562,7 @@ __global__ void __launch_bounds__(256) k_samples(const double* __restrict__ px, 
                 if (d2sq < 0.0) d2sq = 0.0;
                 double ratio_sq = d2sq * inv_sigma * inv_sigma / (d1 * d1);
                 if (ratio_sq > 16.0) continue;
+                c_cand++;
                 // texel coordinates (kernels.py:327, :231-232, :267-276)
                 double gx = (ndc_x + 1.0) * 0.5 * Wd - 0.5;
                 double gy = (1.0 - ndc_y) * 0.5 * Hd - 0.5;
@@ -424,9 +575,10 @@ __global__ void __launch_bounds__(256) k_samples(const double* __restrict__ px, 
                 int bx0 = (int)max(cx - 1, 0LL), bx1 = (int)min(cx + 1, (long long)W - 1);
                 int by0 = (int)max(cy - 1, 0LL), by1 = (int)min(cy + 1, (long long)H - 1);
                 if (MARK) {
+                    // the 3x3 block depth_match may read (it contains the bilinear quad)
                     uint32_t* m = dv.mask + (int64_t)f * H * dv.wwords;
-                    unsigned long long bits = ((1ull << (bx1 - bx0 + 1)) - 1ull) << (bx0 & 31);
-                    int w0 = bx0 >> 5;
+                    const unsigned long long bits = ((1ull << (bx1 - bx0 + 1)) - 1ull) << (bx0 & 31);
+                    const int w0 = bx0 >> 5;
                     for (int yy = by0; yy <= by1; yy++) {
                         uint32_t* row = m + (int64_t)yy * dv.wwords + w0;
                         atomicOr(row, (uint32_t)bits);
@@ -437,157 +589,244 @@ __global__ void __launch_bounds__(256) k_samples(const double* __restrict__ px, 
                 // kernels.py:323-329
                 double eps = eps_abs;
                 if (eps_rel * d > eps) eps = eps_rel * d;
-                const double* dep = dv.depth + (int64_t)f * W * H;
-                if (!depth_match_tex(dep, W, H, gx, gy, bx0, bx1, by0, by1, d, eps)) continue;
+                if (!depth_test(dv, f, gx, gy, bx0, bx1, by0, by1, d, eps)) continue;
+                c_vis++;
                 v += F.amp * exp(-0.5 * ratio_sq);  // kernels.py:340
             }
         }
         if (!MARK && valid) values[i] = v;
+        }
+    }
+    if (dv.stats) {
+        if (MARK) {
+            if (lane == 0) atomicAdd(dv.stats + GM_STAT_L1_TESTS, c_l1 * (unsigned long long)B);
+            atomicAdd(dv.stats + GM_STAT_L2_TESTS, c_l2);
+            atomicAdd(dv.stats + GM_STAT_EXACT, c_exact);
+            atomicAdd(dv.stats + GM_STAT_NDC, c_ndc);
+            atomicAdd(dv.stats + GM_STAT_CANDIDATES, c_cand);
+        } else {
+            atomicAdd(dv.stats + GM_STAT_VISIBLE, c_vis);
+        }
     }
 }
 
-// Fixation-major evaluation of the marked texels.  One CTA of 512 threads per
-// (fixation, 64x64-pixel tile); warp w owns the 16x16 sub-bin w of the tile.
-// The CTA scans the fixation's screen triangles (bbox array, coalesced), keeps
-// those overlapping the tile, stages their records in shared memory TX_CAP at
-// a time and bins them into the 16 sub-bins.  Each warp then walks its
-// sub-bin's triangles; every (triangle, marked texel inside its bbox) pair is
-// pushed to a per-warp ring queue and the queue is drained 32 pairs at a time
-// (one pair per lane: full SIMT use of the FP64 pipe), each pair folding its
-// depth into the texel's shared-memory minimum (atomicMin on the bit pattern:
-// non-negative doubles order like their bits).  The result is exactly the
-// value kernels.rasterize leaves in that pixel (same per-pixel arithmetic).
-#define TX_TILE 64
-#define TX_CAP 96
-#define TX_Q 256
-#define TX_DYN_SMEM (16 * 256 * 8 + 16 * TX_Q * 4)  // s_best + s_q
-__global__ void __launch_bounds__(512) k_texels(TriStore ts, DepthView dv, int tiles_x, int tiles_per_fix,
-                                                const GmFixExact* __restrict__ fixes, long long b0) {
-    __shared__ __align__(16) GmScreenTri s_tri[TX_CAP];
+// Fixation-major evaluation of the marked texels.  Every warp is an
+// independent work item (fixation, 32x16-pixel tile), lane = pixel column, so
+// there are no CTA barriers and no atomics:
+//   1. the tile's rows of the candidate-texel mask are transposed with ballots
+//      (lane c gets the 16-bit row mask of column c);
+//   2. the fixation's screen triangles are scanned through their bbox array
+//      (coalesced); overlapping ones are staged in the warp's shared slice,
+//      TW_CAP records at a time;
+//   3. per staged triangle every lane forms the marked rows of its column inside
+//      the bbox and pushes (triangle, row, column) pairs to the warp's ring
+//      queue; the queue is drained 32 pairs per round, one pair per lane (full
+//      SIMT use of the FP64 pipe), each pair folding its depth into the texel's
+//      minimum in shared memory (same-texel lanes of a round are serialised
+//      with __match_any_sync);
+//   4. the minima of the marked texels are stored to the z-buffer array.
+// The values are exactly what kernels.rasterize leaves in those pixels: same
+// per-pixel arithmetic (texel_depth), min over every covering triangle.
+#define TW_CAP 32
+#define TW_Q 256
+#define TW_WARPS 8
+struct __align__(16) TexelWarpSmem {
+    GmScreenTri rec[TW_CAP];
+    double best[TH * TW];
+    uint32_t q[TW_Q];
+    int idx[TW_CAP + 32];
+};
+#define TX_DYN_SMEM (TW_WARPS * (int)sizeof(TexelWarpSmem))
+
+__global__ void __launch_bounds__(TW_WARPS * 32) k_texels(TriStore ts, DepthView dv, CoarseBins cb, int tiles_x,
+                                                          int tiles_per_fix, int64_t n_items,
+                                                          const GmFixExact* __restrict__ fixes, long long b0) {
     extern __shared__ __align__(16) unsigned char tx_dyn[];
-    auto s_best = reinterpret_cast<unsigned long long (*)[256]>(tx_dyn);
-    auto s_q = reinterpret_cast<uint32_t (*)[TX_Q]>(tx_dyn + 16 * 256 * 8);
-    __shared__ uint32_t s_mask[TX_TILE][2];
-    __shared__ int s_sel[512];
-    __shared__ uint8_t s_list[16][TX_CAP];
-    __shared__ int s_cnt[16];
-    __shared__ int s_nsel;
-    if (*ts.fail <= b0) return;
-    const int f = blockIdx.x / tiles_per_fix;
-    const int tile = blockIdx.x - f * tiles_per_fix;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    TexelWarpSmem& S = reinterpret_cast<TexelWarpSmem*>(tx_dyn)[warp];
+    const int64_t item = (int64_t)blockIdx.x * TW_WARPS + warp;
+    if (item >= n_items || *ts.fail <= b0) return;
+    const int f = (int)(item / tiles_per_fix);
+    const int tile = (int)(item - (int64_t)f * tiles_per_fix);
     const int W = dv.W, H = dv.H;
-    const int xb = (tile % tiles_x) * TX_TILE, yb = (tile / tiles_x) * TX_TILE;
-    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
-    const uint32_t* m = dv.mask + (int64_t)f * H * dv.wwords;
-    {
-        uint32_t v = 0;
-        if (t < 2 * TX_TILE) {
-            int yy = yb + (t >> 1), ww = (xb >> 5) + (t & 1);
-            if (yy < H && ww < dv.wwords) v = m[(int64_t)yy * dv.wwords + ww];
-            s_mask[t >> 1][t & 1] = v;
-        }
-        if (!__syncthreads_or(v != 0u)) return;
-    }
-    // lane -> column (lane & 15) and rows (lane >> 4) * 8 .. + 7 of the warp's sub-bin
-    const int sbx = warp & 3, sby = warp >> 2;
-    const int lcol = lane & 15, lrow0 = (lane >> 4) * 8;
-    const int lx = sbx * 16 + lcol;
-    const int col = xb + lx, row0 = yb + sby * 16 + lrow0;
+    const int xb = (tile % tiles_x) * TW, yb = (tile / tiles_x) * TH;
+    const unsigned FULL = 0xffffffffu;
+    // 1. lane r < TH loads mask row yb + r (one word: xb is a multiple of 32)
+    uint32_t wr = 0;
+    if (lane < TH && yb + lane < H) wr = dv.mask[((int64_t)f * H + yb + lane) * dv.wwords + (xb >> 5)];
+    if (!__any_sync(FULL, wr != 0u)) return;
     uint32_t need = 0;
 #pragma unroll
-    for (int r = 0; r < 8; r++) need |= ((s_mask[sby * 16 + lrow0 + r][lx >> 5] >> (lx & 31)) & 1u) << r;
-#pragma unroll
-    for (int r = 0; r < 8; r++) s_best[warp][(lrow0 + r) * 16 + lcol] = 0x7ff0000000000000ull;  // +inf
-    const bool warp_needs = __any_sync(0xffffffffu, need != 0u);
+    for (int c = 0; c < 32; c++) {
+        const uint32_t b = __ballot_sync(FULL, (wr >> c) & 1u);
+        if (lane == c) need = b & ((1u << TH) - 1u);
+    }
+    for (uint32_t m = need; m; m &= m - 1) S.best[(__ffs(m) - 1) * TW + lane] = CUDART_INF;
+    const int col = xb + lane;
     const double near_ = fixes[f].near_, far_ = fixes[f].far_;
-    const int n = min(ts.count[f], (int)ts.cap_seg);
     const GmScreenTri* seg = ts.tris + (int64_t)f * ts.cap_seg;
     const uint2* segb = ts.bbox + (int64_t)f * ts.cap_seg;
-    const int xe = xb + TX_TILE - 1, ye = yb + TX_TILE - 1;
-    const int sx0 = xb + sbx * 16, sy0 = yb + sby * 16;  // sub-bin origin (pixels)
-    unsigned qhead = 0, qtail = 0;  // warp-uniform ring indices
-    auto drain = [&](unsigned upto) {  // evaluate queued pairs while >= upto are pending
-        while (qtail - qhead >= upto && qtail != qhead) {
-            unsigned k = qhead + lane;
-            if (k < qtail) {
-                uint32_t e = s_q[warp][k & (TX_Q - 1)];
-                const GmScreenTri& T = s_tri[e >> 8];
-                int el = e & 255;
-                double d = texel_depth(T, sx0 + (el & 15), sy0 + (el >> 4), near_, far_);
-                if (d < CUDART_INF) atomicMin(&s_best[warp][el], (unsigned long long)__double_as_longlong(d));
+    // candidate triangles: the tile's coarse bin (or the whole list on overflow)
+    const int* clist = nullptr;
+    int n = min(ts.count[f], (int)ts.cap_seg);
+    if (!cb.ovf[f]) {
+        const int* off = cb.off + (int64_t)f * (GM_MAX_CBINS + 1);
+        const int b = (yb >> cb.shift) * cb.ncx + (xb >> cb.shift);
+        clist = cb.items + (int64_t)f * cb.cap_items + off[b];
+        n = off[b + 1] - off[b];
+    }
+    const int xe = xb + TW - 1, ye = yb + TH - 1;
+    unsigned qh = 0, qt = 0;  // warp-uniform ring indices
+    unsigned long long c_pairs = 0, c_cov = 0;
+
+    auto drain = [&](bool all) {
+        __syncwarp();
+        while (qt - qh >= (all ? 1u : 32u)) {
+            const unsigned k = qh + lane;
+            const bool valid = k < qt;
+            double d = CUDART_INF;
+            int key = 0x10000 + lane;
+            if (valid) {
+                const uint32_t e = S.q[k & (TW_Q - 1)];
+                const int r = (e >> 5) & 31, c = e & 31;
+                d = texel_depth(S.rec[e >> 10], xb + c, yb + r, near_, far_);
+                key = r * TW + c;
+                c_pairs++;
+                c_cov += d < CUDART_INF;
             }
-            qhead += min(32u, qtail - qhead);
+            const unsigned grp = __match_any_sync(FULL, key);
+            const bool upd = valid && d < CUDART_INF;
+            if (grp == (1u << lane)) {
+                if (upd && d < S.best[key]) S.best[key] = d;
+            } else {
+                for (unsigned mm = grp; mm; mm &= mm - 1) {
+                    if (lane == __ffs(mm) - 1 && upd && d < S.best[key]) S.best[key] = d;
+                    __syncwarp(grp);
+                }
+            }
+            qh += min(32u, qt - qh);
+            __syncwarp();
         }
     };
-    for (int base = 0; base < n; base += 512) {
-        if (t == 0) s_nsel = 0;
-        __syncthreads();
-        const int i = base + t;
-        if (i < n) {
-            uint2 bb = segb[i];
-            int x0 = bb.x & 0xffff, x1 = bb.x >> 16, y0 = bb.y & 0xffff, y1 = bb.y >> 16;
-            if (!(x1 < xb || x0 > xe || y1 < yb || y0 > ye)) s_sel[atomicAdd(&s_nsel, 1)] = i;
+
+    // stage S.idx[0..kend) and evaluate their pairs, nearest triangles first
+    auto process = [&](int kend) {
+        __syncwarp();
+        for (int q = lane; q < kend * 6; q += 32) {
+            const int ti = q / 6, part = q - ti * 6;
+            reinterpret_cast<uint4*>(&S.rec[ti])[part] = reinterpret_cast<const uint4*>(seg + S.idx[ti])[part];
         }
-        __syncthreads();
-        const int nsel = s_nsel;
-        for (int c0 = 0; c0 < nsel; c0 += TX_CAP) {
-            const int mcount = min(TX_CAP, nsel - c0);
-            for (int q = t; q < mcount * 6; q += 512) {
-                const int ti = q / 6, part = q - ti * 6;
-                reinterpret_cast<uint4*>(&s_tri[ti])[part] = reinterpret_cast<const uint4*>(seg + s_sel[c0 + ti])[part];
-            }
-            if (t < 16) s_cnt[t] = 0;
-            __syncthreads();
-            if (t < mcount) {  // bin the staged triangles into the 16 sub-bins
-                const GmScreenTri& T = s_tri[t];
-                int bx0 = max((int)T.x0 - xb, 0) >> 4, bx1 = min((int)T.x1 - xb, TX_TILE - 1) >> 4;
-                int by0 = max((int)T.y0 - yb, 0) >> 4, by1 = min((int)T.y1 - yb, TX_TILE - 1) >> 4;
-                for (int by = by0; by <= by1; by++)
-                    for (int bx = bx0; bx <= bx1; bx++) {
-                        int sb = by * 4 + bx;
-                        s_list[sb][atomicAdd(&s_cnt[sb], 1)] = (uint8_t)t;
-                    }
-            }
-            __syncthreads();
-            if (warp_needs) {
-                const int cnt = s_cnt[warp];
-                for (int k = 0; k < cnt; k++) {
-                    const int slot = s_list[warp][k];
-                    const GmScreenTri& T = s_tri[slot];
-                    uint32_t bits = 0;
-                    if (col >= T.x0 && col <= T.x1) {
-                        int lo = max((int)T.y0 - row0, 0), hi = min((int)T.y1 - row0, 7);
-                        if (lo <= hi) bits = need & (((1u << (hi - lo + 1)) - 1u) << lo);
-                    }
-                    int pc = __popc(bits), incl = pc;
+        __syncwarp();
+        // warp bitonic sort of the staged triangles by min depth (lane = slot)
+        float key = lane < kend ? S.rec[lane].minw : CUDART_INF_F;
+        int slot = lane;
 #pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        int v = __shfl_up_sync(0xffffffffu, incl, o);
-                        if (lane >= o) incl += v;
-                    }
-                    const unsigned total = (unsigned)__shfl_sync(0xffffffffu, incl, 31);
-                    if (qtail - qhead + total > TX_Q) drain(1);  // total <= 256 = TX_Q
-                    unsigned at = qtail + (unsigned)(incl - pc);
-                    while (bits) {
-                        int r = __ffs(bits) - 1;
-                        bits &= bits - 1;
-                        s_q[warp][at++ & (TX_Q - 1)] = ((uint32_t)slot << 8) | (uint32_t)((lrow0 + r) * 16 + lcol);
-                    }
-                    qtail += total;
-                    __syncwarp();
-                    drain(32);
+        for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+            for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                const float ok = __shfl_xor_sync(FULL, key, stride);
+                const int os = __shfl_xor_sync(FULL, slot, stride);
+                const bool up = ((lane & size) == 0);
+                const bool lower = (lane & stride) == 0;
+                const bool take = lower ? (up ? (ok < key || (ok == key && os < slot)) : (ok > key || (ok == key && os > slot)))
+                                        : (up ? (ok > key || (ok == key && os > slot)) : (ok < key || (ok == key && os < slot)));
+                if (take) {
+                    key = ok;
+                    slot = os;
                 }
-                drain(1);  // the staged records are replaced after this chunk
             }
-            __syncthreads();
         }
+        for (int kk = 0; kk < kend; kk++) {
+            const int k = __shfl_sync(FULL, slot, kk);
+            const GmScreenTri& T = S.rec[k];
+            uint32_t bits = 0;
+            if (col >= T.x0 && col <= T.x1) {
+                const int lo = max((int)T.y0 - yb, 0), hi = min((int)T.y1 - yb, TH - 1);
+                if (lo <= hi) bits = need & (((1u << (hi - lo + 1)) - 1u) << lo);
+            }
+            // early-out: a texel already holding a nearer depth than this triangle's
+            // minimum cannot change (its depths here are all >= minw)
+            if (bits) {
+                const double thr = (double)T.minw * (1.0 - 1e-9);
+                for (uint32_t m = bits; m; m &= m - 1) {
+                    const int r = __ffs(m) - 1;
+                    if (S.best[r * TW + lane] < thr) bits &= ~(1u << r);
+                }
+            }
+            if (!__any_sync(FULL, bits != 0u)) continue;
+            const int pc = __popc(bits);
+            int incl = pc;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v = __shfl_up_sync(FULL, incl, o);
+                if (lane >= o) incl += v;
+            }
+            const unsigned total = (unsigned)__shfl_sync(FULL, incl, 31);
+            if (total > TW_Q) {
+                // more marked texels under this bbox than the queue holds: each
+                // lane evaluates its own column (it owns those minima)
+                drain(true);
+                while (__any_sync(FULL, bits != 0u)) {
+                    if (bits) {
+                        const int r = __ffs(bits) - 1;
+                        bits &= bits - 1;
+                        const double d = texel_depth(T, col, yb + r, near_, far_);
+                        c_pairs++;
+                        c_cov += d < CUDART_INF;
+                        if (d < S.best[r * TW + lane]) S.best[r * TW + lane] = d;
+                    }
+                }
+                __syncwarp();
+                continue;
+            }
+            if (qt - qh + total > TW_Q) drain(true);
+            unsigned pos = qt + (unsigned)(incl - pc);
+            while (bits) {
+                const int r = __ffs(bits) - 1;
+                bits &= bits - 1;
+                S.q[pos++ & (TW_Q - 1)] = ((uint32_t)k << 10) | ((uint32_t)r << 5) | (uint32_t)lane;
+            }
+            qt += total;
+            drain(false);
+        }
+        drain(true);  // the staged records are replaced next
+    };
+
+    int cnt = 0;
+    for (int base = 0; base < n; base += 32) {
+        int i = base + lane;
+        bool sel = false;
+        if (i < n) {
+            if (clist) i = clist[i];
+            const uint2 bb = segb[i];
+            const int x0 = bb.x & 0xffff, x1 = bb.x >> 16, y0 = bb.y & 0xffff, y1 = bb.y >> 16;
+            sel = !(x1 < xb || x0 > xe || y1 < yb || y0 > ye);
+        }
+        const unsigned bal = __ballot_sync(FULL, sel);
+        if (sel) S.idx[cnt + __popc(bal & ((1u << lane) - 1u))] = i;
+        cnt += __popc(bal);
+        if (cnt >= TW_CAP) {
+            process(TW_CAP);
+            // keep the indices that did not fit (fewer than 32)
+            const int rest = cnt - TW_CAP;
+            const int keep = lane < rest ? S.idx[TW_CAP + lane] : 0;
+            __syncwarp();
+            if (lane < rest) S.idx[lane] = keep;
+            cnt = rest;
+        }
+    }
+    if (cnt > 0) process(cnt);
+    if (dv.stats) {
+        atomicAdd(dv.stats + GM_STAT_TEXELS, (unsigned long long)__popc(need));
+        atomicAdd(dv.stats + GM_STAT_PAIRS, c_pairs);
+        atomicAdd(dv.stats + GM_STAT_COVERED, c_cov);
     }
     if (need) {
         double* dep = dv.depth + (int64_t)f * W * H;
-#pragma unroll
-        for (int r = 0; r < 8; r++)
-            if ((need >> r) & 1u)
-                dep[(int64_t)(row0 + r) * W + col] = __longlong_as_double((long long)s_best[warp][(lrow0 + r) * 16 + lcol]);
+        for (uint32_t m = need; m; m &= m - 1) {
+            const int r = __ffs(m) - 1;
+            dep[(int64_t)(yb + r) * W + col] = S.best[r * TW + lane];
+        }
     }
 }
 
@@ -679,6 +918,14 @@ struct gm_plan {
     float4* d_csph = nullptr;
     double *d_px = nullptr, *d_py = nullptr, *d_pz = nullptr;
     float4* d_chunk = nullptr;
+    float4* d_super = nullptr;  // sphere per 8 chunks (256 samples)
+    int64_t n_supers = 0;
+    uint32_t* d_lvl1 = nullptr;  // [n_supers][B/32] level-1 ballots of the current batch
+    int *d_lcount = nullptr, *d_lorder = nullptr, *d_lcount2 = nullptr, *d_lorder2 = nullptr;
+    int* d_work = nullptr;       // [2] work counters of the two sample passes
+    void* d_sort_tmp = nullptr;
+    size_t sort_tmp_bytes = 0;
+    int64_t cap_lvl1 = 0;
     double* d_values = nullptr;
     // batch buffers: per-fixation setup (device + pinned host ring)
     int cap_B = 0;
@@ -699,7 +946,12 @@ struct gm_plan {
     double* d_depth = nullptr;   // [B][H][W] marked texels only
     uint32_t* d_mask = nullptr;  // [B][H][wwords]
     int64_t cap_depth = 0, cap_mask = 0;
+    int* d_citems = nullptr;  // coarse bins: [B][cap_citems]
+    int* d_coff = nullptr;    // [B][GM_MAX_CBINS + 1]
+    int* d_covf = nullptr;    // [B]
+    int64_t cap_citems = 0, cap_cB = 0;
     unsigned long long* d_max = nullptr;
+    unsigned long long* d_stats = nullptr;  // GM_STAT_N counters
     int host_threads = 8;
     // device-resident setup table (gm_plan_prepare)
     GmFixExact* d_fix_all = nullptr;
@@ -716,10 +968,14 @@ struct gm_plan {
 static void plan_free_scene(gm_plan* p) {
     cudaFree(p->d_tw); cudaFree(p->d_tsph); cudaFree(p->d_csph);
     cudaFree(p->d_px); cudaFree(p->d_py); cudaFree(p->d_pz);
-    cudaFree(p->d_chunk); cudaFree(p->d_values);
-    p->d_tw = nullptr; p->d_tsph = p->d_csph = p->d_chunk = nullptr;
+    cudaFree(p->d_chunk); cudaFree(p->d_values); cudaFree(p->d_super);
+    cudaFree(p->d_lvl1); cudaFree(p->d_lcount); cudaFree(p->d_lorder); cudaFree(p->d_lcount2);
+    cudaFree(p->d_lorder2); cudaFree(p->d_sort_tmp);
+    p->d_lvl1 = nullptr; p->d_lcount = p->d_lorder = p->d_lcount2 = p->d_lorder2 = nullptr;
+    p->d_sort_tmp = nullptr; p->sort_tmp_bytes = 0; p->cap_lvl1 = 0;
+    p->d_tw = nullptr; p->d_tsph = p->d_csph = p->d_chunk = p->d_super = nullptr;
     p->d_px = p->d_py = p->d_pz = p->d_values = nullptr;
-    p->T = p->n_clu = p->N = p->n_chunks = 0;
+    p->T = p->n_clu = p->N = p->n_chunks = p->n_supers = 0;
 }
 
 extern "C" int gm_plan_create(int device, gm_plan** out) {
@@ -736,9 +992,12 @@ extern "C" int gm_plan_create(int device, gm_plan** out) {
     cudaDeviceGetAttribute(&p->sms, cudaDevAttrMultiProcessorCount, device);
     CK(cudaFuncSetAttribute(k_texels, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
     CK(cudaMalloc(&p->d_max, sizeof(unsigned long long)));
+    CK(cudaMalloc(&p->d_stats, GM_STAT_N * sizeof(unsigned long long)));
+    CK(cudaMemset(p->d_stats, 0, GM_STAT_N * sizeof(unsigned long long)));
     CK(cudaMalloc(&p->d_fail, sizeof(long long)));
     CK(cudaMalloc(&p->d_maxcount, sizeof(int)));
     CK(cudaMalloc(&p->d_ntris, sizeof(unsigned long long)));
+    CK(cudaMalloc(&p->d_work, 2 * sizeof(int)));
     for (int r = 0; r < GM_RING; r++) CK(cudaEventCreateWithFlags(&p->h_ev[r], cudaEventDisableTiming));
     unsigned hc = std::thread::hardware_concurrency();
     p->host_threads = hc > 0 ? (int)hc : 8;
@@ -755,10 +1014,11 @@ extern "C" void gm_plan_destroy(gm_plan* p) {
     for (int r = 0; r < GM_RING; r++) {
         cudaFreeHost(p->h_fix[r]); cudaFreeHost(p->h_cull[r]); cudaEventDestroy(p->h_ev[r]);
     }
-    cudaFree(p->d_tris); cudaFree(p->d_bbox); cudaFree(p->d_count); cudaFree(p->d_fail); cudaFree(p->d_maxcount); cudaFree(p->d_ntris);
-    cudaFree(p->d_scan_tmp); cudaFree(p->d_max);
+    cudaFree(p->d_tris); cudaFree(p->d_bbox); cudaFree(p->d_count); cudaFree(p->d_fail); cudaFree(p->d_maxcount); cudaFree(p->d_ntris); cudaFree(p->d_work);
+    cudaFree(p->d_scan_tmp); cudaFree(p->d_max); cudaFree(p->d_stats);
     cudaFree(p->d_fix_all); cudaFree(p->d_cull_all); cudaFree(p->d_flush);
     cudaFree(p->d_depth); cudaFree(p->d_mask);
+    cudaFree(p->d_citems); cudaFree(p->d_coff); cudaFree(p->d_covf);
     cudaStreamDestroy(p->stream);
     delete p;
 }
@@ -809,6 +1069,7 @@ extern "C" int gm_plan_set_scene(gm_plan* p, int n_obj, const int64_t* tri_count
     p->N = N;
     p->n_clu = (T + 31) / 32;
     p->n_chunks = (N + 31) / 32;
+    p->n_supers = (p->n_chunks + 7) / 8;
     int rc;
     if ((rc = dev_alloc(&p->d_tw, (size_t)T * 9))) return rc;
     if ((rc = dev_alloc(&p->d_tsph, (size_t)T))) return rc;
@@ -817,6 +1078,18 @@ extern "C" int gm_plan_set_scene(gm_plan* p, int n_obj, const int64_t* tri_count
     if ((rc = dev_alloc(&p->d_py, (size_t)N))) return rc;
     if ((rc = dev_alloc(&p->d_pz, (size_t)N))) return rc;
     if ((rc = dev_alloc(&p->d_chunk, (size_t)p->n_chunks))) return rc;
+    if ((rc = dev_alloc(&p->d_super, (size_t)p->n_supers))) return rc;
+    if ((rc = dev_alloc(&p->d_lcount, (size_t)p->n_supers))) return rc;
+    if ((rc = dev_alloc(&p->d_lorder, (size_t)p->n_supers))) return rc;
+    if ((rc = dev_alloc(&p->d_lcount2, (size_t)p->n_supers))) return rc;
+    if ((rc = dev_alloc(&p->d_lorder2, (size_t)p->n_supers))) return rc;
+    {
+        size_t tb = 0;
+        cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, p->d_lcount, p->d_lcount2, p->d_lorder,
+                                                  p->d_lorder2, (int)std::max<int64_t>(p->n_supers, 1), 0, 11);
+        if ((rc = dev_alloc((char**)&p->d_sort_tmp, tb + 16))) return rc;
+        p->sort_tmp_bytes = tb + 16;
+    }
     if ((rc = dev_alloc(&p->d_values, (size_t)N))) return rc;
     if (T == 0) return GM_OK;
     double *d_local = nullptr, *d_M = nullptr;
@@ -859,10 +1132,13 @@ extern "C" int gm_plan_set_scene(gm_plan* p, int n_obj, const int64_t* tri_count
         sample_base += No;
     }
     k_tri_spheres<<<blocks_for(T, 256), 256, 0, s>>>(p->d_tw, T, p->d_tsph);
-    k_group_spheres<<<blocks_for(p->n_clu, 128), 128, 0, s>>>(p->d_tsph, nullptr, nullptr, nullptr, T, p->d_csph);
-    if (N > 0)
+    k_group_spheres<<<blocks_for(p->n_clu, 128), 128, 0, s>>>(p->d_tsph, nullptr, nullptr, nullptr, T, p->d_csph, 32);
+    if (N > 0) {
         k_group_spheres<<<blocks_for(p->n_chunks, 128), 128, 0, s>>>(nullptr, p->d_px, p->d_py, p->d_pz, N,
-                                                                      p->d_chunk);
+                                                                      p->d_chunk, 32);
+        k_group_spheres<<<blocks_for(p->n_supers, 128), 128, 0, s>>>(p->d_chunk, nullptr, nullptr, nullptr,
+                                                                      p->n_chunks, p->d_super, 8);
+    }
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(s));
     cudaFree(d_local); cudaFree(d_M); cudaFree(d_res); cudaFree(d_cnt); cudaFree(d_off);
@@ -904,10 +1180,32 @@ static int ensure_batch(gm_plan* p, int B, int W, int H, int64_t seg) {
         if ((rc = dev_alloc(&p->d_depth, (size_t)B * W * H))) return rc;
         p->cap_depth = (int64_t)B * W * H;
     }
+    if (B > p->cap_cB || 4 * p->cap_seg > p->cap_citems) {
+        const int64_t ci = 4 * std::max<int64_t>(p->cap_seg, seg);
+        if ((rc = dev_alloc(&p->d_citems, (size_t)B * ci))) return rc;
+        if ((rc = dev_alloc(&p->d_coff, (size_t)B * (GM_MAX_CBINS + 1)))) return rc;
+        if ((rc = dev_alloc(&p->d_covf, (size_t)B))) return rc;
+        p->cap_citems = ci;
+        p->cap_cB = B;
+    }
+    const int64_t lw = std::max<int64_t>(p->n_supers, 1) * ((B + 31) / 32);
+    if (lw > p->cap_lvl1) {
+        if ((rc = dev_alloc(&p->d_lvl1, (size_t)lw))) return rc;
+        p->cap_lvl1 = lw;
+    }
     return GM_OK;
 }
 
 typedef void (*gm_progress_fn)(int64_t done, int64_t total, void* user);
+
+// Coarse-bin geometry for a W x H buffer: cb = 64 px, doubled until <= GM_MAX_CBINS bins.
+static CoarseBins coarse_bins(gm_plan* p, int W, int H) {
+    int shift = 6;
+    while ((int64_t)((W + (1 << shift) - 1) >> shift) * ((H + (1 << shift) - 1) >> shift) > GM_MAX_CBINS) shift++;
+    CoarseBins cb{p->d_citems, p->d_coff, p->d_covf, p->cap_citems, shift, (W + (1 << shift) - 1) >> shift,
+                  (H + (1 << shift) - 1) >> shift};
+    return cb;
+}
 
 static inline double wall_ms() {
     return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
@@ -921,9 +1219,9 @@ static int enqueue_batch(gm_plan* p, const GmFixExact* d_fix, const GmFixCull* d
                          long long b0, double inv_sigma, const GmConfig* cfg, bool accumulate, cudaEvent_t* ev) {
     cudaStream_t s = p->stream;
     const int wwords = (W + 31) / 32;
-    const int tiles_x = (W + TX_TILE - 1) / TX_TILE, tiles_y = (H + TX_TILE - 1) / TX_TILE;
+    const int tiles_x = (W + TW - 1) / TW, tiles_y = (H + TH - 1) / TH;
     TriStore ts{p->d_tris, p->d_bbox, p->d_count, p->cap_seg, p->d_fail, p->d_maxcount, p->d_ntris};
-    DepthView dv{p->d_depth, p->d_mask, W, H, wwords};
+    DepthView dv{p->d_depth, p->d_mask, W, H, wwords, (cfg->flags & GM_FLAG_STATS) ? p->d_stats : nullptr};
     if (ev) CK(cudaEventRecord(ev[0], s));
     CK(cudaMemsetAsync(p->d_count, 0, sizeof(int) * nb, s));
     if (p->n_clu > 0) {
@@ -932,16 +1230,27 @@ static int enqueue_batch(gm_plan* p, const GmFixExact* d_fix, const GmFixCull* d
     }
     if (ev) CK(cudaEventRecord(ev[1], s));
     if (p->n_chunks > 0 && accumulate) {
-        int grid = (int)std::min<int64_t>((p->n_chunks + 7) / 8, (int64_t)p->sms * 64);
+        const int grid = p->sms * 8;  // persistent: 8 CTAs x 8 warps per SM
         CK(cudaMemsetAsync(p->d_mask, 0, sizeof(uint32_t) * (size_t)nb * H * wwords, s));
-        k_samples<true><<<grid, 256, 0, s>>>(p->d_px, p->d_py, p->d_pz, p->d_chunk, p->N, p->n_chunks, d_fix, d_cull,
-                                             nb, dv, inv_sigma, cfg->eps_abs, cfg->eps_rel, p->d_values, p->d_fail, b0);
+        CK(cudaMemsetAsync(p->d_work, 0, 2 * sizeof(int), s));
+        k_level1<<<blocks_for(p->n_supers, 8), 256, 0, s>>>(p->d_super, p->n_supers, d_cull, nb, p->d_lvl1,
+                                                             p->d_lcount, p->d_lorder, p->d_fail, b0);
+        size_t tb = p->sort_tmp_bytes;
+        CK(cub::DeviceRadixSort::SortPairsDescending(p->d_sort_tmp, tb, p->d_lcount, p->d_lcount2, p->d_lorder,
+                                                     p->d_lorder2, (int)p->n_supers, 0, 11, s));
+        k_samples<true><<<grid, 256, 0, s>>>(p->d_px, p->d_py, p->d_pz, p->d_chunk, p->d_lvl1, p->d_lorder2,
+                                             p->d_work, p->N, p->n_chunks, p->n_supers, d_fix, d_cull, nb, dv,
+                                             inv_sigma, cfg->eps_abs, cfg->eps_rel, p->d_values, p->d_fail, b0);
         if (ev) CK(cudaEventRecord(ev[2], s));
-        k_texels<<<nb * tiles_x * tiles_y, 512, TX_DYN_SMEM, s>>>(ts, dv, tiles_x, tiles_x * tiles_y, d_fix, b0);
+        const int64_t items = (int64_t)nb * tiles_x * tiles_y;
+        CoarseBins cbins = coarse_bins(p, W, H);
+        k_coarse<<<nb, 256, 0, s>>>(ts, cbins, p->d_fail, b0);
+        k_texels<<<(unsigned)((items + TW_WARPS - 1) / TW_WARPS), TW_WARPS * 32, TX_DYN_SMEM, s>>>(
+            ts, dv, cbins, tiles_x, tiles_x * tiles_y, items, d_fix, b0);
         if (ev) CK(cudaEventRecord(ev[3], s));
-        k_samples<false><<<grid, 256, 0, s>>>(p->d_px, p->d_py, p->d_pz, p->d_chunk, p->N, p->n_chunks, d_fix,
-                                              d_cull, nb, dv, inv_sigma, cfg->eps_abs, cfg->eps_rel, p->d_values,
-                                              p->d_fail, b0);
+        k_samples<false><<<grid, 256, 0, s>>>(p->d_px, p->d_py, p->d_pz, p->d_chunk, p->d_lvl1, p->d_lorder2,
+                                              p->d_work + 1, p->N, p->n_chunks, p->n_supers, d_fix, d_cull, nb, dv,
+                                              inv_sigma, cfg->eps_abs, cfg->eps_rel, p->d_values, p->d_fail, b0);
     } else if (ev) {
         CK(cudaEventRecord(ev[2], s));
         CK(cudaEventRecord(ev[3], s));
@@ -968,7 +1277,7 @@ static int run_batches(gm_plan* p, const double* fx, int64_t F, const GmConfig* 
     double t_start = wall_ms();
     const int W = cfg->zbuffer_resolution, H = cfg->zbuffer_resolution;
     int B = cfg->batch > 0 ? cfg->batch : 512;
-    if (B > 4096) B = 4096;
+    if (B > GM_MAX_BATCH) B = GM_MAX_BATCH;
     const int64_t depth_per_fix = (int64_t)W * H;
     int64_t max_d = std::max<int64_t>(1, ((int64_t)1 << 28) / depth_per_fix);  // z-buffer store <= 2 GiB
     if (B > max_d) B = (int)max_d;
@@ -994,6 +1303,7 @@ static int run_batches(gm_plan* p, const double* fx, int64_t F, const GmConfig* 
         CK(cudaEventRecord(ev_start, s));
     }
     if (reset && p->N > 0) CK(cudaMemsetAsync(p->d_values, 0, sizeof(double) * p->N, s));
+    if (cfg->flags & GM_FLAG_STATS) CK(cudaMemsetAsync(p->d_stats, 0, GM_STAT_N * sizeof(unsigned long long), s));
     GmTimings t;
     memset(&t, 0, sizeof(t));
     const bool timing = tm != nullptr;
@@ -1133,10 +1443,12 @@ extern "C" int gm_plan_prepare(gm_plan* p, const double* fx, int64_t F, const Gm
 
 // Replay the prepared fixations (device-resident inputs).  device_ms gets the
 // CUDA-event time of the whole pass on the plan's stream.
-extern "C" int gm_plan_run(gm_plan* p, int reset, GmTimings* tm, float* device_ms) {
+extern "C" int gm_plan_run(gm_plan* p, int reset, int flags, GmTimings* tm, float* device_ms) {
     if (!p) return set_err(GM_ERR_ARG, "null plan");
     if (p->F_prepared < 0) return set_err(GM_ERR_ARG, "gm_plan_prepare was not called");
-    return run_batches(p, nullptr, p->F_prepared, &p->cfg_prepared, reset, tm, nullptr, nullptr, nullptr, device_ms);
+    GmConfig cfg = p->cfg_prepared;
+    cfg.flags = flags;
+    return run_batches(p, nullptr, p->F_prepared, &cfg, reset, tm, nullptr, nullptr, nullptr, device_ms);
 }
 
 // Evict L2 between timed repetitions: write `bytes` (> 126 MB L2) on the plan stream.
@@ -1150,6 +1462,16 @@ extern "C" int gm_plan_flush_l2(gm_plan* p, int64_t bytes) {
         p->flush_bytes = bytes;
     }
     CK(cudaMemsetAsync(p->d_flush, (int)(++p->flush_gen & 0xff), bytes, p->stream));
+    return GM_OK;
+}
+
+// Work counters of the last gm_plan_accumulate / gm_plan_run made with
+// GmConfig.flags & 1 (GM_STAT_* order, 16 x uint64).
+extern "C" int gm_plan_stats(gm_plan* p, unsigned long long* out) {
+    if (!p || !out) return set_err(GM_ERR_ARG, "null argument");
+    CK(cudaSetDevice(p->device));
+    CK(cudaStreamSynchronize(p->stream));
+    CK(cudaMemcpy(out, p->d_stats, GM_STAT_N * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
     return GM_OK;
 }
 
@@ -1350,10 +1672,14 @@ extern "C" int gm_plan_depth_buffer(gm_plan* p, const double* fx, double theta, 
         if ((rc = ensure_batch(p, 1, res, res, want))) return rc;
     }
     TriStore ts{p->d_tris, p->d_bbox, p->d_count, p->cap_seg, p->d_fail, p->d_maxcount, p->d_ntris};
-    DepthView dv{p->d_depth, p->d_mask, res, res, wwords};
+    const int tiles_x = (res + TW - 1) / TW, tiles_y = (res + TH - 1) / TH;
+    DepthView dv{p->d_depth, p->d_mask, res, res, wwords, nullptr};
     k_mark_all<<<blocks_for((int64_t)res * wwords, 256), 256, 0, s>>>(p->d_mask, res, res, wwords);
-    const int tiles_x = (res + TX_TILE - 1) / TX_TILE;
-    k_texels<<<tiles_x * tiles_x, 512, TX_DYN_SMEM, s>>>(ts, dv, tiles_x, tiles_x * tiles_x, p->d_fix, 0);
+    CoarseBins cbins = coarse_bins(p, res, res);
+    k_coarse<<<1, 256, 0, s>>>(ts, cbins, p->d_fail, 0);
+    const int64_t items = (int64_t)tiles_x * tiles_y;
+    k_texels<<<(unsigned)((items + TW_WARPS - 1) / TW_WARPS), TW_WARPS * 32, TX_DYN_SMEM, s>>>(
+        ts, dv, cbins, tiles_x, tiles_x * tiles_y, items, p->d_fix, 0);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(depth, p->d_depth, sizeof(double) * res * res, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));

@@ -41,7 +41,7 @@ struct __attribute__((aligned(16))) GmScreenTri {
     double iw0, iw1, iw2, inv_area;
     uint16_t x0, x1, y0, y1;  // inclusive pixel bbox clamped to the buffer
     uint32_t tl;              // top-left ownership bits for edges 0, 1, 2
-    int32_t fslot;            // fixation slot within the batch
+    float minw;               // min vertex depth, rounded down (a lower bound of every depth it writes)
 };  // 96 B
 
 // Per-config constants for the host setup.
