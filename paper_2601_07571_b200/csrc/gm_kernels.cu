@@ -382,6 +382,7 @@ struct DepthView {
     uint32_t* mask;   // [B][H][wwords]: texels the depth tests will read
     int W, H, wwords;
     unsigned long long* stats;  // optional work counters (GM_STAT_*), nullptr = off
+    float* vbuf;      // [B][H][W]: k_texels' inverse-depth bounds for tiles with many triangles
 };
 
 // Work counters filled when GmConfig.flags & GM_FLAG_STATS (bench roofline).
@@ -611,33 +612,121 @@ __global__ void __launch_bounds__(256) k_samples(const double* __restrict__ px, 
 }
 
 // Fixation-major evaluation of the marked texels.  Every warp is an
-// independent work item (fixation, 32x16-pixel tile), lane = pixel column, so
-// there are no CTA barriers and no atomics:
-//   1. the tile's rows of the candidate-texel mask are transposed with ballots
-//      (lane c gets the 16-bit row mask of column c);
-//   2. the fixation's screen triangles are scanned through their bbox array
-//      (coalesced); overlapping ones are staged in the warp's shared slice,
-//      TW_CAP records at a time;
-//   3. per staged triangle every lane forms the marked rows of its column inside
-//      the bbox and pushes (triangle, row, column) pairs to the warp's ring
-//      queue; the queue is drained 32 pairs per round, one pair per lane (full
-//      SIMT use of the FP64 pipe), each pair folding its depth into the texel's
-//      minimum in shared memory (same-texel lanes of a round are serialised
-//      with __match_any_sync);
-//   4. the minima of the marked texels are stored to the z-buffer array.
-// The values are exactly what kernels.rasterize leaves in those pixels: same
-// per-pixel arithmetic (texel_depth), min over every covering triangle.
+// independent work item (fixation, 32x16-pixel tile): no CTA barriers, no
+// atomics.
+//   1. the tile's triangles (from its coarse bin, bbox-filtered) are staged in
+//      the warp's shared slice TW_CAP at a time -- the exact float64 records
+//      and a float32 form of each (edge-function planes, inverse-depth plane,
+//      rigorous absolute error bounds of those planes) -- and sorted by their
+//      minimum depth, nearest first;
+//   2. lanes take the marked texels of the tile (compacted, 32 per round) and
+//      walk the sorted triangles with uniform float32 tests: a triangle is
+//      "certainly written" (inside by more than the bound, inverse depth
+//      certainly in (1/far, 1/near)) or "maybe written"; V = the largest
+//      certain lower bound of the inverse depth is a proof that the texel's
+//      depth is <= 1/V, so a maybe-triangle whose inverse-depth upper bound is
+//      < V can never be the minimum, and once the next triangle's bound
+//      1/minw is < V no later triangle can be either (early stop);
+//   3. the surviving candidates (normally one) are evaluated exactly with the
+//      reference's float64 pixel arithmetic (texel_depth) and the minimum is
+//      stored -- exactly the value kernels.rasterize leaves in that pixel.
 #define TW_CAP 32
-#define TW_Q 256
-#define TW_WARPS 8
+#define TW_SEL 128  // overlapping triangles remembered per tile (more: rescanned per round)
+#define TW_WARPS 4
+#define TW_K 4  // exact candidates remembered per texel before the slow path
+struct TriF32 {
+    float a[3], b[3], c[3], tol[3];  // edge planes e_i = a x + b y + c (tile-local), |e32 - e_ref| <= tol
+    float A, B, C, tolw;             // inverse-depth plane and its bound
+    float inv_minw;                  // >= every inverse depth the triangle writes
+    uint32_t bx, by;                 // bbox x0 | x1 << 16, y0 | y1 << 16 (tile-local, clamped)
+    int slot;                        // index of the float64 record in rec[]
+};
 struct __align__(16) TexelWarpSmem {
     GmScreenTri rec[TW_CAP];
-    double best[TH * TW];
-    uint32_t q[TW_Q];
-    int idx[TW_CAP + 32];
+    TriF32 t32[TW_CAP];  // in ascending min-depth order
+    int sel[TW_SEL + 32];
+    int rank[TW_CAP];
 };
 #define TX_DYN_SMEM (TW_WARPS * (int)sizeof(TexelWarpSmem))
 
+// position of the k-th (0-based) set bit of w (k < popc(w))
+__device__ __forceinline__ int kth_set_bit(uint32_t w, int k) {
+    int base = 0;
+#pragma unroll
+    for (int half = 16; half >= 1; half >>= 1) {
+        const uint32_t low = w & ((1u << half) - 1u);
+        const int c = __popc(low);
+        if (k >= c) {
+            k -= c;
+            w >>= half;
+            base += half;
+        } else {
+            w = low;
+        }
+    }
+    return base;
+}
+
+// float32 planes of one screen triangle in tile-local pixel coordinates
+// (x - xb, y - yb), with error bounds that cover both the float32 evaluation
+// at any pixel centre of the tile and the reference's own float64 rounding
+// (kernels.py:107-125): |e32 - e_ref| <= tol, |invw32 - invw_ref| <= tolw.
+__device__ __forceinline__ void make_tri_f32(const GmScreenTri& T, int xb, int yb, int slot, TriF32& o) {
+    const double sx[3] = {T.sx0 - xb, T.sx1 - xb, T.sx2 - xb}, sy[3] = {T.sy0 - yb, T.sy1 - yb, T.sy2 - yb};
+    const double iw[3] = {T.iw0, T.iw1, T.iw2};
+    const double xmax = TW, ymax = TH;
+    double A = 0.0, B = 0.0, C = 0.0, Aab = 0.0, Bab = 0.0, Cab = 0.0;
+#pragma unroll
+    for (int i = 0; i < 3; i++) {
+        // edge i runs from vertex (i+1)%3 to (i+2)%3: w_i = (bx-ax)(py-ay) - (by-ay)(px-ax)
+        const int ia = (i + 1) % 3, ib = (i + 2) % 3;
+        const double ex = sx[ib] - sx[ia], ey = sy[ib] - sy[ia];
+        const double a = -ey, b = ex, c = ey * sx[ia] - ex * sy[ia];
+        o.a[i] = (float)a;
+        o.b[i] = (float)b;
+        o.c[i] = (float)c;
+        // float32 plane evaluation error <= ~4 * 2^-24 and the reference's float64
+        // rounding <= ~4 * 2^-53 of |a|(|x|+|ax|) + |b|(|y|+|ay|); tol is >= 2x that
+        const double mag = fabs(a) * (xmax + fabs(sx[ia])) + fabs(b) * (ymax + fabs(sy[ia]));
+        o.tol[i] = (float)(4.8e-7 * mag + 1e-30);
+        const double k = iw[i] * T.inv_area;  // l_i = w_i * inv_area, inv_w = sum l_i iw_i
+        A += a * k;
+        B += b * k;
+        C += c * k;
+        Aab += fabs(a * k);
+        Bab += fabs(b * k);
+        Cab += fabs(c * k);
+    }
+    o.A = (float)A;
+    o.B = (float)B;
+    o.C = (float)C;
+    o.tolw = (float)(4.8e-7 * (Aab * xmax + Bab * ymax + Cab) + 1e-30);
+    o.inv_minw = __double2float_ru(1.0 / (double)T.minw) * (1.0f + 1e-6f);
+    const int x0 = max((int)T.x0 - xb, 0), x1 = min((int)T.x1 - xb, TW - 1);
+    const int y0 = max((int)T.y0 - yb, 0), y1 = min((int)T.y1 - yb, TH - 1);
+    o.bx = (uint32_t)(x0 & 0xffff) | ((uint32_t)(x1 & 0xffff) << 16);
+    o.by = (uint32_t)(y0 & 0xffff) | ((uint32_t)(y1 & 0xffff) << 16);
+    o.slot = slot;
+}
+
+// Fixation-major evaluation of the marked texels.  Every warp is an
+// independent work item (fixation, 32x16-pixel tile): no CTA barriers, no
+// atomics, per-texel state in registers.
+//   1. the tile's triangles are gathered from its coarse bin (bbox-filtered);
+//   2. they are staged in the warp's shared slice TW_CAP at a time -- exact
+//      float64 records plus a float32 form (edge-function planes, inverse-depth
+//      plane, rigorous absolute error bounds) written in ascending min-depth
+//      order;
+//   3. lanes take the marked texels (compacted, 32 per round) and walk the
+//      sorted triangles with uniform float32 tests: "certainly written"
+//      (inside by more than the bound, inverse depth certainly within
+//      (1/far', 1/near')) or "maybe written".  V, the largest certain lower
+//      bound of the inverse depth, proves depth <= 1/V, so a maybe-triangle
+//      whose inverse-depth upper bound is < V can never be the minimum, and
+//      once a triangle's 1/minw bound is < V no later one can be (stop);
+//   4. the surviving candidates (normally one) are evaluated exactly with the
+//      reference's float64 pixel arithmetic (texel_depth) and the minimum is
+//      stored -- the value kernels.rasterize leaves in that pixel.
 __global__ void __launch_bounds__(TW_WARPS * 32) k_texels(TriStore ts, DepthView dv, CoarseBins cb, int tiles_x,
                                                           int tiles_per_fix, int64_t n_items,
                                                           const GmFixExact* __restrict__ fixes, long long b0) {
@@ -651,73 +740,68 @@ __global__ void __launch_bounds__(TW_WARPS * 32) k_texels(TriStore ts, DepthView
     const int W = dv.W, H = dv.H;
     const int xb = (tile % tiles_x) * TW, yb = (tile / tiles_x) * TH;
     const unsigned FULL = 0xffffffffu;
-    // 1. lane r < TH loads mask row yb + r (one word: xb is a multiple of 32)
+    // marked texels: lane r < TH holds the mask word of row yb + r
     uint32_t wr = 0;
     if (lane < TH && yb + lane < H) wr = dv.mask[((int64_t)f * H + yb + lane) * dv.wwords + (xb >> 5)];
-    if (!__any_sync(FULL, wr != 0u)) return;
-    uint32_t need = 0;
+    const int cnt_r = __popc(wr);
+    int pref = cnt_r;  // inclusive prefix over rows
 #pragma unroll
-    for (int c = 0; c < 32; c++) {
-        const uint32_t b = __ballot_sync(FULL, (wr >> c) & 1u);
-        if (lane == c) need = b & ((1u << TH) - 1u);
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(FULL, pref, o);
+        if (lane >= o) pref += v;
     }
-    for (uint32_t m = need; m; m &= m - 1) S.best[(__ffs(m) - 1) * TW + lane] = CUDART_INF;
-    const int col = xb + lane;
-    const double near_ = fixes[f].near_, far_ = fixes[f].far_;
+    const int total = __shfl_sync(FULL, pref, 31);
+    if (total == 0) return;
+    const int pref_ex = pref - cnt_r;
+    const GmFixExact& F = fixes[f];
+    const double near_ = F.near_, far_ = F.far_;
+    // written iff near' <= 1/inv_w <= far' (kernels.py:123-127): certainly inside
+    // [inv_far_hi, inv_near_lo], certainly outside beyond [inv_far_lo, inv_near_hi]
+    const float inv_near = (float)(1.0 / near_), inv_far = (float)(1.0 / far_);
+    const float inv_near_lo = inv_near * (1.0f - 1e-5f), inv_near_hi = inv_near * (1.0f + 1e-5f);
+    const float inv_far_lo = inv_far * (1.0f - 1e-5f), inv_far_hi = inv_far * (1.0f + 1e-5f);
     const GmScreenTri* seg = ts.tris + (int64_t)f * ts.cap_seg;
     const uint2* segb = ts.bbox + (int64_t)f * ts.cap_seg;
-    // candidate triangles: the tile's coarse bin (or the whole list on overflow)
     const int* clist = nullptr;
     int n = min(ts.count[f], (int)ts.cap_seg);
     if (!cb.ovf[f]) {
         const int* off = cb.off + (int64_t)f * (GM_MAX_CBINS + 1);
-        const int b = (yb >> cb.shift) * cb.ncx + (xb >> cb.shift);
-        clist = cb.items + (int64_t)f * cb.cap_items + off[b];
-        n = off[b + 1] - off[b];
+        const int bb = (yb >> cb.shift) * cb.ncx + (xb >> cb.shift);
+        clist = cb.items + (int64_t)f * cb.cap_items + off[bb];
+        n = off[bb + 1] - off[bb];
     }
     const int xe = xb + TW - 1, ye = yb + TH - 1;
-    unsigned qh = 0, qt = 0;  // warp-uniform ring indices
     unsigned long long c_pairs = 0, c_cov = 0;
 
-    auto drain = [&](bool all) {
-        __syncwarp();
-        while (qt - qh >= (all ? 1u : 32u)) {
-            const unsigned k = qh + lane;
-            const bool valid = k < qt;
-            double d = CUDART_INF;
-            int key = 0x10000 + lane;
-            if (valid) {
-                const uint32_t e = S.q[k & (TW_Q - 1)];
-                const int r = (e >> 5) & 31, c = e & 31;
-                d = texel_depth(S.rec[e >> 10], xb + c, yb + r, near_, far_);
-                key = r * TW + c;
-                c_pairs++;
-                c_cov += d < CUDART_INF;
+    // 1. triangles overlapping the tile -> S.sel (scan cursor resumes if > TW_SEL)
+    auto gather = [&](int& cursor) {
+        int cnt = 0;
+        while (cursor < n && cnt < TW_SEL) {
+            int i = cursor + lane;
+            bool sel = false;
+            if (i < n) {
+                if (clist) i = clist[i];
+                const uint2 bbx = segb[i];
+                const int x0 = bbx.x & 0xffff, x1 = bbx.x >> 16, y0 = bbx.y & 0xffff, y1 = bbx.y >> 16;
+                sel = !(x1 < xb || x0 > xe || y1 < yb || y0 > ye);
             }
-            const unsigned grp = __match_any_sync(FULL, key);
-            const bool upd = valid && d < CUDART_INF;
-            if (grp == (1u << lane)) {
-                if (upd && d < S.best[key]) S.best[key] = d;
-            } else {
-                for (unsigned mm = grp; mm; mm &= mm - 1) {
-                    if (lane == __ffs(mm) - 1 && upd && d < S.best[key]) S.best[key] = d;
-                    __syncwarp(grp);
-                }
-            }
-            qh += min(32u, qt - qh);
-            __syncwarp();
+            const unsigned bal = __ballot_sync(FULL, sel);
+            if (sel) S.sel[cnt + __popc(bal & ((1u << lane) - 1u))] = i;
+            cnt += __popc(bal);
+            cursor += 32;
         }
+        __syncwarp();
+        return cnt;  // may exceed TW_SEL by < 32 (S.sel has the room)
     };
 
-    // stage S.idx[0..kend) and evaluate their pairs, nearest triangles first
-    auto process = [&](int kend) {
+    // 2. stage S.sel[c0 .. c0 + kend) sorted by min depth
+    auto stage = [&](int c0, int kend) {
         __syncwarp();
         for (int q = lane; q < kend * 6; q += 32) {
             const int ti = q / 6, part = q - ti * 6;
-            reinterpret_cast<uint4*>(&S.rec[ti])[part] = reinterpret_cast<const uint4*>(seg + S.idx[ti])[part];
+            reinterpret_cast<uint4*>(&S.rec[ti])[part] = reinterpret_cast<const uint4*>(seg + S.sel[c0 + ti])[part];
         }
         __syncwarp();
-        // warp bitonic sort of the staged triangles by min depth (lane = slot)
         float key = lane < kend ? S.rec[lane].minw : CUDART_INF_F;
         int slot = lane;
 #pragma unroll
@@ -726,107 +810,152 @@ __global__ void __launch_bounds__(TW_WARPS * 32) k_texels(TriStore ts, DepthView
             for (int stride = size >> 1; stride > 0; stride >>= 1) {
                 const float ok = __shfl_xor_sync(FULL, key, stride);
                 const int os = __shfl_xor_sync(FULL, slot, stride);
-                const bool up = ((lane & size) == 0);
-                const bool lower = (lane & stride) == 0;
-                const bool take = lower ? (up ? (ok < key || (ok == key && os < slot)) : (ok > key || (ok == key && os > slot)))
-                                        : (up ? (ok > key || (ok == key && os > slot)) : (ok < key || (ok == key && os < slot)));
-                if (take) {
+                const bool keep_min = ((lane & stride) == 0) == ((lane & size) == 0);
+                const bool less = ok < key || (ok == key && os < slot);
+                if (keep_min ? less : !less && !(ok == key && os == slot)) {
                     key = ok;
                     slot = os;
                 }
             }
         }
-        for (int kk = 0; kk < kend; kk++) {
-            const int k = __shfl_sync(FULL, slot, kk);
-            const GmScreenTri& T = S.rec[k];
-            uint32_t bits = 0;
-            if (col >= T.x0 && col <= T.x1) {
-                const int lo = max((int)T.y0 - yb, 0), hi = min((int)T.y1 - yb, TH - 1);
-                if (lo <= hi) bits = need & (((1u << (hi - lo + 1)) - 1u) << lo);
-            }
-            // early-out: a texel already holding a nearer depth than this triangle's
-            // minimum cannot change (its depths here are all >= minw)
-            if (bits) {
-                const double thr = (double)T.minw * (1.0 - 1e-9);
-                for (uint32_t m = bits; m; m &= m - 1) {
-                    const int r = __ffs(m) - 1;
-                    if (S.best[r * TW + lane] < thr) bits &= ~(1u << r);
-                }
-            }
-            if (!__any_sync(FULL, bits != 0u)) continue;
-            const int pc = __popc(bits);
-            int incl = pc;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int v = __shfl_up_sync(FULL, incl, o);
-                if (lane >= o) incl += v;
-            }
-            const unsigned total = (unsigned)__shfl_sync(FULL, incl, 31);
-            if (total > TW_Q) {
-                // more marked texels under this bbox than the queue holds: each
-                // lane evaluates its own column (it owns those minima)
-                drain(true);
-                while (__any_sync(FULL, bits != 0u)) {
-                    if (bits) {
-                        const int r = __ffs(bits) - 1;
-                        bits &= bits - 1;
-                        const double d = texel_depth(T, col, yb + r, near_, far_);
-                        c_pairs++;
-                        c_cov += d < CUDART_INF;
-                        if (d < S.best[r * TW + lane]) S.best[r * TW + lane] = d;
-                    }
-                }
-                __syncwarp();
-                continue;
-            }
-            if (qt - qh + total > TW_Q) drain(true);
-            unsigned pos = qt + (unsigned)(incl - pc);
-            while (bits) {
-                const int r = __ffs(bits) - 1;
-                bits &= bits - 1;
-                S.q[pos++ & (TW_Q - 1)] = ((uint32_t)k << 10) | ((uint32_t)r << 5) | (uint32_t)lane;
-            }
-            qt += total;
-            drain(false);
-        }
-        drain(true);  // the staged records are replaced next
+        S.rank[slot] = lane;  // lane = rank of record `slot`
+        __syncwarp();
+        if (lane < kend) make_tri_f32(S.rec[lane], xb, yb, lane, S.t32[S.rank[lane]]);
+        __syncwarp();
     };
 
-    int cnt = 0;
-    for (int base = 0; base < n; base += 32) {
-        int i = base + lane;
-        bool sel = false;
-        if (i < n) {
-            if (clist) i = clist[i];
-            const uint2 bb = segb[i];
-            const int x0 = bb.x & 0xffff, x1 = bb.x >> 16, y0 = bb.y & 0xffff, y1 = bb.y >> 16;
-            sel = !(x1 < xb || x0 > xe || y1 < yb || y0 > ye);
+    // texel of compact id q: (row, tile-local column)
+    auto texel_of = [&](int q, int& row, int& colo) {
+        row = 0;
+#pragma unroll
+        for (int step = 8; step > 0; step >>= 1) {
+            const int cand = row + step;
+            const int pc = __shfl_sync(FULL, pref_ex, cand & 31);
+            if (cand < TH && pc <= q) row = cand;
         }
-        const unsigned bal = __ballot_sync(FULL, sel);
-        if (sel) S.idx[cnt + __popc(bal & ((1u << lane) - 1u))] = i;
-        cnt += __popc(bal);
-        if (cnt >= TW_CAP) {
-            process(TW_CAP);
-            // keep the indices that did not fit (fewer than 32)
-            const int rest = cnt - TW_CAP;
-            const int keep = lane < rest ? S.idx[TW_CAP + lane] : 0;
-            __syncwarp();
-            if (lane < rest) S.idx[lane] = keep;
-            cnt = rest;
+        const uint32_t w_row = __shfl_sync(FULL, wr, row);
+        const int k_in_row = q - __shfl_sync(FULL, pref_ex, row);
+        colo = q < total ? kth_set_bit(w_row, k_in_row) : 0;
+    };
+
+    // 3 + 4 for the staged chunk (kend triangles) and one texel: updates V, best
+    auto walk = [&](int kend, bool valid, int row, int colo, float& V, double& best) {
+        const float fx = (float)colo + 0.5f, fy = (float)row + 0.5f;  // tile-local pixel centre
+        int cand_slot[TW_K];
+        float cand_hi[TW_K];
+        int ncand = 0;
+        bool overflow = false;
+        for (int kk = 0; kk < kend; kk++) {
+            const TriF32& t = S.t32[kk];
+            const float inv_minw = t.inv_minw;
+            if (__all_sync(FULL, !(inv_minw >= V))) break;  // nothing later can be nearer
+            const uint32_t tbx = t.bx, tby = t.by;
+            if (!(inv_minw >= V) || colo < (int)(tbx & 0xffff) || colo > (int)(tbx >> 16) ||
+                row < (int)(tby & 0xffff) || row > (int)(tby >> 16))
+                continue;
+            bool maybe = true, certain = true;
+#pragma unroll
+            for (int i = 0; i < 3; i++) {
+                const float e = __fmaf_rn(t.a[i], fx, __fmaf_rn(t.b[i], fy, t.c[i]));
+                maybe = maybe && (e >= -t.tol[i]);
+                certain = certain && (e > t.tol[i]);
+            }
+            if (!maybe) continue;
+            const float iwv = __fmaf_rn(t.A, fx, __fmaf_rn(t.B, fy, t.C));
+            const float lo = iwv - t.tolw, hi = iwv + t.tolw;
+            if (!(hi > 0.0f) || lo > inv_near_hi || hi < inv_far_lo) continue;  // certainly not written
+            if (certain && lo > 0.0f && hi <= inv_near_lo && lo >= inv_far_hi && lo * (1.0f - 1e-6f) > V)
+                V = lo * (1.0f - 1e-6f);
+            if (hi >= V) {
+                if (ncand < TW_K) {
+                    cand_slot[ncand] = t.slot;
+                    cand_hi[ncand] = hi;
+                    ncand++;
+                } else {
+                    overflow = true;
+                }
+            }
+        }
+        const int px = xb + colo, py = yb + row;
+        if (!overflow) {
+#pragma unroll
+            for (int c = 0; c < TW_K; c++) {
+                if (valid && c < ncand && cand_hi[c] >= V) {
+                    const double d = texel_depth(S.rec[cand_slot[c]], px, py, near_, far_);
+                    c_pairs++;
+                    c_cov += d < CUDART_INF;
+                    if (d < best) best = d;
+                }
+            }
+        } else if (valid) {  // slow path: every staged triangle whose bbox covers the texel
+            for (int k = 0; k < kend; k++) {
+                const GmScreenTri& T = S.rec[k];
+                if (px < T.x0 || px > T.x1 || py < T.y0 || py > T.y1) continue;
+                const double d = texel_depth(T, px, py, near_, far_);
+                c_pairs++;
+                c_cov += d < CUDART_INF;
+                if (d < best) best = d;
+            }
+        }
+    };
+
+    double* dep = dv.depth + (int64_t)f * W * H;
+    int cursor = 0;
+    int nsel = gather(cursor);
+    if (cursor >= n && nsel <= TW_CAP) {
+        // common case: one staging serves every round, per-texel state in registers
+        if (nsel > 0) stage(0, nsel);
+        for (int r0 = 0; r0 < total; r0 += 32) {
+            const int q = r0 + lane;
+            const bool valid = q < total;
+            int row, colo;
+            texel_of(q, row, colo);
+            float V = valid ? 0.0f : CUDART_INF_F;
+            double best = CUDART_INF;
+            if (nsel > 0) walk(nsel, valid, row, colo, V, best);
+            if (valid) dep[(int64_t)(yb + row) * W + xb + colo] = best;
+        }
+    } else {
+        // many triangles: chunk by chunk (each staged once), per-texel state kept in
+        // the depth array and the inverse-depth-bound buffer between chunks
+        float* vb = dv.vbuf + (int64_t)f * W * H;
+        bool first = true;
+        while (true) {
+            for (int c0 = 0; c0 < nsel; c0 += TW_CAP) {
+                const int kend = min(TW_CAP, nsel - c0);
+                stage(c0, kend);
+                for (int r0 = 0; r0 < total; r0 += 32) {
+                    const int q = r0 + lane;
+                    const bool valid = q < total;
+                    int row, colo;
+                    texel_of(q, row, colo);
+                    const int64_t at = (int64_t)(yb + row) * W + xb + colo;
+                    float V = valid ? (first ? 0.0f : vb[at]) : CUDART_INF_F;
+                    double best = (valid && !first) ? dep[at] : CUDART_INF;
+                    walk(kend, valid, row, colo, V, best);
+                    if (valid) {
+                        dep[at] = best;
+                        vb[at] = V;
+                    }
+                }
+                first = false;
+            }
+            if (cursor >= n) break;
+            nsel = gather(cursor);
+        }
+        if (first) {  // no triangle at all
+            for (int r0 = 0; r0 < total; r0 += 32) {
+                const int q = r0 + lane;
+                int row, colo;
+                texel_of(q, row, colo);
+                if (q < total) dep[(int64_t)(yb + row) * W + xb + colo] = CUDART_INF;
+            }
         }
     }
-    if (cnt > 0) process(cnt);
     if (dv.stats) {
-        atomicAdd(dv.stats + GM_STAT_TEXELS, (unsigned long long)__popc(need));
+        if (lane == 0) atomicAdd(dv.stats + GM_STAT_TEXELS, (unsigned long long)total);
         atomicAdd(dv.stats + GM_STAT_PAIRS, c_pairs);
         atomicAdd(dv.stats + GM_STAT_COVERED, c_cov);
-    }
-    if (need) {
-        double* dep = dv.depth + (int64_t)f * W * H;
-        for (uint32_t m = need; m; m &= m - 1) {
-            const int r = __ffs(m) - 1;
-            dep[(int64_t)(yb + r) * W + col] = S.best[r * TW + lane];
-        }
     }
 }
 
@@ -944,6 +1073,7 @@ struct gm_plan {
     unsigned long long* d_ntris = nullptr;
     // marked z-buffer texels
     double* d_depth = nullptr;   // [B][H][W] marked texels only
+    float* d_vbuf = nullptr;     // [B][H][W] k_texels state for crowded tiles
     uint32_t* d_mask = nullptr;  // [B][H][wwords]
     int64_t cap_depth = 0, cap_mask = 0;
     int* d_citems = nullptr;  // coarse bins: [B][cap_citems]
@@ -1017,7 +1147,7 @@ extern "C" void gm_plan_destroy(gm_plan* p) {
     cudaFree(p->d_tris); cudaFree(p->d_bbox); cudaFree(p->d_count); cudaFree(p->d_fail); cudaFree(p->d_maxcount); cudaFree(p->d_ntris); cudaFree(p->d_work);
     cudaFree(p->d_scan_tmp); cudaFree(p->d_max); cudaFree(p->d_stats);
     cudaFree(p->d_fix_all); cudaFree(p->d_cull_all); cudaFree(p->d_flush);
-    cudaFree(p->d_depth); cudaFree(p->d_mask);
+    cudaFree(p->d_depth); cudaFree(p->d_mask); cudaFree(p->d_vbuf);
     cudaFree(p->d_citems); cudaFree(p->d_coff); cudaFree(p->d_covf);
     cudaStreamDestroy(p->stream);
     delete p;
@@ -1178,6 +1308,7 @@ static int ensure_batch(gm_plan* p, int B, int W, int H, int64_t seg) {
     }
     if ((int64_t)B * W * H > p->cap_depth) {
         if ((rc = dev_alloc(&p->d_depth, (size_t)B * W * H))) return rc;
+        if ((rc = dev_alloc(&p->d_vbuf, (size_t)B * W * H))) return rc;
         p->cap_depth = (int64_t)B * W * H;
     }
     if (B > p->cap_cB || 4 * p->cap_seg > p->cap_citems) {
@@ -1221,7 +1352,8 @@ static int enqueue_batch(gm_plan* p, const GmFixExact* d_fix, const GmFixCull* d
     const int wwords = (W + 31) / 32;
     const int tiles_x = (W + TW - 1) / TW, tiles_y = (H + TH - 1) / TH;
     TriStore ts{p->d_tris, p->d_bbox, p->d_count, p->cap_seg, p->d_fail, p->d_maxcount, p->d_ntris};
-    DepthView dv{p->d_depth, p->d_mask, W, H, wwords, (cfg->flags & GM_FLAG_STATS) ? p->d_stats : nullptr};
+    DepthView dv{p->d_depth, p->d_mask, W, H, wwords, (cfg->flags & GM_FLAG_STATS) ? p->d_stats : nullptr,
+                 p->d_vbuf};
     if (ev) CK(cudaEventRecord(ev[0], s));
     CK(cudaMemsetAsync(p->d_count, 0, sizeof(int) * nb, s));
     if (p->n_clu > 0) {
@@ -1285,7 +1417,7 @@ static int run_batches(gm_plan* p, const double* fx, int64_t F, const GmConfig* 
     B = std::max(B, 1);
     GmSetupConsts consts;
     gm_setup_consts(cfg->theta, cfg->filtering, W, H, &consts);
-    int rc = ensure_batch(p, B, W, H, std::max<int64_t>(p->cap_seg, 4096));
+    int rc = ensure_batch(p, B, W, H, std::max<int64_t>(p->cap_seg, 16384));
     if (rc) return rc;
     cudaStream_t s = p->stream;
     cudaEvent_t ev_start = nullptr, ev_end = nullptr;
@@ -1673,7 +1805,7 @@ extern "C" int gm_plan_depth_buffer(gm_plan* p, const double* fx, double theta, 
     }
     TriStore ts{p->d_tris, p->d_bbox, p->d_count, p->cap_seg, p->d_fail, p->d_maxcount, p->d_ntris};
     const int tiles_x = (res + TW - 1) / TW, tiles_y = (res + TH - 1) / TH;
-    DepthView dv{p->d_depth, p->d_mask, res, res, wwords, nullptr};
+    DepthView dv{p->d_depth, p->d_mask, res, res, wwords, nullptr, p->d_vbuf};
     k_mark_all<<<blocks_for((int64_t)res * wwords, 256), 256, 0, s>>>(p->d_mask, res, res, wwords);
     CoarseBins cbins = coarse_bins(p, res, res);
     k_coarse<<<1, 256, 0, s>>>(ts, cbins, p->d_fail, 0);

@@ -1,7 +1,7 @@
 mkdir -p gpurun_out
-timeout 1200 python -m pytest tests -m gpu -q --timeout 600 -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1
+timeout 1200 python -m pytest tests -m gpu -q --timeout 600 -p no:cacheprovider -x --durations=8 > gpurun_out/pytest_gpu.log 2>&1
 echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 timeout 900 python bench.py --steps 3 --warmup 3 --no-cpu > gpurun_out/bench.log 2>&1
 echo "rc=$?" >> gpurun_out/bench.log
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_texels|k_samples|k_tri_setup|k_level1|k_coarse' -s 40 -c 6 -o gpurun_out/prof_r1e python bench.py --fixations 4096 --batch 512 --steps 1 --warmup 3 --no-cpu --no-e2e > gpurun_out/ncu_full.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_texels' -s 10 -c 1 -o gpurun_out/prof_r1h python bench.py --fixations 4096 --batch 512 --steps 1 --warmup 3 --no-cpu --no-e2e > gpurun_out/ncu_full.log 2>&1
 echo "rc=$?" >> gpurun_out/ncu_full.log
