@@ -229,8 +229,65 @@ __global__ void k_group_spheres(const float4* __restrict__ member, const double*
 // result: the first batch that overflows sets *fail (sticky) and every later
 // kernel of that and following batches returns immediately; the host grows
 // the segments and resumes from that batch (log order is preserved).
+// float32 form of one screen triangle for k_texels' selection stage: the
+// three edge-function planes and the inverse-depth plane in the triangle's
+// bbox-local pixel frame (x - x0, y - y0), with error bounds that cover both
+// the float32 evaluation at any pixel centre of the bbox and the reference's
+// own float64 rounding (kernels.py:107-125): |e32 - e_ref| <= tol,
+// |invw32 - invw_ref| <= tolw.  Built once per screen triangle in k_tri_setup.
+struct __align__(16) TriF32 {
+    float a[3], b[3], c[3], tol[3];  // e_i = a x + b y + c
+    float A, B, C, tolw;             // inverse depth
+    float inv_minw;                  // >= every inverse depth the triangle writes
+    int ox, oy;                      // frame origin = bbox corner (pixels)
+    uint32_t bx, by;                 // bbox x0 | x1 << 16, y0 | y1 << 16
+    int gidx;                        // index of the float64 record in the fixation's segment
+    int pad[2];
+};  // 96 B
+
+__device__ __forceinline__ void make_tri_f32(const GmScreenTri& T, int gidx, TriF32& o) {
+    const double ox = T.x0, oy = T.y0;
+    const double sx[3] = {T.sx0 - ox, T.sx1 - ox, T.sx2 - ox}, sy[3] = {T.sy0 - oy, T.sy1 - oy, T.sy2 - oy};
+    const double iw[3] = {T.iw0, T.iw1, T.iw2};
+    const double xmax = (double)(T.x1 - T.x0 + 1), ymax = (double)(T.y1 - T.y0 + 1);
+    double A = 0.0, B = 0.0, C = 0.0, Aab = 0.0, Bab = 0.0, Cab = 0.0;
+#pragma unroll
+    for (int i = 0; i < 3; i++) {
+        // edge i runs from vertex (i+1)%3 to (i+2)%3: w_i = (bx-ax)(py-ay) - (by-ay)(px-ax)
+        const int ia = (i + 1) % 3, ib = (i + 2) % 3;
+        const double ex = sx[ib] - sx[ia], ey = sy[ib] - sy[ia];
+        const double a = -ey, b = ex, c = ey * sx[ia] - ex * sy[ia];
+        o.a[i] = (float)a;
+        o.b[i] = (float)b;
+        o.c[i] = (float)c;
+        // float32 plane evaluation error <= ~4 * 2^-24 and the reference's float64
+        // rounding <= ~4 * 2^-53 of |a|(|x|+|ax|) + |b|(|y|+|ay|); tol is >= 2x that
+        const double mag = fabs(a) * (xmax + fabs(sx[ia])) + fabs(b) * (ymax + fabs(sy[ia]));
+        o.tol[i] = (float)(4.8e-7 * mag + 1e-30);
+        const double k = iw[i] * T.inv_area;  // l_i = w_i * inv_area, inv_w = sum l_i iw_i
+        A += a * k;
+        B += b * k;
+        C += c * k;
+        Aab += fabs(a * k);
+        Bab += fabs(b * k);
+        Cab += fabs(c * k);
+    }
+    o.A = (float)A;
+    o.B = (float)B;
+    o.C = (float)C;
+    o.tolw = (float)(4.8e-7 * (Aab * xmax + Bab * ymax + Cab) + 1e-30);
+    o.inv_minw = __double2float_ru(1.0 / (double)T.minw) * (1.0f + 1e-6f);
+    o.ox = T.x0;
+    o.oy = T.y0;
+    o.bx = (uint32_t)T.x0 | ((uint32_t)T.x1 << 16);
+    o.by = (uint32_t)T.y0 | ((uint32_t)T.y1 << 16);
+    o.gidx = gidx;
+    o.pad[0] = o.pad[1] = 0;
+}
+
 struct TriStore {
     GmScreenTri* tris;
+    TriF32* t32;  // float32 form of tris (same index)
     uint2* bbox;
     int* count;
     int64_t cap_seg;
@@ -289,6 +346,7 @@ __global__ void __launch_bounds__(256) k_tri_setup(const double* __restrict__ tw
         for (int q = 0; q < n; q++) {
             if (at + q < ts.cap_seg) {
                 seg[at + q] = out[q];
+                make_tri_f32(out[q], at + q, ts.t32[(int64_t)f * ts.cap_seg + at + q]);
                 segb[at + q] = make_uint2((uint32_t)out[q].x0 | ((uint32_t)out[q].x1 << 16),
                                           (uint32_t)out[q].y0 | ((uint32_t)out[q].y1 << 16));
             }
@@ -611,41 +669,12 @@ __global__ void __launch_bounds__(256) k_samples(const double* __restrict__ px, 
     }
 }
 
-// Fixation-major evaluation of the marked texels.  Every warp is an
-// independent work item (fixation, 32x16-pixel tile): no CTA barriers, no
-// atomics.
-//   1. the tile's triangles (from its coarse bin, bbox-filtered) are staged in
-//      the warp's shared slice TW_CAP at a time -- the exact float64 records
-//      and a float32 form of each (edge-function planes, inverse-depth plane,
-//      rigorous absolute error bounds of those planes) -- and sorted by their
-//      minimum depth, nearest first;
-//   2. lanes take the marked texels of the tile (compacted, 32 per round) and
-//      walk the sorted triangles with uniform float32 tests: a triangle is
-//      "certainly written" (inside by more than the bound, inverse depth
-//      certainly in (1/far, 1/near)) or "maybe written"; V = the largest
-//      certain lower bound of the inverse depth is a proof that the texel's
-//      depth is <= 1/V, so a maybe-triangle whose inverse-depth upper bound is
-//      < V can never be the minimum, and once the next triangle's bound
-//      1/minw is < V no later triangle can be either (early stop);
-//   3. the surviving candidates (normally one) are evaluated exactly with the
-//      reference's float64 pixel arithmetic (texel_depth) and the minimum is
-//      stored -- exactly the value kernels.rasterize leaves in that pixel.
 #define TW_CAP 32
 #define TW_SEL 128  // overlapping triangles remembered per tile (more: rescanned per round)
 #define TW_WARPS 4
-#define TW_K 4  // exact candidates remembered per texel before the slow path
-struct TriF32 {
-    float a[3], b[3], c[3], tol[3];  // edge planes e_i = a x + b y + c (tile-local), |e32 - e_ref| <= tol
-    float A, B, C, tolw;             // inverse-depth plane and its bound
-    float inv_minw;                  // >= every inverse depth the triangle writes
-    uint32_t bx, by;                 // bbox x0 | x1 << 16, y0 | y1 << 16 (tile-local, clamped)
-    int slot;                        // index of the float64 record in rec[]
-};
 struct __align__(16) TexelWarpSmem {
-    GmScreenTri rec[TW_CAP];
-    TriF32 t32[TW_CAP];  // in ascending min-depth order
+    TriF32 t32[TW_CAP];  // staged, in ascending min-depth order
     int sel[TW_SEL + 32];
-    int rank[TW_CAP];
 };
 #define TX_DYN_SMEM (TW_WARPS * (int)sizeof(TexelWarpSmem))
 
@@ -667,56 +696,14 @@ __device__ __forceinline__ int kth_set_bit(uint32_t w, int k) {
     return base;
 }
 
-// float32 planes of one screen triangle in tile-local pixel coordinates
-// (x - xb, y - yb), with error bounds that cover both the float32 evaluation
-// at any pixel centre of the tile and the reference's own float64 rounding
-// (kernels.py:107-125): |e32 - e_ref| <= tol, |invw32 - invw_ref| <= tolw.
-__device__ __forceinline__ void make_tri_f32(const GmScreenTri& T, int xb, int yb, int slot, TriF32& o) {
-    const double sx[3] = {T.sx0 - xb, T.sx1 - xb, T.sx2 - xb}, sy[3] = {T.sy0 - yb, T.sy1 - yb, T.sy2 - yb};
-    const double iw[3] = {T.iw0, T.iw1, T.iw2};
-    const double xmax = TW, ymax = TH;
-    double A = 0.0, B = 0.0, C = 0.0, Aab = 0.0, Bab = 0.0, Cab = 0.0;
-#pragma unroll
-    for (int i = 0; i < 3; i++) {
-        // edge i runs from vertex (i+1)%3 to (i+2)%3: w_i = (bx-ax)(py-ay) - (by-ay)(px-ax)
-        const int ia = (i + 1) % 3, ib = (i + 2) % 3;
-        const double ex = sx[ib] - sx[ia], ey = sy[ib] - sy[ia];
-        const double a = -ey, b = ex, c = ey * sx[ia] - ex * sy[ia];
-        o.a[i] = (float)a;
-        o.b[i] = (float)b;
-        o.c[i] = (float)c;
-        // float32 plane evaluation error <= ~4 * 2^-24 and the reference's float64
-        // rounding <= ~4 * 2^-53 of |a|(|x|+|ax|) + |b|(|y|+|ay|); tol is >= 2x that
-        const double mag = fabs(a) * (xmax + fabs(sx[ia])) + fabs(b) * (ymax + fabs(sy[ia]));
-        o.tol[i] = (float)(4.8e-7 * mag + 1e-30);
-        const double k = iw[i] * T.inv_area;  // l_i = w_i * inv_area, inv_w = sum l_i iw_i
-        A += a * k;
-        B += b * k;
-        C += c * k;
-        Aab += fabs(a * k);
-        Bab += fabs(b * k);
-        Cab += fabs(c * k);
-    }
-    o.A = (float)A;
-    o.B = (float)B;
-    o.C = (float)C;
-    o.tolw = (float)(4.8e-7 * (Aab * xmax + Bab * ymax + Cab) + 1e-30);
-    o.inv_minw = __double2float_ru(1.0 / (double)T.minw) * (1.0f + 1e-6f);
-    const int x0 = max((int)T.x0 - xb, 0), x1 = min((int)T.x1 - xb, TW - 1);
-    const int y0 = max((int)T.y0 - yb, 0), y1 = min((int)T.y1 - yb, TH - 1);
-    o.bx = (uint32_t)(x0 & 0xffff) | ((uint32_t)(x1 & 0xffff) << 16);
-    o.by = (uint32_t)(y0 & 0xffff) | ((uint32_t)(y1 & 0xffff) << 16);
-    o.slot = slot;
-}
-
 // Fixation-major evaluation of the marked texels.  Every warp is an
 // independent work item (fixation, 32x16-pixel tile): no CTA barriers, no
 // atomics, per-texel state in registers.
 //   1. the tile's triangles are gathered from its coarse bin (bbox-filtered);
-//   2. they are staged in the warp's shared slice TW_CAP at a time -- exact
-//      float64 records plus a float32 form (edge-function planes, inverse-depth
-//      plane, rigorous absolute error bounds) written in ascending min-depth
-//      order;
+//   2. their float32 forms (TriF32, built once per screen triangle by
+//      k_tri_setup: edge-function and inverse-depth planes with rigorous error
+//      bounds) are staged in the warp's shared slice TW_CAP at a time, in
+//      ascending min-depth order;
 //   3. lanes take the marked texels (compacted, 32 per round) and walk the
 //      sorted triangles with uniform float32 tests: "certainly written"
 //      (inside by more than the bound, inverse depth certainly within
@@ -725,8 +712,9 @@ __device__ __forceinline__ void make_tri_f32(const GmScreenTri& T, int xb, int y
 //      whose inverse-depth upper bound is < V can never be the minimum, and
 //      once a triangle's 1/minw bound is < V no later one can be (stop);
 //   4. the surviving candidates (normally one) are evaluated exactly with the
-//      reference's float64 pixel arithmetic (texel_depth) and the minimum is
-//      stored -- the value kernels.rasterize leaves in that pixel.
+//      reference's float64 pixel arithmetic (texel_depth, float64 record read
+//      from L1/L2) and the minimum is stored -- the value kernels.rasterize
+//      leaves in that pixel.
 __global__ void __launch_bounds__(TW_WARPS * 32) k_texels(TriStore ts, DepthView dv, CoarseBins cb, int tiles_x,
                                                           int tiles_per_fix, int64_t n_items,
                                                           const GmFixExact* __restrict__ fixes, long long b0) {
@@ -794,15 +782,12 @@ __global__ void __launch_bounds__(TW_WARPS * 32) k_texels(TriStore ts, DepthView
         return cnt;  // may exceed TW_SEL by < 32 (S.sel has the room)
     };
 
-    // 2. stage S.sel[c0 .. c0 + kend) sorted by min depth
+    // 2. stage S.sel[c0 .. c0 + kend) (float32 forms) in ascending min-depth order
+    const TriF32* segf = ts.t32 + (int64_t)f * ts.cap_seg;
     auto stage = [&](int c0, int kend) {
         __syncwarp();
-        for (int q = lane; q < kend * 6; q += 32) {
-            const int ti = q / 6, part = q - ti * 6;
-            reinterpret_cast<uint4*>(&S.rec[ti])[part] = reinterpret_cast<const uint4*>(seg + S.sel[c0 + ti])[part];
-        }
-        __syncwarp();
-        float key = lane < kend ? S.rec[lane].minw : CUDART_INF_F;
+        const int gi = lane < kend ? S.sel[c0 + lane] : 0;
+        float key = lane < kend ? -__ldg(&segf[gi].inv_minw) : CUDART_INF_F;  // ascending min depth
         int slot = lane;
 #pragma unroll
         for (int size = 2; size <= 32; size <<= 1) {
@@ -818,9 +803,14 @@ __global__ void __launch_bounds__(TW_WARPS * 32) k_texels(TriStore ts, DepthView
                 }
             }
         }
-        S.rank[slot] = lane;  // lane = rank of record `slot`
-        __syncwarp();
-        if (lane < kend) make_tri_f32(S.rec[lane], xb, yb, lane, S.t32[S.rank[lane]]);
+        // lane = rank; it copies the record of sorted position `lane`
+        const int src = __shfl_sync(FULL, gi, slot);
+        if (lane < kend) {
+            const uint4* from = reinterpret_cast<const uint4*>(segf + src);
+            uint4* to = reinterpret_cast<uint4*>(&S.t32[lane]);
+#pragma unroll
+            for (int part = 0; part < 6; part++) to[part] = from[part];
+        }
         __syncwarp();
     };
 
@@ -840,19 +830,19 @@ __global__ void __launch_bounds__(TW_WARPS * 32) k_texels(TriStore ts, DepthView
 
     // 3 + 4 for the staged chunk (kend triangles) and one texel: updates V, best
     auto walk = [&](int kend, bool valid, int row, int colo, float& V, double& best) {
-        const float fx = (float)colo + 0.5f, fy = (float)row + 0.5f;  // tile-local pixel centre
-        int cand_slot[TW_K];
-        float cand_hi[TW_K];
-        int ncand = 0;
+        const int px = xb + colo, py = yb + row;
+        int cs0 = -1, cs1 = -1;  // exact candidates (global record index) and their bounds
+        float ch0 = 0.0f, ch1 = 0.0f;
         bool overflow = false;
         for (int kk = 0; kk < kend; kk++) {
             const TriF32& t = S.t32[kk];
             const float inv_minw = t.inv_minw;
             if (__all_sync(FULL, !(inv_minw >= V))) break;  // nothing later can be nearer
             const uint32_t tbx = t.bx, tby = t.by;
-            if (!(inv_minw >= V) || colo < (int)(tbx & 0xffff) || colo > (int)(tbx >> 16) ||
-                row < (int)(tby & 0xffff) || row > (int)(tby >> 16))
+            if (!(inv_minw >= V) || px < (int)(tbx & 0xffff) || px > (int)(tbx >> 16) || py < (int)(tby & 0xffff) ||
+                py > (int)(tby >> 16))
                 continue;
+            const float fx = (float)(px - t.ox) + 0.5f, fy = (float)(py - t.oy) + 0.5f;  // bbox-local centre
             bool maybe = true, certain = true;
 #pragma unroll
             for (int i = 0; i < 3; i++) {
@@ -867,31 +857,44 @@ __global__ void __launch_bounds__(TW_WARPS * 32) k_texels(TriStore ts, DepthView
             if (certain && lo > 0.0f && hi <= inv_near_lo && lo >= inv_far_hi && lo * (1.0f - 1e-6f) > V)
                 V = lo * (1.0f - 1e-6f);
             if (hi >= V) {
-                if (ncand < TW_K) {
-                    cand_slot[ncand] = t.slot;
-                    cand_hi[ncand] = hi;
-                    ncand++;
+                if (cs0 < 0) {
+                    cs0 = t.gidx;
+                    ch0 = hi;
+                } else if (cs1 < 0) {
+                    cs1 = t.gidx;
+                    ch1 = hi;
+                } else if (ch0 < V) {  // a stale candidate can be replaced
+                    cs0 = t.gidx;
+                    ch0 = hi;
+                } else if (ch1 < V) {
+                    cs1 = t.gidx;
+                    ch1 = hi;
                 } else {
                     overflow = true;
                 }
             }
         }
-        const int px = xb + colo, py = yb + row;
+        if (!valid) return;
         if (!overflow) {
-#pragma unroll
-            for (int c = 0; c < TW_K; c++) {
-                if (valid && c < ncand && cand_hi[c] >= V) {
-                    const double d = texel_depth(S.rec[cand_slot[c]], px, py, near_, far_);
-                    c_pairs++;
-                    c_cov += d < CUDART_INF;
-                    if (d < best) best = d;
-                }
+            if (cs0 >= 0 && ch0 >= V) {
+                const double d = texel_depth(seg[cs0], px, py, near_, far_);
+                c_pairs++;
+                c_cov += d < CUDART_INF;
+                if (d < best) best = d;
             }
-        } else if (valid) {  // slow path: every staged triangle whose bbox covers the texel
+            if (cs1 >= 0 && ch1 >= V) {
+                const double d = texel_depth(seg[cs1], px, py, near_, far_);
+                c_pairs++;
+                c_cov += d < CUDART_INF;
+                if (d < best) best = d;
+            }
+        } else {  // slow path: every staged triangle whose bbox covers the texel
             for (int k = 0; k < kend; k++) {
-                const GmScreenTri& T = S.rec[k];
-                if (px < T.x0 || px > T.x1 || py < T.y0 || py > T.y1) continue;
-                const double d = texel_depth(T, px, py, near_, far_);
+                const TriF32& t = S.t32[k];
+                if (px < (int)(t.bx & 0xffff) || px > (int)(t.bx >> 16) || py < (int)(t.by & 0xffff) ||
+                    py > (int)(t.by >> 16))
+                    continue;
+                const double d = texel_depth(seg[t.gidx], px, py, near_, far_);
                 c_pairs++;
                 c_cov += d < CUDART_INF;
                 if (d < best) best = d;
@@ -1065,6 +1068,7 @@ struct gm_plan {
     cudaEvent_t h_ev[GM_RING] = {};
     // per-fixation screen-triangle segments
     GmScreenTri* d_tris = nullptr;
+    TriF32* d_t32 = nullptr;
     uint2* d_bbox = nullptr;
     int* d_count = nullptr;
     int64_t cap_seg = 0, cap_seg_B = 0;
@@ -1144,7 +1148,7 @@ extern "C" void gm_plan_destroy(gm_plan* p) {
     for (int r = 0; r < GM_RING; r++) {
         cudaFreeHost(p->h_fix[r]); cudaFreeHost(p->h_cull[r]); cudaEventDestroy(p->h_ev[r]);
     }
-    cudaFree(p->d_tris); cudaFree(p->d_bbox); cudaFree(p->d_count); cudaFree(p->d_fail); cudaFree(p->d_maxcount); cudaFree(p->d_ntris); cudaFree(p->d_work);
+    cudaFree(p->d_tris); cudaFree(p->d_t32); cudaFree(p->d_bbox); cudaFree(p->d_count); cudaFree(p->d_fail); cudaFree(p->d_maxcount); cudaFree(p->d_ntris); cudaFree(p->d_work);
     cudaFree(p->d_scan_tmp); cudaFree(p->d_max); cudaFree(p->d_stats);
     cudaFree(p->d_fix_all); cudaFree(p->d_cull_all); cudaFree(p->d_flush);
     cudaFree(p->d_depth); cudaFree(p->d_mask); cudaFree(p->d_vbuf);
@@ -1296,6 +1300,7 @@ static int ensure_batch(gm_plan* p, int B, int W, int H, int64_t seg) {
     if (seg > p->cap_seg || (int64_t)B * seg > p->cap_seg_B) {
         int64_t cs = std::max(seg, p->cap_seg);
         if ((rc = dev_alloc(&p->d_tris, (size_t)(B * cs)))) return rc;
+        if ((rc = dev_alloc(&p->d_t32, (size_t)(B * cs)))) return rc;
         if ((rc = dev_alloc(&p->d_bbox, (size_t)(B * cs)))) return rc;
         p->cap_seg = cs;
         p->cap_seg_B = B * cs;
@@ -1351,7 +1356,7 @@ static int enqueue_batch(gm_plan* p, const GmFixExact* d_fix, const GmFixCull* d
     cudaStream_t s = p->stream;
     const int wwords = (W + 31) / 32;
     const int tiles_x = (W + TW - 1) / TW, tiles_y = (H + TH - 1) / TH;
-    TriStore ts{p->d_tris, p->d_bbox, p->d_count, p->cap_seg, p->d_fail, p->d_maxcount, p->d_ntris};
+    TriStore ts{p->d_tris, p->d_t32, p->d_bbox, p->d_count, p->cap_seg, p->d_fail, p->d_maxcount, p->d_ntris};
     DepthView dv{p->d_depth, p->d_mask, W, H, wwords, (cfg->flags & GM_FLAG_STATS) ? p->d_stats : nullptr,
                  p->d_vbuf};
     if (ev) CK(cudaEventRecord(ev[0], s));
@@ -1787,7 +1792,7 @@ extern "C" int gm_plan_depth_buffer(gm_plan* p, const double* fx, double theta, 
         k_set_i64<<<1, 1, 0, s>>>(p->d_fail, LLONG_MAX);
         CK(cudaMemsetAsync(p->d_maxcount, 0, sizeof(int), s));
         CK(cudaMemsetAsync(p->d_count, 0, sizeof(int), s));
-        TriStore ts{p->d_tris, p->d_bbox, p->d_count, p->cap_seg, p->d_fail, p->d_maxcount, p->d_ntris};
+        TriStore ts{p->d_tris, p->d_t32, p->d_bbox, p->d_count, p->cap_seg, p->d_fail, p->d_maxcount, p->d_ntris};
         if (p->n_clu > 0) {
             dim3 grid(blocks_for((p->n_clu + 31) / 32, 8), 1);
             k_tri_setup<<<grid, 256, 0, s>>>(p->d_tw, p->T, p->d_tsph, p->d_csph, p->n_clu, p->d_fix, p->d_cull, res,
@@ -1803,7 +1808,7 @@ extern "C" int gm_plan_depth_buffer(gm_plan* p, const double* fx, double theta, 
         p->cap_seg = 0;
         if ((rc = ensure_batch(p, 1, res, res, want))) return rc;
     }
-    TriStore ts{p->d_tris, p->d_bbox, p->d_count, p->cap_seg, p->d_fail, p->d_maxcount, p->d_ntris};
+    TriStore ts{p->d_tris, p->d_t32, p->d_bbox, p->d_count, p->cap_seg, p->d_fail, p->d_maxcount, p->d_ntris};
     const int tiles_x = (res + TW - 1) / TW, tiles_y = (res + TH - 1) / TH;
     DepthView dv{p->d_depth, p->d_mask, res, res, wwords, nullptr, p->d_vbuf};
     k_mark_all<<<blocks_for((int64_t)res * wwords, 256), 256, 0, s>>>(p->d_mask, res, res, wwords);
