@@ -3,5 +3,5 @@ timeout 1200 python -m pytest tests -m gpu -q --timeout 600 -p no:cacheprovider 
 echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 timeout 900 python bench.py --steps 3 --warmup 3 --no-cpu > gpurun_out/bench.log 2>&1
 echo "rc=$?" >> gpurun_out/bench.log
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_texels' -s 10 -c 1 -o gpurun_out/prof_r1h python bench.py --fixations 4096 --batch 512 --steps 1 --warmup 3 --no-cpu --no-e2e > gpurun_out/ncu_full.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_mark|k_samples|k_texels' -s 30 -c 3 -o gpurun_out/prof_r1h python bench.py --fixations 4096 --batch 512 --steps 1 --warmup 3 --no-cpu --no-e2e > gpurun_out/ncu_full.log 2>&1
 echo "rc=$?" >> gpurun_out/ncu_full.log
