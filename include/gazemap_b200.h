@@ -159,6 +159,31 @@ int gm_plan_candidates(gm_plan* plan, const double* fixations, int64_t F, double
 /* World sample positions of the plan (N x 3), _SampleCache.base_world. */
 int gm_plan_positions(gm_plan* plan, double* out);
 
+/* ---- fixation-log ingestion ----------------------------- */
+
+/* parse_fixation_log (gaze.py:130-188) line scanner over an in-memory log
+ * (bytes of the file).  Multi-threaded (threads <= 0: all) over line-aligned
+ * chunks.  Produces every numeric row before the first failing line: the
+ * 18 fields with the gaze normalised like Fixation.__post_init__
+ * (gaze.py:91-95), the row's Fixation validation verdict, its source line and
+ * its pose-override groups (object id + 10 floats).  The time window and the
+ * error policy are applied by the caller (fixlog.py).  Returns 0 and a handle
+ * unless the arguments are invalid. */
+typedef struct gm_fixlog gm_fixlog;
+int gm_fixlog_parse(const char* buf, int64_t len, int threads, gm_fixlog** out);
+int64_t gm_fixlog_rows(const gm_fixlog* log);
+int64_t gm_fixlog_groups(const gm_fixlog* log);
+/* table rows x 18; line rows; code rows (0 valid, 1 zero gaze, 2 duration,
+ * 3 near/far, 4 bounds, 5 gaze z >= 0); gstart rows + 1; goid groups x 2 (byte
+ * offset, length of the object id); gvals groups x 10.  Outputs may be NULL. */
+int gm_fixlog_copy(const gm_fixlog* log, double* table, int64_t* line, int32_t* code, int64_t* gstart,
+                   int64_t* goid, double* gvals);
+/* info[7]: kind (0 none, 1 < 18 fields, 2 bad number, 3 override group count,
+ * 4 bad override number, 5 non-ASCII buffer, 6 separators-only line), line,
+ * token offset, token length, field count, line offset, line length. */
+int gm_fixlog_error(const gm_fixlog* log, int64_t* info);
+void gm_fixlog_free(gm_fixlog* log);
+
 #ifdef __cplusplus
 }
 #endif

@@ -10,6 +10,7 @@ from .density import (DEFAULT_EPS_ABS, DEFAULT_EPS_REL, DEFAULT_K, DEFAULT_RESOL
 from .errors import (ConfigError, GazemapError, GazeOutsideFrustumError, InvalidFrustumError, LayoutMismatchError,
                      ParseError)
 from .estimator import FixationDensityMapper
+from .fixlog import FixationLog, parse_fixation_log, parse_fixation_table
 from .gaze import (DEFAULT_THETA, SQRT_TWO_PI, Fixation, GazeCone, fixation_setup, fixation_table,
                    frustum_from_matrix, gaussian_weight, perspective_matrix)
 from .geometry import (Mesh, SampledMesh, Scene, SceneObject, Transform, TriangleSampling, adaptive_resolution,

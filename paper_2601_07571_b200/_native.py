@@ -7,6 +7,7 @@ is visible, every compute call raises `NativeUnavailableError`.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from pathlib import Path
 
@@ -84,6 +85,12 @@ SIGNATURES = {
     "gm_plan_candidates": (ctypes.c_int, [_VP, _D, ctypes.c_int64, ctypes.c_double, ctypes.c_int, ctypes.c_int,
                                           _I64, ctypes.c_int64, _I64]),
     "gm_plan_positions": (ctypes.c_int, [_VP, _D]),
+    "gm_fixlog_parse": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int64, ctypes.c_int, ctypes.POINTER(_VP)]),
+    "gm_fixlog_rows": (ctypes.c_int64, [_VP]),
+    "gm_fixlog_groups": (ctypes.c_int64, [_VP]),
+    "gm_fixlog_copy": (ctypes.c_int, [_VP, _D, _I64, ctypes.c_void_p, _I64, _I64, _D]),
+    "gm_fixlog_error": (ctypes.c_int, [_VP, _I64]),
+    "gm_fixlog_free": (None, [_VP]),
 }
 
 _lib = None
@@ -98,7 +105,8 @@ def load(build_if_missing: bool = True):
     with _lock:
         if _lib is not None:
             return _lib
-        if build_if_missing:
+        so_path = Path(os.environ.get("GAZEMAP_B200_SO", SO_PATH))  # experimental variants (build.py)
+        if build_if_missing and so_path == SO_PATH:
             try:
                 from . import build as _build
 
@@ -107,12 +115,12 @@ def load(build_if_missing: bool = True):
             except Exception as e:  # no nvcc on this host: only a prebuilt .so can work
                 if not SO_PATH.exists():
                     raise NativeUnavailableError(f"CUDA extension missing and build failed: {e}") from e
-        if not SO_PATH.exists():
-            raise NativeUnavailableError(f"CUDA extension not built: {SO_PATH}")
+        if not so_path.exists():
+            raise NativeUnavailableError(f"CUDA extension not built: {so_path}")
         try:
-            lib = ctypes.CDLL(str(SO_PATH))
+            lib = ctypes.CDLL(str(so_path))
         except OSError as e:
-            raise NativeUnavailableError(f"cannot load {SO_PATH}: {e}") from e
+            raise NativeUnavailableError(f"cannot load {so_path}: {e}") from e
         for name, (res, args) in SIGNATURES.items():
             fn = getattr(lib, name)
             fn.restype = res

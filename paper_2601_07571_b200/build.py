@@ -50,25 +50,30 @@ def needs_build() -> bool:
     return any(s.stat().st_mtime > t for s in _sources()) or Path(__file__).stat().st_mtime > t
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, defines=(), out: Path | None = None) -> Path:
+    """Compile the extension; `defines`/`out` build an experimental variant
+    (e.g. defines=["-DKS_MINB=4"], out=PKG / "_variant.so") without touching
+    the production library."""
+    so = Path(out) if out else SO
+    if not force and not defines and out is None and not needs_build():
         return SO
-    BUILD.mkdir(exist_ok=True)
+    build_dir = BUILD if out is None else BUILD / so.stem
+    build_dir.mkdir(parents=True, exist_ok=True)
     gxx = _tool("g++", "g++")
     nvcc = _nvcc()
     objs = []
     cmds = []
     for cu in sorted(CSRC.glob("*.cu")):
-        obj = BUILD / (cu.stem + ".o")
+        obj = build_dir / (cu.stem + ".o")
         cmds.append([nvcc, "-c", str(cu), "-o", str(obj), *ARCH, "-O3", "-std=c++17", "-lineinfo", "-fmad=false",
-                     "-Xptxas", "-v", "-ccbin", gxx, "-Xcompiler", "-fPIC", "-I", str(CSRC)])
+                     "-Xptxas", "-v", "-ccbin", gxx, "-Xcompiler", "-fPIC", "-I", str(CSRC), *defines])
         objs.append(obj)
     for cpp in sorted(CSRC.glob("*.cpp")):
-        obj = BUILD / (cpp.stem + ".o")
+        obj = build_dir / (cpp.stem + ".o")
         cmds.append([gxx, "-c", str(cpp), "-o", str(obj), "-O2", "-std=c++17", "-fPIC", "-fopenmp",
                      "-ffp-contract=off", "-fno-fast-math", "-fno-builtin", "-I", str(CSRC)])
         objs.append(obj)
-    tmp = SO.with_suffix(".so.tmp")
+    tmp = so.with_suffix(".so.tmp")
     cmds.append([nvcc, "-shared", *ARCH, "-o", str(tmp), *map(str, objs), "-ccbin", gxx, "-Xcompiler", "-fopenmp",
                  "-lgomp"])
     for c in cmds:
@@ -78,9 +83,9 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         if r.returncode:
             raise RuntimeError(f"build failed: {' '.join(c[:3])} ...")
         if "-Xptxas" in c:
-            (BUILD / (Path(c[2]).stem + ".ptxas.txt")).write_text(r.stderr)
-    os.replace(tmp, SO)
-    return SO
+            (build_dir / (Path(c[2]).stem + ".ptxas.txt")).write_text(r.stderr)
+    os.replace(tmp, so)
+    return so
 
 
 if __name__ == "__main__":

@@ -737,6 +737,7 @@ __global__ void __launch_bounds__(256) k_mark(const float* __restrict__ pxf, con
     }
 }
 
+template <bool STATS>
 __global__ void __launch_bounds__(256) k_samples(const double* __restrict__ px, const double* __restrict__ py,
                                                  const double* __restrict__ pz, const float4* __restrict__ chunks,
                                                  const uint32_t* __restrict__ lvl1, const int* __restrict__ order,
@@ -753,7 +754,7 @@ __global__ void __launch_bounds__(256) k_samples(const double* __restrict__ px, 
     const double Wd = (double)W, Hd = (double)H;
     const double lo = -1.0 - GM_NDC_SLACK, hi = 1.0 + GM_NDC_SLACK;
     const int64_t n_items = n_supers * 8;
-    unsigned long long c_l1 = 0, c_l2 = 0, c_exact = 0, c_ndc = 0, c_cand = 0, c_vis = 0;
+    unsigned c_l1 = 0, c_l2 = 0, c_exact = 0, c_ndc = 0, c_cand = 0, c_vis = 0;
     // persistent warps; items = chunks of the super-chunks in descending-work
     // order (k_level1 + radix sort), claimed one at a time
     for (;;) {
@@ -765,7 +766,7 @@ __global__ void __launch_bounds__(256) k_samples(const double* __restrict__ px, 
         const int64_t ch = sc * 8 + (item & 7);
         if (ch >= n_chunks) continue;
         const unsigned l1 = lane < ngroups ? lvl1[sc * ngroups + lane] : 0u;  // lane g: group g
-        c_l1 += 1;
+        if (STATS) c_l1 += 1;
         if (!__any_sync(0xffffffffu, l1 != 0u)) continue;
         {
         const int64_t i = ch * 32 + lane;
@@ -784,7 +785,7 @@ __global__ void __launch_bounds__(256) k_samples(const double* __restrict__ px, 
             const int g = gi * 32;
             // level 2: this chunk's 32 samples against the fixations that passed level 1
             bool pass = ((sm >> lane) & 1u) && sphere_visible(culls[g + lane], sph, false);
-            c_l2 += (sm >> lane) & 1u;
+            if (STATS) c_l2 += (sm >> lane) & 1u;
             unsigned mask = __ballot_sync(0xffffffffu, pass);
             while (mask) {
                 const int j = __ffs(mask) - 1;
@@ -792,7 +793,7 @@ __global__ void __launch_bounds__(256) k_samples(const double* __restrict__ px, 
                 if (!valid) continue;
                 const int f = g + j;
                 const GmFixExact& F = fixes[f];
-                c_exact++;
+                if (STATS) c_exact++;
                 // kernels.py:305-319
                 double x = F.rot[0] * wx + F.rot[1] * wy + F.rot[2] * wz + F.trans[0];
                 double y = F.rot[3] * wx + F.rot[4] * wy + F.rot[5] * wz + F.trans[1];
@@ -805,7 +806,7 @@ __global__ void __launch_bounds__(256) k_samples(const double* __restrict__ px, 
                 double ndc_y = (F.p11 * y + F.p12 * z) / w;
                 if (ndc_x < lo || ndc_x > hi) continue;
                 if (ndc_y < lo || ndc_y > hi) continue;
-                c_ndc++;
+                if (STATS) c_ndc++;
                 // kernels.py:330-339 (moved before the depth test)
                 double d1 = x * F.gaze[0] + y * F.gaze[1] + z * F.gaze[2];
                 if (d1 <= 0.0) continue;
@@ -813,7 +814,7 @@ __global__ void __launch_bounds__(256) k_samples(const double* __restrict__ px, 
                 if (d2sq < 0.0) d2sq = 0.0;
                 double ratio_sq = d2sq * inv_sigma * inv_sigma / (d1 * d1);
                 if (ratio_sq > 16.0) continue;
-                c_cand++;
+                if (STATS) c_cand++;
                 // texel coordinates (kernels.py:327, :231-232, :267-276)
                 double gx = (ndc_x + 1.0) * 0.5 * Wd - 0.5;
                 double gy = (1.0 - ndc_y) * 0.5 * Hd - 0.5;
@@ -829,20 +830,20 @@ __global__ void __launch_bounds__(256) k_samples(const double* __restrict__ px, 
                 double eps = eps_abs;
                 if (eps_rel * d > eps) eps = eps_rel * d;
                 if (!depth_test(dv, f, gx, gy, bx0, bx1, by0, by1, d, eps)) continue;
-                c_vis++;
+                if (STATS) c_vis++;
                 v += F.amp * exp(-0.5 * ratio_sq);  // kernels.py:340
             }
         }
         if (valid) values[i] = v;
         }
     }
-    if (dv.stats) {
+    if (STATS) {
         if (lane == 0) atomicAdd(dv.stats + GM_STAT_L1_TESTS, c_l1 * (unsigned long long)B);
-        atomicAdd(dv.stats + GM_STAT_L2_TESTS, c_l2);
-        atomicAdd(dv.stats + GM_STAT_EXACT, c_exact);
-        atomicAdd(dv.stats + GM_STAT_NDC, c_ndc);
-        atomicAdd(dv.stats + GM_STAT_CANDIDATES, c_cand);
-        atomicAdd(dv.stats + GM_STAT_VISIBLE, c_vis);
+        atomicAdd(dv.stats + GM_STAT_L2_TESTS, (unsigned long long)c_l2);
+        atomicAdd(dv.stats + GM_STAT_EXACT, (unsigned long long)c_exact);
+        atomicAdd(dv.stats + GM_STAT_NDC, (unsigned long long)c_ndc);
+        atomicAdd(dv.stats + GM_STAT_CANDIDATES, (unsigned long long)c_cand);
+        atomicAdd(dv.stats + GM_STAT_VISIBLE, (unsigned long long)c_vis);
     }
 }
 
@@ -1582,9 +1583,10 @@ static int enqueue_batch(gm_plan* p, const GmFixExact* d_fix, const GmFixCull* d
         k_texels<<<(unsigned)((items + TW_WARPS - 1) / TW_WARPS), TW_WARPS * 32, TX_DYN_SMEM, s>>>(
             ts, dv, cbins, tiles_x, tiles_x * tiles_y, items, d_fix, b0);
         if (ev) CK(cudaEventRecord(ev[3], s));
-        k_samples<<<grid, 256, 0, s>>>(p->d_px, p->d_py, p->d_pz, p->d_chunk, p->d_lvl1, p->d_lorder2,
-                                              p->d_work + 1, p->N, p->n_chunks, p->n_supers, d_fix, d_cull, nb, dv,
-                                              inv_sigma, cfg->eps_abs, cfg->eps_rel, p->d_values, p->d_fail, b0);
+        auto ks = dv.stats ? k_samples<true> : k_samples<false>;
+        ks<<<grid, 256, 0, s>>>(p->d_px, p->d_py, p->d_pz, p->d_chunk, p->d_lvl1, p->d_lorder2, p->d_work + 1, p->N,
+                                p->n_chunks, p->n_supers, d_fix, d_cull, nb, dv, inv_sigma, cfg->eps_abs,
+                                cfg->eps_rel, p->d_values, p->d_fail, b0);
     } else if (ev) {
         CK(cudaEventRecord(ev[2], s));
         CK(cudaEventRecord(ev[3], s));

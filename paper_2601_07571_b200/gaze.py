@@ -112,6 +112,9 @@ class Fixation:
 def fixation_table(fixations) -> np.ndarray:
     """(F, 18) float64 table from Fixation objects (this package's or any
     object with the reference's fields) or pass an (F, 18) array through."""
+    table = getattr(fixations, "table", None)  # FixationLog (fixlog.parse_fixation_log)
+    if isinstance(table, np.ndarray) and isinstance(fixations, list) and len(table) == len(fixations):
+        return table
     if isinstance(fixations, np.ndarray):
         t = np.ascontiguousarray(fixations, dtype=np.float64)
         if t.ndim != 2 or t.shape[1] != FIX_COLUMNS:

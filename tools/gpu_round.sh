@@ -1,7 +1,15 @@
+# One GPU round: parity tests, smoke, bench (both arms), launch list, one ncu --set full capture.
 mkdir -p gpurun_out
-timeout 1200 python -m pytest tests -m gpu -q --timeout 600 -p no:cacheprovider -x --durations=8 > gpurun_out/pytest_gpu.log 2>&1
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/gpu.txt 2>&1
+timeout 1500 python -m pytest tests -m gpu -q --timeout 900 -p no:cacheprovider -x --durations=12 > gpurun_out/pytest_gpu.log 2>&1
 echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-timeout 900 python bench.py --steps 3 --warmup 3 --no-cpu > gpurun_out/bench.log 2>&1
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
+echo "rc=$?" >> gpurun_out/smoke.log
+timeout 900 python bench.py --steps 3 --warmup 3 > gpurun_out/bench.log 2>&1
 echo "rc=$?" >> gpurun_out/bench.log
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_mark|k_samples|k_texels' -s 30 -c 3 -o gpurun_out/prof_r1h python bench.py --fixations 4096 --batch 512 --steps 1 --warmup 3 --no-cpu --no-e2e > gpurun_out/ncu_full.log 2>&1
+timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.log 2>&1
+echo "rc=$?" >> gpurun_out/bench_ref.log
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file gpurun_out/launches.csv python bench.py --fixations 8192 --batch 512 --steps 1 --warmup 3 --no-cpu --no-e2e > gpurun_out/ncu_launches.log 2>&1
+echo "rc=$?" >> gpurun_out/ncu_launches.log
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_tri_setup|k_samples|k_texels|k_coarse|k_level1' -s 60 -c 6 -o gpurun_out/prof_r1 python bench.py --fixations 4096 --batch 512 --steps 1 --warmup 3 --no-cpu --no-e2e > gpurun_out/ncu_full.log 2>&1
 echo "rc=$?" >> gpurun_out/ncu_full.log
