@@ -42,7 +42,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c2off", "c5"])
+    ap.add_argument("--config", default="c2",
+                    choices=["c1", "c2", "c2off", "c3k1", "c3k3", "c3k10", "c3k30", "c3k100", "c4", "c5"])
     ap.add_argument("--fixations", type=int, default=0, help="override fixations per rank")
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
@@ -62,6 +63,16 @@ def workload(name: str, n_fix: int, rank: int):
         k = 10_000.0
         fx = W.room_fixations(n_fix or 100_000, seed=1 + 1000 * rank, scene=scene)
         filtering = name == "c2"
+    elif name.startswith("c3k"):
+        scene = W.room_scene()
+        k = 1000.0 * int(name[3:])
+        fx = W.room_fixations(n_fix or 10_000, seed=1 + 1000 * rank, scene=scene)
+    elif name == "c4":
+        scene = W.room_scene()
+        k = 10_000.0
+        fx = W.session_fixations(scene=scene)
+        if n_fix:
+            fx = fx[:n_fix]
     elif name == "c5":
         scene = W.shells_scene()
         k = 20_000.0
@@ -73,7 +84,9 @@ def workload(name: str, n_fix: int, rank: int):
     desc = {"c1": "C1 icosphere(3), k=1e3, 200 fixations",
             "c2": "C2 room 98,080 tris/20 objects, k=1e4, 100k fixations, filtering on",
             "c2off": "C2 room 98,080 tris/20 objects, k=1e4, 100k fixations, filtering off",
-            "c5": "C5 12 nested icosphere(6) shells 983,040 tris, k=2e4, 50k fixations"}[name]
+            "c4": "C4 room, 50 users x 20k fixations (1M), k=1e4, filtering on",
+            "c5": "C5 12 nested icosphere(6) shells 983,040 tris, k=2e4, 50k fixations"}.get(
+                name, f"C3 room sample-density sweep, k={name[3:]}e3, 10k fixations")
     return scene, k, np.ascontiguousarray(fx), filtering, desc
 
 
@@ -157,7 +170,7 @@ def run_reference(args, rank, world):
         return
     scene, k, fx, filtering, desc = workload(args.config, args.fixations, 0)
     threads = host_threads()
-    per_step = args.cpu_fixations or (100 if args.config != "c1" else 200)
+    per_step = args.cpu_fixations or (300 if args.config != "c1" else 200)
     from oracle import oracle as O
 
     lay = O.build_layouts(scene, k)
@@ -260,9 +273,10 @@ def run_ours(args, rank, world):
         step_ms = float(tt.item())
     value = world * N * F / (step_ms / 1e3)
     tm = tms[-1]
-    # per step: k_set_i64; per batch: k_tri_setup, k_samples<mark>, k_texels, k_samples<accumulate>;
-    # then k_max
-    launches = int(tm.batches) * 4 + 2
+    # per step: k_set_i64, then per batch k_tri_setup, k_level1, k_fix32, k_mark, k_coarse, k_texels,
+    # k_samples (+ 4 CUB radix-sort kernels ordering the super-chunks); then k_max
+    launches = int(tm.batches) * 7 + 2
+    library_launches = int(tm.batches) * 4
 
     # ---- e2e through the public API (host table in, host values out) -----
     # Every step: fixation table (host) -> host setup -> H2D -> kernels -> D2H of
@@ -335,7 +349,7 @@ def run_ours(args, rank, world):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
-            n_cpu = args.cpu_fixations or (200 if args.config == "c1" else 100)
+            n_cpu = args.cpu_fixations or (200 if args.config == "c1" else 1000)
             v, dt, _ = cpu_port_pairs_per_s(scene, k, fx, filtering, n_cpu, host_threads())
             cpu = {"value": v, "unit": UNIT, "cores": host_threads(), "kind": "port",
                    "sample": f"first {n_cpu} fixations of the workload ({dt:.1f} s), oracle/gm_oracle.c with OpenMP"}
@@ -353,6 +367,7 @@ def run_ours(args, rank, world):
                        "l2": "flushed (512 MiB write) before every timed step",
                        "timing": "CUDA events on the plan stream around each full generation (+ all-reduce)"},
             "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "clocks": clk.summary(), "gpu_launches": launches,
+            "library_launches": library_launches,
             "phases_ms": {"cull": tm.cull_ms, "mark": tm.mark_ms, "texels": tm.texel_ms,
                           "accumulate": tm.accumulate_ms, "batches": tm.batches, "retries": tm.retries,
                           "screen_tris": tm.screen_tris},

@@ -110,6 +110,13 @@ int gm_plan_set_host_threads(gm_plan* plan, int n);
  * objects' samples concatenated in object order. */
 int gm_plan_set_scene(gm_plan* plan, int n_obj, const int64_t* tri_counts, const double* tri_local,
                       const double* xforms, const int64_t* res, const uint8_t* include);
+/* Replace the object poses (n_obj x [t, q, s]) of a plan: world triangles and
+ * sample positions are recomputed from the local layout on the device
+ * (Transform.apply, geometry.py:86-89, as _SampleCache.world applies a pose
+ * override, density.py:121-127, and scene_world_triangles(scene, overrides),
+ * raster.py:68-78).  The accumulated values are kept: generate() walks a
+ * dynamic-scene log as runs of fixations sharing one override set. */
+int gm_plan_set_poses(gm_plan* plan, const double* xforms);
 int64_t gm_plan_num_samples(gm_plan* plan);
 int64_t gm_plan_num_triangles(gm_plan* plan);
 double* gm_plan_values_device(gm_plan* plan); /* device pointer to the N accumulators */
@@ -183,6 +190,20 @@ int gm_fixlog_copy(const gm_fixlog* log, double* table, int64_t* line, int32_t* 
  * token offset, token length, field count, line offset, line length. */
 int gm_fixlog_error(const gm_fixlog* log, int64_t* info);
 void gm_fixlog_free(gm_fixlog* log);
+
+/* ---- export wire format --------------------------------- */
+
+/* write_export records (io_export.py:63-116) of one object, byte-identical to
+ * the reference: "oid,tri,within,w1,w2,w3,lx,ly,lz,wx,wy,wz,value\n" per
+ * sample, floats as Python f"{x:.9g}".  res/offsets: the SampledMesh layout
+ * (T); local/world: N x 3; values: N.  OpenMP over sample ranges. */
+typedef struct gm_buffer gm_buffer;
+int gm_export_format(const char* oid, int64_t oid_len, const int64_t* res, const int64_t* offsets, int64_t T,
+                     int64_t N, const double* local, const double* world, const double* values, int threads,
+                     gm_buffer** out);
+const char* gm_buffer_data(const gm_buffer* buf);
+int64_t gm_buffer_size(const gm_buffer* buf);
+void gm_buffer_free(gm_buffer* buf);
 
 #ifdef __cplusplus
 }

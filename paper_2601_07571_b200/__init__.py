@@ -11,6 +11,8 @@ from .errors import (ConfigError, GazemapError, GazeOutsideFrustumError, Invalid
                      ParseError)
 from .estimator import FixationDensityMapper
 from .fixlog import FixationLog, parse_fixation_log, parse_fixation_table
+from .io_export import (EXPORT_HEADER, ExportRecord, load_config, load_map, save_map, scene_layout_hash,
+                        write_export)
 from .gaze import (DEFAULT_THETA, SQRT_TWO_PI, Fixation, GazeCone, fixation_setup, fixation_table,
                    frustum_from_matrix, gaussian_weight, perspective_matrix)
 from .geometry import (Mesh, SampledMesh, Scene, SceneObject, Transform, TriangleSampling, adaptive_resolution,

@@ -66,6 +66,7 @@ SIGNATURES = {
     "gm_plan_destroy": (None, [_VP]),
     "gm_plan_set_host_threads": (ctypes.c_int, [_VP, ctypes.c_int]),
     "gm_plan_set_scene": (ctypes.c_int, [_VP, ctypes.c_int, _I64, _D, _D, _I64, _U8]),
+    "gm_plan_set_poses": (ctypes.c_int, [_VP, _D]),
     "gm_plan_num_samples": (ctypes.c_int64, [_VP]),
     "gm_plan_num_triangles": (ctypes.c_int64, [_VP]),
     "gm_plan_values_device": (ctypes.c_void_p, [_VP]),
@@ -91,6 +92,11 @@ SIGNATURES = {
     "gm_fixlog_copy": (ctypes.c_int, [_VP, _D, _I64, ctypes.c_void_p, _I64, _I64, _D]),
     "gm_fixlog_error": (ctypes.c_int, [_VP, _I64]),
     "gm_fixlog_free": (None, [_VP]),
+    "gm_export_format": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int64, _I64, _I64, ctypes.c_int64, ctypes.c_int64,
+                                        _D, _D, _D, ctypes.c_int, ctypes.POINTER(_VP)]),
+    "gm_buffer_data": (ctypes.c_void_p, [_VP]),
+    "gm_buffer_size": (ctypes.c_int64, [_VP]),
+    "gm_buffer_free": (None, [_VP]),
 }
 
 _lib = None

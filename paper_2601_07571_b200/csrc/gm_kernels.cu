@@ -1278,6 +1278,15 @@ struct gm_plan {
     int flush_gen = 0;
     void* d_scan_tmp = nullptr;
     size_t scan_tmp_bytes = 0;
+    // scene layout kept for pose changes (gm_plan_set_poses): local corners,
+    // sample offsets per triangle, per-object triangle/sample ranges
+    double* d_local = nullptr;
+    int64_t* d_res = nullptr;
+    int64_t* d_off = nullptr;
+    double* d_M = nullptr;  // [n_obj][12] current R diag(s) + t
+    int n_obj = 0;
+    std::vector<int64_t> tstart, nsamp;
+    std::vector<uint8_t> include;
 };
 
 static void plan_free_scene(gm_plan* p) {
@@ -1293,6 +1302,10 @@ static void plan_free_scene(gm_plan* p) {
     p->d_tw = nullptr; p->d_tsph = p->d_csph = p->d_chunk = p->d_super = nullptr;
     p->d_px = p->d_py = p->d_pz = p->d_values = nullptr;
     p->T = p->n_clu = p->N = p->n_chunks = p->n_supers = 0;
+    cudaFree(p->d_local); cudaFree(p->d_res); cudaFree(p->d_off); cudaFree(p->d_M);
+    p->d_local = nullptr; p->d_res = p->d_off = nullptr; p->d_M = nullptr;
+    p->n_obj = 0;
+    p->tstart.clear(); p->nsamp.clear(); p->include.clear();
 }
 
 extern "C" int gm_plan_create(int device, gm_plan** out) {
@@ -1359,6 +1372,8 @@ static void xform_matrix(const double* xf, double M[9], double t[3]) {
     for (int i = 0; i < 3; i++) t[i] = xf[i];
 }
 
+extern "C" int gm_plan_set_poses(gm_plan* p, const double* xforms);
+
 // Upload a scene: n_obj objects, tri_counts[o] triangles each, local triangle
 // corners tri_local (sum T x 9, object order), transforms xforms (n_obj x 10),
 // per-triangle resolutions res (sum T; the SampledMesh layouts), include flags.
@@ -1411,42 +1426,68 @@ extern "C" int gm_plan_set_scene(gm_plan* p, int n_obj, const int64_t* tri_count
         p->sort_tmp_bytes = tb + 16;
     }
     if ((rc = dev_alloc(&p->d_values, (size_t)N))) return rc;
+    p->n_obj = n_obj;
+    p->tstart = tstart;
+    p->nsamp = nsamp;
+    p->include.assign(include, include + n_obj);
     if (T == 0) return GM_OK;
-    double *d_local = nullptr, *d_M = nullptr;
-    int64_t *d_res = nullptr, *d_cnt = nullptr, *d_off = nullptr;
-    if ((rc = dev_alloc(&d_local, (size_t)T * 9))) return rc;
-    if ((rc = dev_alloc(&d_M, (size_t)n_obj * 12))) return rc;
-    if ((rc = dev_alloc(&d_res, (size_t)T))) return rc;
+    int64_t* d_cnt = nullptr;
+    if ((rc = dev_alloc(&p->d_local, (size_t)T * 9))) return rc;
+    if ((rc = dev_alloc(&p->d_M, (size_t)n_obj * 12))) return rc;
+    if ((rc = dev_alloc(&p->d_res, (size_t)T))) return rc;
     if ((rc = dev_alloc(&d_cnt, (size_t)T))) return rc;
-    if ((rc = dev_alloc(&d_off, (size_t)T))) return rc;
-    std::vector<double> Mt(n_obj * 12);
-    for (int o = 0; o < n_obj; o++) xform_matrix(xforms + 10 * o, &Mt[12 * o], &Mt[12 * o + 9]);
+    if ((rc = dev_alloc(&p->d_off, (size_t)T))) return rc;
     cudaStream_t s = p->stream;
-    CK(cudaMemcpyAsync(d_local, tri_local, sizeof(double) * 9 * T, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(d_M, Mt.data(), sizeof(double) * 12 * n_obj, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(d_res, res, sizeof(int64_t) * T, cudaMemcpyHostToDevice, s));
-    int64_t sample_base = 0;
+    CK(cudaMemcpyAsync(p->d_local, tri_local, sizeof(double) * 9 * T, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(p->d_res, res, sizeof(int64_t) * T, cudaMemcpyHostToDevice, s));
     for (int o = 0; o < n_obj; o++) {
         int64_t To = tri_counts[o];
-        if (To == 0) continue;
-        const double* loc = d_local + 9 * tstart[o];
-        k_world_tris<<<blocks_for(3 * To, 256), 256, 0, s>>>(loc, To, d_M + 12 * o, d_M + 12 * o + 9,
-                                                              p->d_tw + 9 * tstart[o]);
-        if (!include[o] || nsamp[o] == 0) continue;
-        k_layout<<<blocks_for(To, 256), 256, 0, s>>>(loc, To, 0.0, d_res + tstart[o], nullptr,
+        if (To == 0 || !include[o] || nsamp[o] == 0) continue;
+        const double* loc = p->d_local + 9 * tstart[o];
+        k_layout<<<blocks_for(To, 256), 256, 0, s>>>(loc, To, 0.0, p->d_res + tstart[o], nullptr,
                                                        d_cnt + tstart[o]);
         size_t tmp = 0;
-        cub::DeviceScan::ExclusiveSum(nullptr, tmp, d_cnt + tstart[o], d_off + tstart[o], To, s);
+        cub::DeviceScan::ExclusiveSum(nullptr, tmp, d_cnt + tstart[o], p->d_off + tstart[o], To, s);
         if (tmp > p->scan_tmp_bytes) {
             cudaFree(p->d_scan_tmp);
             p->d_scan_tmp = nullptr;
             CK(cudaMalloc(&p->d_scan_tmp, tmp));
             p->scan_tmp_bytes = tmp;
         }
-        CK(cub::DeviceScan::ExclusiveSum(p->d_scan_tmp, tmp, d_cnt + tstart[o], d_off + tstart[o], To, s));
-        int64_t No = nsamp[o];
-        k_positions<<<blocks_for(No, 256), 256, 0, s>>>(loc, To, d_res + tstart[o], d_off + tstart[o], No,
-                                                          d_M + 12 * o, d_M + 12 * o + 9, nullptr,
+        CK(cub::DeviceScan::ExclusiveSum(p->d_scan_tmp, tmp, d_cnt + tstart[o], p->d_off + tstart[o], To, s));
+    }
+    CK(cudaStreamSynchronize(s));
+    cudaFree(d_cnt);
+    return gm_plan_set_poses(p, xforms);
+}
+
+// Object poses (n_obj x [t(3), q xyzw(4), s(3)]) of a plan whose layout is
+// set: world occluder triangles (scene_world_triangles, raster.py:68-78) and
+// world sample positions (_SampleCache.world, density.py:121-127: override
+// .apply(local)), both with the OpenBLAS FMA chain, then every derived
+// structure (float32 copies, bounding spheres).  generate() calls it between
+// runs of fixations that share the same pose overrides (dynamic scenes).
+extern "C" int gm_plan_set_poses(gm_plan* p, const double* xforms) {
+    if (!p || (p->n_obj > 0 && !xforms)) return set_err(GM_ERR_ARG, "bad plan/poses");
+    CK(cudaSetDevice(p->device));
+    const int64_t T = p->T, N = p->N;
+    const int n_obj = p->n_obj;
+    if (T == 0) return GM_OK;
+    cudaStream_t s = p->stream;
+    std::vector<double> Mt(n_obj * 12);
+    for (int o = 0; o < n_obj; o++) xform_matrix(xforms + 10 * o, &Mt[12 * o], &Mt[12 * o + 9]);
+    CK(cudaMemcpyAsync(p->d_M, Mt.data(), sizeof(double) * 12 * n_obj, cudaMemcpyHostToDevice, s));
+    int64_t sample_base = 0;
+    for (int o = 0; o < n_obj; o++) {
+        const int64_t To = p->tstart[o + 1] - p->tstart[o];
+        if (To == 0) continue;
+        const double* loc = p->d_local + 9 * p->tstart[o];
+        k_world_tris<<<blocks_for(3 * To, 256), 256, 0, s>>>(loc, To, p->d_M + 12 * o, p->d_M + 12 * o + 9,
+                                                              p->d_tw + 9 * p->tstart[o]);
+        if (!p->include[o] || p->nsamp[o] == 0) continue;
+        const int64_t No = p->nsamp[o];
+        k_positions<<<blocks_for(No, 256), 256, 0, s>>>(loc, To, p->d_res + p->tstart[o], p->d_off + p->tstart[o],
+                                                          No, p->d_M + 12 * o, p->d_M + 12 * o + 9, nullptr,
                                                           p->d_px + sample_base, p->d_py + sample_base,
                                                           p->d_pz + sample_base);
         sample_base += No;
@@ -1471,7 +1512,6 @@ extern "C" int gm_plan_set_scene(gm_plan* p, int n_obj, const int64_t* tri_count
     }
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(s));
-    cudaFree(d_local); cudaFree(d_M); cudaFree(d_res); cudaFree(d_cnt); cudaFree(d_off);
     return GM_OK;
 }
 

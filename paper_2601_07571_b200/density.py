@@ -144,6 +144,9 @@ class ScenePlan:
         tc, tl, xf, rs, fl = self._keep
         _native.check(lib.gm_plan_set_scene(h, len(objs), _native.iptr(tc), _native.dptr(tl), _native.dptr(xf),
                                             _native.iptr(rs), _native.u8ptr(fl)), "gm_plan_set_scene")
+        self._base_poses = xf.copy()
+        self._obj_index = {o.object_id: i for i, o in enumerate(objs)}
+        self._pose_key = ()
         n = int(lib.gm_plan_num_samples(h))
         if n != self.n_samples:
             raise RuntimeError(f"plan sample count {n} != layout total {self.n_samples}")
@@ -187,6 +190,56 @@ class ScenePlan:
             timers.add("rasterize", (tm.rasterize_ms + tm.texel_ms) / 1e3)
             timers.add("accumulate", (tm.mark_ms + tm.accumulate_ms) / 1e3)
             timers.add("setup", tm.setup_ms / 1e3)
+
+    def set_overrides(self, overrides: dict | None) -> None:
+        """Pose the scene for one fixation's overrides (object_id -> Transform;
+        ids not in the scene are ignored, like _SampleCache.world and
+        scene_world_triangles, reference density.py:121-127, raster.py:68-78);
+        None/{} restores the base poses."""
+        key = _pose_key(overrides, self._obj_index)
+        if key == self._pose_key:
+            return
+        xf = self._base_poses.copy()
+        for oid, t in (overrides or {}).items():
+            i = self._obj_index.get(oid)
+            if i is not None:
+                xf[i] = _packed(t)
+        _native.check(self._lib.gm_plan_set_poses(self._h, _native.dptr(np.ascontiguousarray(xf))),
+                      "gm_plan_set_poses")
+        self._pose_key = key
+
+    def accumulate_log(self, fixations, config: GenerationConfig, reset: bool = True, progress=None,
+                       timers: Timings | None = None, batch: int = 0) -> None:
+        """accumulate() over a log that may carry pose overrides (dynamic
+        scenes, reference density.py:123-127,161-165): the log is cut into
+        runs of consecutive fixations with the same effective override set;
+        each run is accumulated with the scene posed for it, in log order."""
+        table = fixation_table(fixations)
+        ovs = _override_list(fixations)
+        if ovs is None:
+            self.set_overrides(None)
+            self.accumulate(table, config, reset=reset, progress=progress, timers=timers, batch=batch)
+            return
+        F = len(table)
+        keys = [_pose_key(o, self._obj_index) for o in ovs]
+        try:
+            a = 0
+            first = True
+            while a < F:
+                b = a + 1
+                while b < F and keys[b] == keys[a]:
+                    b += 1
+                self.set_overrides(ovs[a])
+                cb = None
+                if progress is not None:
+                    cb = (lambda off: (lambda i, _t: progress(off + i, F)))(a)
+                self.accumulate(table[a:b], config, reset=reset and first, progress=cb, timers=timers, batch=batch)
+                first = False
+                a = b
+            if first and reset:
+                self.accumulate(table[:0], config, reset=True)
+        finally:
+            self.set_overrides(None)
 
     def global_max(self) -> float:
         out = np.zeros(1)
@@ -282,14 +335,26 @@ def get_plan(scene, sampled_meshes: dict, config: GenerationConfig, device: int 
     return plan
 
 
-def _reject_overrides(fixations) -> None:
+def _packed(t) -> np.ndarray:
+    return np.concatenate([np.asarray(t.translation, np.float64).reshape(3), np.asarray(t.rotation, np.float64).reshape(4),
+                           np.asarray(t.scale, np.float64).reshape(3)])
+
+
+def _pose_key(overrides, index: dict) -> tuple:
+    """Hashable identity of the poses an override dict imposes on the scene."""
+    if not overrides:
+        return ()
+    return tuple(sorted((oid, _packed(t).tobytes()) for oid, t in overrides.items() if oid in index))
+
+
+def _override_list(fixations):
+    """Per-fixation override dicts, or None when the log has none at all."""
     if isinstance(fixations, np.ndarray):
-        return
-    for f in fixations:
-        if getattr(f, "overrides", None):
-            raise NotImplementedError(
-                "per-fixation pose overrides (dynamic scenes) are not supported by the B200 path yet; "
-                "there is no CPU fallback")
+        return None
+    if getattr(fixations, "n_override_groups", None) == 0:  # FixationLog knows it parsed none
+        return None
+    ovs = [getattr(f, "overrides", None) or None for f in fixations]
+    return ovs if any(o for o in ovs) else None
 
 
 def generate(scene, sampled_meshes: dict, fixations, config: GenerationConfig, workers: int | None = None,
@@ -297,15 +362,14 @@ def generate(scene, sampled_meshes: dict, fixations, config: GenerationConfig, w
     """All fixations, in log order, into a fresh un-normalized map.
 
     `fixations` is a list of Fixation objects (this package's or the
-    reference's) or an (F, 18) table in fixation-log column order.  `workers`
+    reference's; pose overrides honoured) or an (F, 18) table in
+    fixation-log column order.  `workers`
     is accepted for API compatibility; the GPU result does not depend on it.
     """
     config.validate()
-    _reject_overrides(fixations)
     plan = get_plan(scene, sampled_meshes, config, device)
-    table = fixation_table(fixations)
-    plan.accumulate(table, config, reset=True, progress=progress, timers=timers, batch=batch)
-    gmax = plan.global_max() if len(table) else 0.0
+    plan.accumulate_log(fixations, config, reset=True, progress=progress, timers=timers, batch=batch)
+    gmax = plan.global_max() if len(fixations) else 0.0
     values = plan.split(plan.read(), sampled_meshes)
     return DensityMap(values, global_max=gmax, normalized=False)
 
@@ -313,10 +377,9 @@ def generate(scene, sampled_meshes: dict, fixations, config: GenerationConfig, w
 def accumulate_fixation(dmap: DensityMap, scene, sampled_meshes: dict, fixation, config: GenerationConfig,
                         cache=None, timers: Timings | None = None, device: int = 0) -> DensityMap:
     """Add one fixation to `dmap` in place (running max updated), return it."""
-    _reject_overrides([fixation])
     plan = cache if isinstance(cache, ScenePlan) else get_plan(scene, sampled_meshes, config, device)
     plan.write(plan.gather(dmap.values))
-    plan.accumulate([fixation], config, reset=False, timers=timers)
+    plan.accumulate_log([fixation], config, reset=False, timers=timers)
     flat = plan.read()
     running = dmap.global_max
     for oid, (a, b) in plan.slices.items():

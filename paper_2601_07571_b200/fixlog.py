@@ -213,4 +213,5 @@ def parse_fixation_log(path, time_window=None, threads: int = 0) -> FixationLog:
             log.append(f)
     log.table = table
     log.line = line
+    log.n_override_groups = sum(len(o) for o in overrides if o)
     return log

@@ -36,13 +36,13 @@ class _CudaArray:
         self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (ptr, False), "version": 3}
 
 
-def _gpu_partial(scene, sampled_meshes, table, config, device):
-    """Accumulate on this rank's GPU; return (torch tensor aliasing the plan's
-    device values, plan)."""
+def _gpu_partial(scene, sampled_meshes, shard, config, device):
+    """Accumulate on this rank's GPU (pose overrides honoured); return (torch
+    tensor aliasing the plan's device values, plan)."""
     import torch
 
     plan = get_plan(scene, sampled_meshes, config, device)
-    plan.accumulate(table, config, reset=True)
+    plan.accumulate_log(shard, config, reset=True)
     plan.sync()
     t = torch.as_tensor(_CudaArray(plan.values_device_ptr(), plan.n_samples), device=f"cuda:{device}")
     return t, plan
@@ -68,7 +68,8 @@ def generate_sharded(scene, sampled_meshes: dict, fixations, config: GenerationC
     shard = table[a:b]
     if local_compute is None:
         dev = torch.cuda.current_device() if device is None else device
-        vals, plan = _gpu_partial(scene, sampled_meshes, shard, config, dev)
+        objs = shard if isinstance(fixations, np.ndarray) else list(fixations)[a:b]
+        vals, plan = _gpu_partial(scene, sampled_meshes, objs, config, dev)
         if world > 1:
             dist.all_reduce(vals, op=dist.ReduceOp.SUM, group=group)
         torch.cuda.synchronize(dev)

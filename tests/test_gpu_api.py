@@ -220,14 +220,6 @@ def test_normalize_and_estimator():
         gm.FixationDensityMapper().fit(X)
 
 
-def test_overrides_rejected_loudly():
-    scene = quad_scene()
-    f = gm.Fixation(0.0, 1.0, [0, 0, 0], [0, 0, 0, 1], W.FRUSTUM, [0, 0, -1],
-                    overrides={"q": gm.Transform([0, 0, 0], [0, 0, 0, 1], [1, 1, 1])})
-    with pytest.raises(NotImplementedError):
-        run(scene, [f], k=1000.0)
-
-
 def test_reference_dataclasses_accepted():
     """Duck typing: objects shaped like the reference's dataclasses."""
 
