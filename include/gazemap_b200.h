@@ -28,7 +28,8 @@ enum {
     GM_ERR_INVALID_FRUSTUM = 3,  /* perspective_matrix bounds -> InvalidFrustumError (gaze.py:325-328) */
     GM_ERR_NO_DEVICE = 4,        /* no CUDA device: there is no CPU fallback */
     GM_ERR_OOM = 5,
-    GM_ERR_UNSUPPORTED = 6
+    GM_ERR_UNSUPPORTED = 6,
+    GM_ERR_GAZE_OUTSIDE = 7      /* 4-sigma cone misses the near plane -> GazeOutsideFrustumError */
 };
 
 /* Fixation table: F rows x 18 float64 in the fixation-log column order
@@ -95,6 +96,14 @@ int gm_normalize(int device, const double* values, int64_t n, double gmax, doubl
  * csrc/gm_types.h), cull: F x 20 float32 or NULL. */
 int gm_fixation_setup(const double* fixations, int64_t F, double theta, int filtering, int res, double* ex,
                       void* cull, int64_t* bad_fixation);
+
+/* ellipse_intersection(gaze_dir, n, cone) (gaze.py:252-309) for the cone's
+ * 4-sigma half-angle phi: out[18] = center_E[3], major_a, minor_b,
+ * inclination_alpha, A0[3], A1[3], B0[3], B1[3]; GM_ERR_GAZE_OUTSIDE when
+ * the cone does not cut the near plane in an ellipse. */
+int gm_ellipse_intersection(const double* gaze, double n, double phi, double* out);
+/* crop_bounds (gaze.py:312-320): (l', r', b', t') of an out[18] above. */
+int gm_crop_bounds(const double* ellipse, double* lrbt);
 
 /* ---- scene plan: occluders + samples resident on one GPU ---------------- */
 
@@ -165,6 +174,38 @@ int gm_plan_candidates(gm_plan* plan, const double* fixations, int64_t F, double
 
 /* World sample positions of the plan (N x 3), _SampleCache.base_world. */
 int gm_plan_positions(gm_plan* plan, double* out);
+
+/* ---- general camera: z-buffer, attributes, heatmap (kernel seam + 8f-2) --- */
+
+/* kernels.rasterize (kernels.py:140-192) of world triangles (T x 3 x 3, the
+ * order is the rasterization order) for one camera: rot 3x3 row-major and
+ * trans 3 (world -> camera), the projection's p00 p11 p02 p12, a W x H buffer,
+ * near/far.  depth (H x W, +inf where nothing is drawn) always; with_attrs
+ * outputs when non-NULL: tri_id (H x W, -1 where empty) and the
+ * perspective-correct barycentrics bary (H x W x 3) of the winning triangle
+ * (the first in order among equal minimum depths).  Used by
+ * raster.rasterize_triangles / rasterize_depth (raster.py:99-137). */
+int gm_rasterize(int device, const double* tris, int64_t T, const double* rot, const double* trans, double p00,
+                 double p11, double p02, double p12, int W, int H, double near_, double far_, double* depth,
+                 int32_t* tri_id, double* bary);
+
+/* render_heatmap (render.py:95-186) after the camera setup: rasterize every
+ * triangle with attributes, interpolate the density over each triangle's
+ * sample grid (res: per-triangle resolution, base: the triangle's first
+ * sample in `values`), colormap (n_stops <= 16 stops, colors n_stops x 3,
+ * gamma) and round to uint8; img is H x W x 3 (background black). */
+int gm_render_heatmap(int device, const double* tris, int64_t T, const double* rot, const double* trans, double p00,
+                      double p11, double p02, double p12, int W, int H, double near_, double far_,
+                      const int64_t* res, const int64_t* base, const double* values, int64_t N, const double* stops,
+                      const double* colors, int n_stops, double gamma, uint8_t* img);
+
+/* kernels.cull_mask (kernels.py:195-216) on the GPU: keep[t] = 0 iff all
+ * three vertices of triangle t are outside one of the n_planes planes. */
+int gm_cull_mask(int device, const double* tris, int64_t T, const double* planes, int n_planes, uint8_t* keep);
+
+/* kernels.depth_match (kernels.py:219-285) on a host H x W buffer (host
+ * scalar query, raster.is_visible). */
+int gm_depth_match(const double* depth, int64_t height, int64_t width, double fx, double fy, double d, double eps);
 
 /* ---- fixation-log ingestion ----------------------------- */
 

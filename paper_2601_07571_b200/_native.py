@@ -13,11 +13,12 @@ from pathlib import Path
 
 import numpy as np
 
-from .errors import ConfigError, GazemapError, InvalidFrustumError
+from .errors import ConfigError, GazemapError, GazeOutsideFrustumError, InvalidFrustumError
 
 SO_PATH = Path(__file__).resolve().parent / "_gazemap_b200.so"
 
-GM_OK, GM_ERR_CUDA, GM_ERR_ARG, GM_ERR_INVALID_FRUSTUM, GM_ERR_NO_DEVICE, GM_ERR_OOM, GM_ERR_UNSUPPORTED = range(7)
+(GM_OK, GM_ERR_CUDA, GM_ERR_ARG, GM_ERR_INVALID_FRUSTUM, GM_ERR_NO_DEVICE, GM_ERR_OOM, GM_ERR_UNSUPPORTED,
+ GM_ERR_GAZE_OUTSIDE) = range(8)
 
 _D = ctypes.POINTER(ctypes.c_double)
 _I64 = ctypes.POINTER(ctypes.c_int64)
@@ -86,6 +87,18 @@ SIGNATURES = {
     "gm_plan_candidates": (ctypes.c_int, [_VP, _D, ctypes.c_int64, ctypes.c_double, ctypes.c_int, ctypes.c_int,
                                           _I64, ctypes.c_int64, _I64]),
     "gm_plan_positions": (ctypes.c_int, [_VP, _D]),
+    "gm_rasterize": (ctypes.c_int, [ctypes.c_int, _D, ctypes.c_int64, _D, _D, ctypes.c_double, ctypes.c_double,
+                                    ctypes.c_double, ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                    ctypes.c_double, _D, ctypes.c_void_p, _D]),
+    "gm_render_heatmap": (ctypes.c_int, [ctypes.c_int, _D, ctypes.c_int64, _D, _D, ctypes.c_double, ctypes.c_double,
+                                         ctypes.c_double, ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                         ctypes.c_double, _I64, _I64, _D, ctypes.c_int64, _D, _D, ctypes.c_int,
+                                         ctypes.c_double, ctypes.c_void_p]),
+    "gm_cull_mask": (ctypes.c_int, [ctypes.c_int, _D, ctypes.c_int64, _D, ctypes.c_int, ctypes.c_void_p]),
+    "gm_depth_match": (ctypes.c_int, [_D, ctypes.c_int64, ctypes.c_int64, ctypes.c_double, ctypes.c_double,
+                                      ctypes.c_double, ctypes.c_double]),
+    "gm_ellipse_intersection": (ctypes.c_int, [_D, ctypes.c_double, ctypes.c_double, _D]),
+    "gm_crop_bounds": (ctypes.c_int, [_D, _D]),
     "gm_fixlog_parse": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int64, ctypes.c_int, ctypes.POINTER(_VP)]),
     "gm_fixlog_rows": (ctypes.c_int64, [_VP]),
     "gm_fixlog_groups": (ctypes.c_int64, [_VP]),
@@ -147,6 +160,8 @@ def check(rc: int, what: str = "") -> None:
         msg = f"{what}: {msg}"
     if rc == GM_ERR_INVALID_FRUSTUM:
         raise InvalidFrustumError(msg)
+    if rc == GM_ERR_GAZE_OUTSIDE:
+        raise GazeOutsideFrustumError(msg)
     if rc == GM_ERR_NO_DEVICE:
         raise NativeUnavailableError(msg)
     if rc == GM_ERR_ARG:

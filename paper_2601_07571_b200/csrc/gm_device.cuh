@@ -151,6 +151,7 @@ __device__ __forceinline__ int project_triangle(const double* tw, const GmFixExa
             iw[m] = 1.0 / w;
         }
         if (ok && make_screen_tri(sx, sy, iw, W, H, &out[n_out])) {
+            out[n_out].tl |= (uint32_t)k << 3;  // fan index; the caller adds 2 t (rasterization order key)
             // depth written at any covered pixel = 1 / (convex combination of 1/w) >= min w
             // (up to a few ulps, far inside the 1e-9 margin k_texels applies)
             const double w0 = -vout[0][2], w1 = -vout[k + 1][2], w2 = -vout[k + 2][2];

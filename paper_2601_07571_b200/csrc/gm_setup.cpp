@@ -65,8 +65,11 @@ inline bool near_hit(const V3& d, double n, V3* out) {
     return true;
 }
 
-// gaze.py:252-320; false == GazeOutsideFrustumError (caller falls back)
-bool crop_box(const double* gaze, double n, const GmSetupConsts& c, double lrbt[4]) {
+// gaze.py:252-309 ellipse_intersection: 0, or the GazeOutsideFrustumError
+// raised (1: a rotated ray misses the near plane, gaze.py:244-247; 2: no
+// ellipse, :285-286).  out (EllipseParams): center_E[3], major_a, minor_b,
+// inclination_alpha, A0[3], A1[3], B0[3], B1[3].
+int ellipse(const double* gaze, double n, const GmSetupConsts& c, double out[18]) {
     V3 g{gaze[0], gaze[1], gaze[2]};
     V3 r = divided(g, np_norm(g));
     V3 u1 = np_cross(r, V3{0.0, 0.0, -1.0});
@@ -81,14 +84,13 @@ bool crop_box(const double* gaze, double n, const GmSetupConsts& c, double lrbt[
     V3 E, A0, A1, B0, B1;
     if (!near_hit(r, n, &E) || !near_hit(a0, n, &A0) || !near_hit(a1, n, &A1) || !near_hit(b0, n, &B0) ||
         !near_hit(b1, n, &B1))
-        return false;
+        return 1;
     V3 dA{A1.x - A0.x, A1.y - A0.y, A1.z - A0.z};
     double a = 0.5 * np_norm(dA);
     double cos_beta = -r.z;
     double disc = std::pow(c.cos_phi, 2.0) - (1.0 - cos_beta * cos_beta);
-    if (disc <= 0.0) return false;
+    if (disc <= 0.0) return 2;
     double b = n * c.sin_phi / std::sqrt(disc);
-    double cx = 0.5 * (A0.x + A1.x), cy = 0.5 * (A0.y + A1.y);
     V3 me{E.x - 0.0, E.y - 0.0, E.z - (-n)};
     double me_norm = np_norm(me);
     double alpha = 0.0;
@@ -98,15 +100,38 @@ bool crop_box(const double* gaze, double n, const GmSetupConsts& c, double lrbt[
         x = std::fmax(-1.0, std::fmin(1.0, x));
         alpha = std::acos(x);
     }
-    double major = a > b ? a : b, minor = a < b ? a : b;
-    double a2 = std::pow(major, 2.0), b2 = std::pow(minor, 2.0);
-    double ca2 = std::pow(std::cos(alpha), 2.0), sa2 = std::pow(std::sin(alpha), 2.0);
+    out[0] = 0.5 * (A0.x + A1.x);
+    out[1] = 0.5 * (A0.y + A1.y);
+    out[2] = 0.5 * (A0.z + A1.z);
+    out[3] = a > b ? a : b;  // max(a, b)
+    out[4] = a < b ? a : b;  // min(a, b)
+    out[5] = alpha;
+    const V3 pts[4] = {A0, A1, B0, B1};
+    for (int k = 0; k < 4; k++) {
+        out[6 + 3 * k] = pts[k].x;
+        out[7 + 3 * k] = pts[k].y;
+        out[8 + 3 * k] = pts[k].z;
+    }
+    return 0;
+}
+
+// gaze.py:312-320 crop_bounds: (l', r', b', t') of an EllipseParams
+void bounds(const double e[18], double lrbt[4]) {
+    double a2 = std::pow(e[3], 2.0), b2 = std::pow(e[4], 2.0);
+    double ca2 = std::pow(std::cos(e[5]), 2.0), sa2 = std::pow(std::sin(e[5]), 2.0);
     double dx = std::sqrt(a2 * ca2 + b2 * sa2);
     double dy = std::sqrt(a2 * sa2 + b2 * ca2);
-    lrbt[0] = cx - dx;
-    lrbt[1] = cx + dx;
-    lrbt[2] = cy - dy;
-    lrbt[3] = cy + dy;
+    lrbt[0] = e[0] - dx;
+    lrbt[1] = e[0] + dx;
+    lrbt[2] = e[1] - dy;
+    lrbt[3] = e[1] + dy;
+}
+
+// gaze.py:372-381 without the projection; false == GazeOutsideFrustumError
+bool crop_box(const double* gaze, double n, const GmSetupConsts& c, double lrbt[4]) {
+    double e[18];
+    if (ellipse(gaze, n, c, e)) return false;
+    bounds(e, lrbt);
     return true;
 }
 
@@ -244,4 +269,40 @@ extern "C" int64_t gm_setup_batch(const double* fx, int64_t F, const GmSetupCons
         cull[i] = k;
     }
     return bad == INT64_MAX ? -1 : bad;
+}
+
+// ---- the crop-frustum steps as C-ABI entry points (Python API: gaze.py) ----
+
+static void phi_consts(double phi, GmSetupConsts* c) {
+    std::memset(c, 0, sizeof(*c));
+    c->phi = phi;
+    double hp = 0.5 * phi, hm = 0.5 * -phi;
+    c->cos_hp = std::cos(hp);
+    c->sin_hp = std::sin(hp);
+    c->cos_hm = std::cos(hm);
+    c->sin_hm = std::sin(hm);
+    c->cos_phi = std::cos(phi);
+    c->sin_phi = std::sin(phi);
+}
+
+// ellipse_intersection(gaze_dir, n, cone) (gaze.py:252-309) for a cone of
+// 4-sigma half-angle phi: out[18] as in ellipse(); GM_ERR_GAZE_OUTSIDE with
+// out[0] = 1 or 2 (which GazeOutsideFrustumError) when there is no ellipse.
+extern "C" int gm_ellipse_intersection(const double* gaze, double n, double phi, double* out) {
+    if (!gaze || !out) return GM_ERR_ARG;
+    GmSetupConsts c;
+    phi_consts(phi, &c);
+    const int why = ellipse(gaze, n, c, out);
+    if (why) {
+        out[0] = (double)why;
+        return GM_ERR_GAZE_OUTSIDE;
+    }
+    return GM_OK;
+}
+
+// crop_bounds(e) (gaze.py:312-320) of an 18-double EllipseParams.
+extern "C" int gm_crop_bounds(const double* e, double* lrbt) {
+    if (!e || !lrbt) return GM_ERR_ARG;
+    bounds(e, lrbt);
+    return GM_OK;
 }

@@ -40,7 +40,8 @@ struct __attribute__((aligned(16))) GmScreenTri {
     double sx0, sy0, sx1, sy1, sx2, sy2;
     double iw0, iw1, iw2, inv_area;
     uint16_t x0, x1, y0, y1;  // inclusive pixel bbox clamped to the buffer
-    uint32_t tl;              // top-left ownership bits for edges 0, 1, 2
+    uint32_t tl;              // bits 0-2: top-left ownership of edges 0, 1, 2; bits 3+: order key
+                              // 2 t + fan (t < 2^28), the rasterization order of kernels.py:158-192
     float minw;               // min vertex depth, rounded down (a lower bound of every depth it writes)
 };  // 96 B
 
@@ -98,4 +99,5 @@ enum {
     GM_ERR_NO_DEVICE = 4,
     GM_ERR_OOM = 5,
     GM_ERR_UNSUPPORTED = 6,
+    GM_ERR_GAZE_OUTSIDE = 7,
 };

@@ -16,10 +16,11 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _native
-from .errors import InvalidFrustumError
+from .errors import GazeOutsideFrustumError, InvalidFrustumError
 
-__all__ = ["GazeCone", "Fixation", "DEFAULT_THETA", "SQRT_TWO_PI", "fixation_table", "fixation_setup",
-           "perspective_matrix", "frustum_from_matrix", "gaussian_weight"]
+__all__ = ["GazeCone", "Fixation", "EllipseParams", "CropFrustum", "DEFAULT_THETA", "SQRT_TWO_PI", "fixation_table",
+           "fixation_setup", "perspective_matrix", "frustum_from_matrix", "gaussian_weight", "ellipse_intersection",
+           "crop_bounds", "crop_projection_matrix", "build_crop_frustum"]
 
 SQRT_TWO_PI = math.sqrt(2.0 * math.pi)
 DEFAULT_THETA = math.radians(1.0)
@@ -179,6 +180,80 @@ def gaussian_weight(p, gaze_dir, duration_t: float, cone: GazeCone) -> float:
     if ratio > 4.0:
         return 0.0
     return duration_t / (cone.sigma * SQRT_TWO_PI) * math.exp(-0.5 * ratio * ratio)
+
+
+# ------------------------------------------------ 4-sigma cone crop frustum
+
+@dataclass(frozen=True)
+class EllipseParams:
+    """The 4-sigma cone's ellipse on the near plane z = -n (ref gaze.py:218-229)."""
+
+    center_E: np.ndarray
+    major_a: float
+    minor_b: float
+    inclination_alpha: float
+    A0: np.ndarray
+    A1: np.ndarray
+    B0: np.ndarray
+    B1: np.ndarray
+
+    def packed(self) -> np.ndarray:
+        return np.concatenate([self.center_E, [self.major_a, self.minor_b, self.inclination_alpha], self.A0,
+                               self.A1, self.B0, self.B1]).astype(np.float64)
+
+
+_GAZE_OUTSIDE = {1: "gaze cone ray does not reach the near clip plane (z >= 0)",
+                 2: "gaze cone does not cut the near plane in an ellipse"}
+
+
+def ellipse_intersection(gaze_dir, n: float, cone: GazeCone) -> EllipseParams:
+    """Near-plane ellipse of the 4-sigma cone (ref gaze.py:252-309), computed
+    by the same host code (csrc/gm_setup.cpp) the generation setup uses:
+    bit-identical to the reference (glibc trig, OpenBLAS FMA-chain norms).
+    Raises GazeOutsideFrustumError like the reference."""
+    g = np.ascontiguousarray(np.asarray(gaze_dir, dtype=np.float64).reshape(3))
+    out = np.zeros(18)
+    rc = _native.load().gm_ellipse_intersection(_native.dptr(g), float(n), float(cone.phi), _native.dptr(out))
+    if rc == _native.GM_ERR_GAZE_OUTSIDE:
+        raise GazeOutsideFrustumError(_GAZE_OUTSIDE[int(out[0])])
+    _native.check(rc, "gm_ellipse_intersection")
+    return EllipseParams(out[0:3].copy(), float(out[3]), float(out[4]), float(out[5]), out[6:9].copy(),
+                         out[9:12].copy(), out[12:15].copy(), out[15:18].copy())
+
+
+def crop_bounds(e: EllipseParams) -> tuple:
+    """(l', r', b', t') bounding box of the near-plane ellipse (ref gaze.py:312-320)."""
+    lrbt = np.zeros(4)
+    _native.check(_native.load().gm_crop_bounds(_native.dptr(e.packed()), _native.dptr(lrbt)), "gm_crop_bounds")
+    return float(lrbt[0]), float(lrbt[1]), float(lrbt[2]), float(lrbt[3])
+
+
+def crop_projection_matrix(bounds, n: float, f: float) -> np.ndarray:
+    """Perspective matrix of the sub-frustum bounded by the ellipse box (ref gaze.py:339-342)."""
+    l, r, b, t = bounds
+    return perspective_matrix(l, r, b, t, n, f)
+
+
+@dataclass(frozen=True)
+class CropFrustum:
+    """4-sigma-cone-fitted sub-frustum and its projection (ref gaze.py:359-369)."""
+
+    left: float
+    right: float
+    bottom: float
+    top: float
+    near: float
+    far: float
+    projection_matrix: np.ndarray
+
+
+def build_crop_frustum(fixation, cone: GazeCone) -> CropFrustum:
+    """Crop frustum of a fixation's 4-sigma cone (ref gaze.py:372-381); raises
+    GazeOutsideFrustumError when the cone does not fully face the near plane."""
+    n, f = fixation.frustum[4], fixation.frustum[5]
+    e = ellipse_intersection(fixation.gaze_dir, n, cone)
+    l, r, b, t = crop_bounds(e)
+    return CropFrustum(l, r, b, t, n, f, crop_projection_matrix((l, r, b, t), n, f))
 
 
 # GmFixExact field offsets (float64 units, 26 per record), csrc/gm_types.h
