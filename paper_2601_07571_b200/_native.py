@@ -49,7 +49,8 @@ FIX_CULL_FLOATS = 20
 
 GM_FLAG_STATS = 1
 STAT_NAMES = ["l1_tests", "l2_tests", "exact_evals", "ndc_candidates", "cone_candidates", "visible",
-              "texels", "texel_pairs", "covered_pairs"]
+              "texels", "texel_pairs", "covered_pairs", "reserved9", "tx_tiles", "tx_staged", "tx_list", "tx_iter",
+              "tx_edge"]
 
 PROGRESS_FN = ctypes.CFUNCTYPE(None, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p)
 

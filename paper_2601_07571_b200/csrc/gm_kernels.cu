@@ -458,6 +458,11 @@ enum {
     GM_STAT_TEXELS = 6,      // marked texels evaluated
     GM_STAT_PAIRS = 7,       // (texel, screen triangle) exact evaluations
     GM_STAT_COVERED = 8,     // pairs where the triangle covers the texel
+    GM_STAT_TX_TILES = 10,   // k_texels work items with marked texels
+    GM_STAT_TX_STAGED = 11,  // triangles staged per item (sum)
+    GM_STAT_TX_LIST = 12,    // coarse-bin list entries scanned per item (sum)
+    GM_STAT_TX_ITER = 13,    // warp iterations of the selection walk
+    GM_STAT_TX_EDGE = 14,    // lane x triangle edge-function evaluations in the walk
     GM_STAT_N = 16
 };
 #define GM_FLAG_STATS 1
@@ -897,7 +902,7 @@ __device__ __forceinline__ int kth_set_bit(uint32_t w, int k) {
 //      reference's float64 pixel arithmetic (texel_depth, float64 record read
 //      from L1/L2) and the minimum is stored -- the value kernels.rasterize
 //      leaves in that pixel.
-template <bool ATTRS>
+template <bool ATTRS, bool STATS>
 __global__ void __launch_bounds__(TW_WARPS * 32) k_texels(TriStore ts, DepthView dv, CoarseBins cb, int tiles_x,
                                                           int tiles_per_fix, int64_t n_items,
                                                           const GmFixExact* __restrict__ fixes, long long b0) {
@@ -942,7 +947,7 @@ __global__ void __launch_bounds__(TW_WARPS * 32) k_texels(TriStore ts, DepthView
         n = off[bb + 1] - off[bb];
     }
     const int xe = xb + TW - 1, ye = yb + TH - 1;
-    unsigned long long c_pairs = 0, c_cov = 0;
+    unsigned long long c_pairs = 0, c_cov = 0, c_iter = 0, c_edge = 0;
 
     // 1. triangles overlapping the tile -> S.sel (scan cursor resumes if > TW_SEL)
     auto gather = [&](int& cursor) {
@@ -1034,10 +1039,12 @@ __global__ void __launch_bounds__(TW_WARPS * 32) k_texels(TriStore ts, DepthView
             const TriF32& t = S.t32[kk];
             const float inv_minw = t.inv_minw;
             if (__all_sync(FULL, !(inv_minw >= V))) break;  // nothing later can be nearer
+            if (STATS) c_iter++;
             const uint32_t tbx = t.bx, tby = t.by;
             if (!(inv_minw >= V) || px < (int)(tbx & 0xffff) || px > (int)(tbx >> 16) || py < (int)(tby & 0xffff) ||
                 py > (int)(tby >> 16))
                 continue;
+            if (STATS) c_edge++;
             const float fx = (float)(px - t.ox) + 0.5f, fy = (float)(py - t.oy) + 0.5f;  // bbox-local centre
             bool maybe = true, certain = true;
 #pragma unroll
@@ -1074,14 +1081,14 @@ __global__ void __launch_bounds__(TW_WARPS * 32) k_texels(TriStore ts, DepthView
         if (!overflow) {
             if (cs0 >= 0 && ch0 >= V) {
                 const double d = texel_depth(seg[cs0], px, py, near_, far_);
-                c_pairs++;
-                c_cov += d < CUDART_INF;
+                if (STATS) c_pairs++;
+                if (STATS) c_cov += d < CUDART_INF;
                 take(d, cs0, best, bkey);
             }
             if (cs1 >= 0 && ch1 >= V) {
                 const double d = texel_depth(seg[cs1], px, py, near_, far_);
-                c_pairs++;
-                c_cov += d < CUDART_INF;
+                if (STATS) c_pairs++;
+                if (STATS) c_cov += d < CUDART_INF;
                 take(d, cs1, best, bkey);
             }
         } else {  // slow path: every staged triangle whose bbox covers the texel
@@ -1091,8 +1098,8 @@ __global__ void __launch_bounds__(TW_WARPS * 32) k_texels(TriStore ts, DepthView
                     py > (int)(t.by >> 16))
                     continue;
                 const double d = texel_depth(seg[t.gidx], px, py, near_, far_);
-                c_pairs++;
-                c_cov += d < CUDART_INF;
+                if (STATS) c_pairs++;
+                if (STATS) c_cov += d < CUDART_INF;
                 take(d, t.gidx, best, bkey);
             }
         }
@@ -1101,6 +1108,7 @@ __global__ void __launch_bounds__(TW_WARPS * 32) k_texels(TriStore ts, DepthView
     double* dep = dv.depth + (int64_t)f * W * H;
     int cursor = 0;
     int nsel = gather(cursor);
+    int nsel_total = STATS ? nsel : 0;
     if (cursor >= n && nsel <= TW_CAP) {
         // common case: one staging serves every round, per-texel state in registers
         if (nsel > 0) stage(0, nsel);
@@ -1148,6 +1156,7 @@ __global__ void __launch_bounds__(TW_WARPS * 32) k_texels(TriStore ts, DepthView
             }
             if (cursor >= n) break;
             nsel = gather(cursor);
+            if (STATS) nsel_total += nsel;
         }
         if (first) {  // no triangle at all
             for (int r0 = 0; r0 < total; r0 += 32) {
@@ -1161,10 +1170,17 @@ __global__ void __launch_bounds__(TW_WARPS * 32) k_texels(TriStore ts, DepthView
             }
         }
     }
-    if (dv.stats) {
-        if (lane == 0) atomicAdd(dv.stats + GM_STAT_TEXELS, (unsigned long long)total);
+    if (STATS) {
+        if (lane == 0) {
+            atomicAdd(dv.stats + GM_STAT_TEXELS, (unsigned long long)total);
+            atomicAdd(dv.stats + GM_STAT_TX_TILES, 1ull);
+            atomicAdd(dv.stats + GM_STAT_TX_STAGED, (unsigned long long)nsel_total);
+            atomicAdd(dv.stats + GM_STAT_TX_LIST, (unsigned long long)n);
+            atomicAdd(dv.stats + GM_STAT_TX_ITER, c_iter);
+        }
         atomicAdd(dv.stats + GM_STAT_PAIRS, c_pairs);
         atomicAdd(dv.stats + GM_STAT_COVERED, c_cov);
+        atomicAdd(dv.stats + GM_STAT_TX_EDGE, c_edge);
     }
 }
 
@@ -1350,8 +1366,9 @@ extern "C" int gm_plan_create(int device, gm_plan** out) {
         return set_err(GM_ERR_CUDA, cudaGetErrorString(e));
     }
     cudaDeviceGetAttribute(&p->sms, cudaDevAttrMultiProcessorCount, device);
-    CK(cudaFuncSetAttribute(k_texels<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
-    CK(cudaFuncSetAttribute(k_texels<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
     CK(cudaMalloc(&p->d_max, sizeof(unsigned long long)));
     CK(cudaMalloc(&p->d_stats, GM_STAT_N * sizeof(unsigned long long)));
     CK(cudaMemset(p->d_stats, 0, GM_STAT_N * sizeof(unsigned long long)));
@@ -1651,7 +1668,8 @@ static int enqueue_batch(gm_plan* p, const GmFixExact* d_fix, const GmFixCull* d
         const int64_t items = (int64_t)nb * tiles_x * tiles_y;
         CoarseBins cbins = coarse_bins(p, W, H);
         k_coarse<<<nb, 256, 0, s>>>(ts, cbins, p->d_fail, b0);
-        k_texels<false><<<(unsigned)((items + TW_WARPS - 1) / TW_WARPS), TW_WARPS * 32, TX_DYN_SMEM, s>>>(
+        auto kt = dv.stats ? k_texels<false, true> : k_texels<false, false>;
+        kt<<<(unsigned)((items + TW_WARPS - 1) / TW_WARPS), TW_WARPS * 32, TX_DYN_SMEM, s>>>(
             ts, dv, cbins, tiles_x, tiles_x * tiles_y, items, d_fix, b0);
         if (ev) CK(cudaEventRecord(ev[3], s));
         auto ks = dv.stats ? k_samples<true> : k_samples<false>;
@@ -1683,7 +1701,7 @@ static int run_batches(gm_plan* p, const double* fx, int64_t F, const GmConfig* 
     const bool prepared = fx == nullptr;
     double t_start = wall_ms();
     const int W = cfg->zbuffer_resolution, H = cfg->zbuffer_resolution;
-    int B = cfg->batch > 0 ? cfg->batch : 512;
+    int B = cfg->batch > 0 ? cfg->batch : 1024;
     if (B > GM_MAX_BATCH) B = GM_MAX_BATCH;
     const int64_t depth_per_fix = (int64_t)W * H;
     int64_t max_d = std::max<int64_t>(1, ((int64_t)1 << 28) / depth_per_fix);  // z-buffer store <= 2 GiB
@@ -2084,10 +2102,10 @@ static int raster_pass(gm_plan* p, int W, int H, bool attrs) {
     const int64_t items = (int64_t)tiles_x * tiles_y;
     const unsigned grid = (unsigned)((items + TW_WARPS - 1) / TW_WARPS);
     if (attrs)
-        k_texels<true><<<grid, TW_WARPS * 32, TX_DYN_SMEM, s>>>(ts, dv, cbins, tiles_x, tiles_x * tiles_y, items,
+        k_texels<true, false><<<grid, TW_WARPS * 32, TX_DYN_SMEM, s>>>(ts, dv, cbins, tiles_x, tiles_x * tiles_y, items,
                                                                 p->d_fix, 0);
     else
-        k_texels<false><<<grid, TW_WARPS * 32, TX_DYN_SMEM, s>>>(ts, dv, cbins, tiles_x, tiles_x * tiles_y, items,
+        k_texels<false, false><<<grid, TW_WARPS * 32, TX_DYN_SMEM, s>>>(ts, dv, cbins, tiles_x, tiles_x * tiles_y, items,
                                                                  p->d_fix, 0);
     CK(cudaGetLastError());
     return GM_OK;

@@ -1,3 +1,4 @@
 mkdir -p gpurun_out
-timeout 1200 python -m pytest tests -m gpu -q --timeout 600 -p no:cacheprovider > gpurun_out/pytest_gpu4.log 2>&1
-echo "pytest rc=$?" >> gpurun_out/pytest_gpu4.log
+for b in 512 1024 256; do
+timeout 600 python bench.py --steps 2 --warmup 3 --batch $b --no-cpu --no-e2e > gpurun_out/bench_b$b.log 2>&1
+done
