@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-fixations", type=int, default=0)
+    ap.add_argument("--no-stats", action="store_true", help="skip the instrumented roofline pass (profiling runs)")
     return ap.parse_args()
 
 
@@ -320,8 +321,9 @@ def run_ours(args, rank, world):
     stats = (ctypes.c_uint64 * 16)()
     tm_s = _native.GmTimings()
     ms_s = ctypes.c_float(0.0)
-    _native.check(lib.gm_plan_run(plan._h, 1, _native.GM_FLAG_STATS, ctypes.byref(tm_s), ctypes.byref(ms_s)))
-    _native.check(lib.gm_plan_stats(plan._h, stats))
+    if not args.no_stats:
+        _native.check(lib.gm_plan_run(plan._h, 1, _native.GM_FLAG_STATS, ctypes.byref(tm_s), ctypes.byref(ms_s)))
+        _native.check(lib.gm_plan_stats(plan._h, stats))
     st = dict(zip(_native.STAT_NAMES, [int(x) for x in stats]))
     peaks_path = ROOT / "MEASURED_PEAKS.json"
     peaks = json.loads(peaks_path.read_text()) if peaks_path.exists() else {}
@@ -340,8 +342,22 @@ def run_ours(args, rank, world):
     dom = max(times, key=times.get)
     dom_flops = fl.get(dom, 0)
     ach = dom_flops / (times[dom] / 1e3) / 1e12 if times[dom] else None
+    # DRAM bytes per launch of the dominant kernel from the committed ncu --set full capture
+    # (profiles/r1_ncu_traffic.json, written by tools/ncu_traffic.py), per launch like `achieved`
+    traffic, hbm = None, None
+    tpath = ROOT / "profiles" / "r1_ncu_traffic.json"
+    kname = {"k_samples<mark>": "k_mark", "k_samples<accumulate>": "k_samples"}.get(dom, dom)
+    if tpath.exists():
+        tk = json.loads(tpath.read_text())["kernels"].get(kname)
+        if tk and int(tm.batches):
+            traffic = tk["dram_bytes_per_launch"]
+            launch_ms = times[dom] / int(tm.batches)
+            gbs = traffic / (launch_ms / 1e3) / 1e9
+            hbm_peak = peaks.get("hbm_gbs", 7700.0)
+            hbm = {"achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak,
+                   "launch_ms": launch_ms, "fixations_per_launch": tk["fixations_per_launch"]}
     roof = {"bound": "fp64", "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s",
-            "frac": (ach / fp64_peak) if ach else None, "traffic": None, "kernel": dom,
+            "frac": (ach / fp64_peak) if ach else None, "traffic": traffic, "hbm": hbm, "kernel": dom,
             "kernel_ms_per_step": times[dom], "kernel_share": times[dom] / step_ms,
             "algorithmic_flops_per_step": dom_flops,
             "peak_kind": "nominal FP64 FMA peak at max SM clock (MEASURED_PEAKS.json has no FP64 figure)",

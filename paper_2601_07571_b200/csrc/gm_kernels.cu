@@ -35,6 +35,23 @@
 #include "gm_types.h"
 
 #define GM_MAX_BATCH 1024
+// launch bounds of the hot kernels; -DTX_MINB=n etc. (build variants) cap
+// their registers for n CTAs per SM
+#ifdef TX_MINB
+#define TX_BOUNDS __launch_bounds__(TW_WARPS * 32, TX_MINB)
+#else
+#define TX_BOUNDS __launch_bounds__(TW_WARPS * 32)
+#endif
+#ifdef KS_MINB
+#define KS_BOUNDS __launch_bounds__(256, KS_MINB)
+#else
+#define KS_BOUNDS __launch_bounds__(256)
+#endif
+#ifdef KM_MINB
+#define KM_BOUNDS __launch_bounds__(256, KM_MINB)
+#else
+#define KM_BOUNDS __launch_bounds__(256)
+#endif
 
 extern "C" void gm_setup_consts(double theta, int filtering, int width, int height, GmSetupConsts* c);
 extern "C" int64_t gm_setup_batch(const double* fx, int64_t F, const GmSetupConsts* c, GmFixExact* ex,
@@ -466,6 +483,17 @@ enum {
     GM_STAT_N = 16
 };
 #define GM_FLAG_STATS 1
+#define GM_STAT_STRIPES 128  // counter copies (summed by gm_plan_stats): keeps the stats pass free of atomic hot spots
+
+// Warp-aggregated add of a per-lane count to stripe (block % GM_STAT_STRIPES)
+// of counter idx.  Every lane of the warp must call it.
+__device__ __forceinline__ void stat_add(unsigned long long* stats, int idx, unsigned long long v) {
+    const unsigned lo = __reduce_add_sync(0xffffffffu, (unsigned)(v & 0xffffffffu));
+    const unsigned hi = __reduce_add_sync(0xffffffffu, (unsigned)(v >> 32));
+    if ((threadIdx.x & 31) == 0)
+        atomicAdd(stats + (size_t)(blockIdx.x % GM_STAT_STRIPES) * GM_STAT_N + idx,
+                  (unsigned long long)lo + ((unsigned long long)hi << 32));
+}
 
 // kernels.py:219-285 depth_match, reading the texels k_texels evaluated
 // (the 3x3 block around rint(g), which contains the bilinear quad).
@@ -615,7 +643,7 @@ __global__ void k_fix32(const GmFixExact* __restrict__ ex, int nb, double pmax, 
 // -- and the exact float64 computation for the rare lanes whose bounds are too
 // loose (samples within ~E of the camera plane).  Marking extra texels only
 // costs texel work; every texel an exact depth test reads is marked.
-__global__ void __launch_bounds__(256) k_mark(const float* __restrict__ pxf, const float* __restrict__ pyf,
+__global__ void KM_BOUNDS k_mark(const float* __restrict__ pxf, const float* __restrict__ pyf,
                                               const float* __restrict__ pzf, const double* __restrict__ px,
                                               const double* __restrict__ py, const double* __restrict__ pz,
                                               const float4* __restrict__ chunks, const uint32_t* __restrict__ lvl1,
@@ -747,7 +775,7 @@ __global__ void __launch_bounds__(256) k_mark(const float* __restrict__ pxf, con
 }
 
 template <bool STATS>
-__global__ void __launch_bounds__(256) k_samples(const double* __restrict__ px, const double* __restrict__ py,
+__global__ void KS_BOUNDS k_samples(const double* __restrict__ px, const double* __restrict__ py,
                                                  const double* __restrict__ pz, const float4* __restrict__ chunks,
                                                  const uint32_t* __restrict__ lvl1, const int* __restrict__ order,
                                                  int* __restrict__ work, int64_t N, int64_t n_chunks,
@@ -847,12 +875,12 @@ __global__ void __launch_bounds__(256) k_samples(const double* __restrict__ px, 
         }
     }
     if (STATS) {
-        if (lane == 0) atomicAdd(dv.stats + GM_STAT_L1_TESTS, c_l1 * (unsigned long long)B);
-        atomicAdd(dv.stats + GM_STAT_L2_TESTS, (unsigned long long)c_l2);
-        atomicAdd(dv.stats + GM_STAT_EXACT, (unsigned long long)c_exact);
-        atomicAdd(dv.stats + GM_STAT_NDC, (unsigned long long)c_ndc);
-        atomicAdd(dv.stats + GM_STAT_CANDIDATES, (unsigned long long)c_cand);
-        atomicAdd(dv.stats + GM_STAT_VISIBLE, (unsigned long long)c_vis);
+        stat_add(dv.stats, GM_STAT_L1_TESTS, lane == 0 ? c_l1 * (unsigned long long)B : 0ull);
+        stat_add(dv.stats, GM_STAT_L2_TESTS, c_l2);
+        stat_add(dv.stats, GM_STAT_EXACT, c_exact);
+        stat_add(dv.stats, GM_STAT_NDC, c_ndc);
+        stat_add(dv.stats, GM_STAT_CANDIDATES, c_cand);
+        stat_add(dv.stats, GM_STAT_VISIBLE, c_vis);
     }
 }
 
@@ -903,7 +931,7 @@ __device__ __forceinline__ int kth_set_bit(uint32_t w, int k) {
 //      from L1/L2) and the minimum is stored -- the value kernels.rasterize
 //      leaves in that pixel.
 template <bool ATTRS, bool STATS>
-__global__ void __launch_bounds__(TW_WARPS * 32) k_texels(TriStore ts, DepthView dv, CoarseBins cb, int tiles_x,
+__global__ void TX_BOUNDS k_texels(TriStore ts, DepthView dv, CoarseBins cb, int tiles_x,
                                                           int tiles_per_fix, int64_t n_items,
                                                           const GmFixExact* __restrict__ fixes, long long b0) {
     extern __shared__ __align__(16) unsigned char tx_dyn[];
@@ -1171,16 +1199,15 @@ __global__ void __launch_bounds__(TW_WARPS * 32) k_texels(TriStore ts, DepthView
         }
     }
     if (STATS) {
-        if (lane == 0) {
-            atomicAdd(dv.stats + GM_STAT_TEXELS, (unsigned long long)total);
-            atomicAdd(dv.stats + GM_STAT_TX_TILES, 1ull);
-            atomicAdd(dv.stats + GM_STAT_TX_STAGED, (unsigned long long)nsel_total);
-            atomicAdd(dv.stats + GM_STAT_TX_LIST, (unsigned long long)n);
-            atomicAdd(dv.stats + GM_STAT_TX_ITER, c_iter);
-        }
-        atomicAdd(dv.stats + GM_STAT_PAIRS, c_pairs);
-        atomicAdd(dv.stats + GM_STAT_COVERED, c_cov);
-        atomicAdd(dv.stats + GM_STAT_TX_EDGE, c_edge);
+        const bool l0 = lane == 0;
+        stat_add(dv.stats, GM_STAT_TEXELS, l0 ? (unsigned long long)total : 0ull);
+        stat_add(dv.stats, GM_STAT_TX_TILES, l0 ? 1ull : 0ull);
+        stat_add(dv.stats, GM_STAT_TX_STAGED, l0 ? (unsigned long long)nsel_total : 0ull);
+        stat_add(dv.stats, GM_STAT_TX_LIST, l0 ? (unsigned long long)n : 0ull);
+        stat_add(dv.stats, GM_STAT_TX_ITER, l0 ? c_iter : 0ull);
+        stat_add(dv.stats, GM_STAT_PAIRS, c_pairs);
+        stat_add(dv.stats, GM_STAT_COVERED, c_cov);
+        stat_add(dv.stats, GM_STAT_TX_EDGE, c_edge);
     }
 }
 
@@ -1370,8 +1397,8 @@ extern "C" int gm_plan_create(int device, gm_plan** out) {
     CK(cudaFuncSetAttribute(k_texels<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
     CK(cudaFuncSetAttribute(k_texels<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
     CK(cudaMalloc(&p->d_max, sizeof(unsigned long long)));
-    CK(cudaMalloc(&p->d_stats, GM_STAT_N * sizeof(unsigned long long)));
-    CK(cudaMemset(p->d_stats, 0, GM_STAT_N * sizeof(unsigned long long)));
+    CK(cudaMalloc(&p->d_stats, GM_STAT_STRIPES * GM_STAT_N * sizeof(unsigned long long)));
+    CK(cudaMemset(p->d_stats, 0, GM_STAT_STRIPES * GM_STAT_N * sizeof(unsigned long long)));
     CK(cudaMalloc(&p->d_fail, sizeof(long long)));
     CK(cudaMalloc(&p->d_maxcount, sizeof(int)));
     CK(cudaMalloc(&p->d_ntris, sizeof(unsigned long long)));
@@ -1728,7 +1755,8 @@ static int run_batches(gm_plan* p, const double* fx, int64_t F, const GmConfig* 
         CK(cudaEventRecord(ev_start, s));
     }
     if (reset && p->N > 0) CK(cudaMemsetAsync(p->d_values, 0, sizeof(double) * p->N, s));
-    if (cfg->flags & GM_FLAG_STATS) CK(cudaMemsetAsync(p->d_stats, 0, GM_STAT_N * sizeof(unsigned long long), s));
+    if (cfg->flags & GM_FLAG_STATS)
+        CK(cudaMemsetAsync(p->d_stats, 0, GM_STAT_STRIPES * GM_STAT_N * sizeof(unsigned long long), s));
     GmTimings t;
     memset(&t, 0, sizeof(t));
     const bool timing = tm != nullptr;
@@ -1896,7 +1924,13 @@ extern "C" int gm_plan_stats(gm_plan* p, unsigned long long* out) {
     if (!p || !out) return set_err(GM_ERR_ARG, "null argument");
     CK(cudaSetDevice(p->device));
     CK(cudaStreamSynchronize(p->stream));
-    CK(cudaMemcpy(out, p->d_stats, GM_STAT_N * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    std::vector<unsigned long long> st((size_t)GM_STAT_STRIPES * GM_STAT_N);
+    CK(cudaMemcpy(st.data(), p->d_stats, st.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    for (int k = 0; k < GM_STAT_N; k++) {
+        unsigned long long a = 0;
+        for (int r = 0; r < GM_STAT_STRIPES; r++) a += st[(size_t)r * GM_STAT_N + k];
+        out[k] = a;
+    }
     return GM_OK;
 }
 

@@ -9,7 +9,7 @@ timeout 900 python bench.py --steps 3 --warmup 3 > gpurun_out/bench.log 2>&1
 echo "rc=$?" >> gpurun_out/bench.log
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.log 2>&1
 echo "rc=$?" >> gpurun_out/bench_ref.log
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file gpurun_out/launches.csv python bench.py --fixations 8192 --batch 512 --steps 1 --warmup 3 --no-cpu --no-e2e > gpurun_out/ncu_launches.log 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 4000 --csv --log-file gpurun_out/launches.csv python bench.py --fixations 10240 --steps 1 --warmup 2 --no-cpu --no-e2e --no-stats > gpurun_out/ncu_launches.log 2>&1
 echo "rc=$?" >> gpurun_out/ncu_launches.log
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_tri_setup|k_samples|k_texels|k_coarse|k_level1' -s 60 -c 6 -o gpurun_out/prof_r1 python bench.py --fixations 4096 --batch 512 --steps 1 --warmup 3 --no-cpu --no-e2e > gpurun_out/ncu_full.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_tri_setup|k_samples|k_texels|k_coarse|k_level1|k_mark' -s 70 -c 7 -o gpurun_out/prof_r1 -f python bench.py --fixations 4096 --steps 1 --warmup 3 --no-cpu --no-e2e --no-stats > gpurun_out/ncu_full.log 2>&1
 echo "rc=$?" >> gpurun_out/ncu_full.log
