@@ -453,7 +453,9 @@ __global__ void __launch_bounds__(256) k_coarse(TriStore ts, CoarseBins cb, cons
 }
 
 #define TW 32      // k_texels tile width (pixels) = warp lanes
-#define TH 16      // k_texels tile height (pixels)
+#ifndef TH
+#define TH 16      // k_texels tile height (pixels), a power of two <= 32
+#endif
 
 struct DepthView {
     double* depth;    // [B][H][W]: marked texels only
@@ -650,8 +652,8 @@ __global__ void KM_BOUNDS k_mark(const float* __restrict__ pxf, const float* __r
                                               const int* __restrict__ order, int* __restrict__ work, int64_t N,
                                               int64_t n_chunks, int64_t n_supers, const GmFixExact* __restrict__ fixes,
                                               const GmFixF32* __restrict__ fix32, const GmFixCull* __restrict__ culls,
-                                              int B, DepthView dv, double inv_sigma, const long long* __restrict__ fail,
-                                              long long b0) {
+                                              int B, DepthView dv, double inv_sigma, uint32_t* __restrict__ cbits,
+                                              const long long* __restrict__ fail, long long b0) {
     if (*fail <= b0) return;
     const int lane = threadIdx.x & 31;
     const int ngroups = (B + 31) >> 5;
@@ -684,6 +686,7 @@ __global__ void KM_BOUNDS k_mark(const float* __restrict__ pxf, const float* __r
             const int g = gi * 32;
             const bool pass = ((sm >> lane) & 1u) && sphere_visible(culls[g + lane], sph, false);
             unsigned mask = __ballot_sync(0xffffffffu, pass);
+            unsigned my_bits = 0;  // fixations (bit j of group gi) for which this lane is a candidate
             while (mask) {
                 const int j = __ffs(mask) - 1;
                 mask &= mask - 1;
@@ -761,6 +764,7 @@ __global__ void KM_BOUNDS k_mark(const float* __restrict__ pxf, const float* __r
                 }
                 const int bx0 = max(cxlo - 1, 0), bx1 = min(cxhi + 1, W - 1);
                 const int by0 = max(cylo - 1, 0), by1 = min(cyhi + 1, H - 1);
+                my_bits |= 1u << j;
                 uint32_t* m = dv.mask + (int64_t)f * H * dv.wwords;
                 const unsigned long long bits = ((1ull << (bx1 - bx0 + 1)) - 1ull) << (bx0 & 31);
                 const int w0 = bx0 >> 5;
@@ -770,6 +774,10 @@ __global__ void KM_BOUNDS k_mark(const float* __restrict__ pxf, const float* __r
                     if (bits >> 32) atomicOr(row + 1, (uint32_t)(bits >> 32));
                 }
             }
+            // level 3 for the accumulation pass: the fixations of this group with at
+            // least one (float32-superset) candidate in this chunk
+            const unsigned word = __reduce_or_sync(0xffffffffu, my_bits);
+            if (lane == 0) cbits[ch * 32 + gi] = word;
         }
     }
 }
@@ -782,8 +790,8 @@ __global__ void KS_BOUNDS k_samples(const double* __restrict__ px, const double*
                                                  int64_t n_supers, const GmFixExact* __restrict__ fixes,
                                                  const GmFixCull* __restrict__ culls, int B, DepthView dv,
                                                  double inv_sigma, double eps_abs, double eps_rel,
-                                                 double* __restrict__ values, const long long* __restrict__ fail,
-                                                 long long b0) {
+                                                 double* __restrict__ values, const uint32_t* __restrict__ cbits,
+                                                 const long long* __restrict__ fail, long long b0) {
     if (*fail <= b0) return;  // this batch overflowed the triangle store: the host redoes it
     const int lane = threadIdx.x & 31;
     const int ngroups = (B + 31) >> 5;  // <= 32 (B <= GM_MAX_BATCH)
@@ -815,15 +823,13 @@ __global__ void KS_BOUNDS k_samples(const double* __restrict__ px, const double*
             wz = pz[i];
             v = values[i];
         }
-        const float4 sph = chunks[ch];
         for (int gi = 0; gi < ngroups; gi++) {
             const unsigned sm = __shfl_sync(0xffffffffu, l1, gi);
             if (!sm) continue;
             const int g = gi * 32;
-            // level 2: this chunk's 32 samples against the fixations that passed level 1
-            bool pass = ((sm >> lane) & 1u) && sphere_visible(culls[g + lane], sph, false);
+            // levels 2 + 3 (k_mark): the fixations of this group with a candidate in the chunk
             if (STATS) c_l2 += (sm >> lane) & 1u;
-            unsigned mask = __ballot_sync(0xffffffffu, pass);
+            unsigned mask = cbits[ch * 32 + gi];
             while (mask) {
                 const int j = __ffs(mask) - 1;
                 mask &= mask - 1;
@@ -1034,7 +1040,7 @@ __global__ void TX_BOUNDS k_texels(TriStore ts, DepthView dv, CoarseBins cb, int
     auto texel_of = [&](int q, int& row, int& colo) {
         row = 0;
 #pragma unroll
-        for (int step = 8; step > 0; step >>= 1) {
+        for (int step = TH / 2; step > 0; step >>= 1) {
             const int cand = row + step;
             const int pc = __shfl_sync(FULL, pref_ex, cand & 31);
             if (cand < TH && pc <= q) row = cand;
@@ -1304,6 +1310,7 @@ struct gm_plan {
     float4* d_super = nullptr;  // sphere per 8 chunks (256 samples)
     int64_t n_supers = 0;
     uint32_t* d_lvl1 = nullptr;  // [n_supers][B/32] level-1 ballots of the current batch
+    uint32_t* d_cbits = nullptr; // [n_chunks][32] k_mark's per-chunk candidate fixations (bit j of group g)
     int *d_lcount = nullptr, *d_lorder = nullptr, *d_lcount2 = nullptr, *d_lorder2 = nullptr;
     int* d_work = nullptr;       // [2] work counters of the two sample passes
     void* d_sort_tmp = nullptr;
@@ -1368,9 +1375,9 @@ static void plan_free_scene(gm_plan* p) {
     cudaFree(p->d_pxf); cudaFree(p->d_pyf); cudaFree(p->d_pzf);
     p->d_pxf = p->d_pyf = p->d_pzf = nullptr;
     cudaFree(p->d_chunk); cudaFree(p->d_values); cudaFree(p->d_super);
-    cudaFree(p->d_lvl1); cudaFree(p->d_lcount); cudaFree(p->d_lorder); cudaFree(p->d_lcount2);
+    cudaFree(p->d_lvl1); cudaFree(p->d_cbits); cudaFree(p->d_lcount); cudaFree(p->d_lorder); cudaFree(p->d_lcount2);
     cudaFree(p->d_lorder2); cudaFree(p->d_sort_tmp);
-    p->d_lvl1 = nullptr; p->d_lcount = p->d_lorder = p->d_lcount2 = p->d_lorder2 = nullptr;
+    p->d_lvl1 = nullptr; p->d_cbits = nullptr; p->d_lcount = p->d_lorder = p->d_lcount2 = p->d_lorder2 = nullptr;
     p->d_sort_tmp = nullptr; p->sort_tmp_bytes = 0; p->cap_lvl1 = 0;
     p->d_tw = nullptr; p->d_tsph = p->d_csph = p->d_chunk = p->d_super = nullptr;
     p->d_px = p->d_py = p->d_pz = p->d_values = nullptr;
@@ -1493,6 +1500,7 @@ extern "C" int gm_plan_set_scene(gm_plan* p, int n_obj, const int64_t* tri_count
     if ((rc = dev_alloc(&p->d_lorder, (size_t)p->n_supers))) return rc;
     if ((rc = dev_alloc(&p->d_lcount2, (size_t)p->n_supers))) return rc;
     if ((rc = dev_alloc(&p->d_lorder2, (size_t)p->n_supers))) return rc;
+    if ((rc = dev_alloc(&p->d_cbits, (size_t)std::max<int64_t>(p->n_chunks, 1) * 32))) return rc;
     {
         size_t tb = 0;
         cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, p->d_lcount, p->d_lcount2, p->d_lorder,
@@ -1690,7 +1698,7 @@ static int enqueue_batch(gm_plan* p, const GmFixExact* d_fix, const GmFixCull* d
         k_fix32<<<blocks_for(nb, 128), 128, 0, s>>>(d_fix, nb, p->pmax, 1.0 / inv_sigma, p->d_fix32);
         k_mark<<<grid, 256, 0, s>>>(p->d_pxf, p->d_pyf, p->d_pzf, p->d_px, p->d_py, p->d_pz, p->d_chunk, p->d_lvl1,
                                     p->d_lorder2, p->d_work, p->N, p->n_chunks, p->n_supers, d_fix, p->d_fix32,
-                                    d_cull, nb, dv, inv_sigma, p->d_fail, b0);
+                                    d_cull, nb, dv, inv_sigma, p->d_cbits, p->d_fail, b0);
         if (ev) CK(cudaEventRecord(ev[2], s));
         const int64_t items = (int64_t)nb * tiles_x * tiles_y;
         CoarseBins cbins = coarse_bins(p, W, H);
@@ -1702,7 +1710,7 @@ static int enqueue_batch(gm_plan* p, const GmFixExact* d_fix, const GmFixCull* d
         auto ks = dv.stats ? k_samples<true> : k_samples<false>;
         ks<<<grid, 256, 0, s>>>(p->d_px, p->d_py, p->d_pz, p->d_chunk, p->d_lvl1, p->d_lorder2, p->d_work + 1, p->N,
                                 p->n_chunks, p->n_supers, d_fix, d_cull, nb, dv, inv_sigma, cfg->eps_abs,
-                                cfg->eps_rel, p->d_values, p->d_fail, b0);
+                                cfg->eps_rel, p->d_values, p->d_cbits, p->d_fail, b0);
     } else if (ev) {
         CK(cudaEventRecord(ev[2], s));
         CK(cudaEventRecord(ev[3], s));
