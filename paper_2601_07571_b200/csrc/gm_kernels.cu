@@ -384,6 +384,12 @@ __global__ void __launch_bounds__(256) k_tri_setup(const double* __restrict__ tw
 // scan, fill.  Per-fixation CSR in citems[f * cap_items ...]; if the items do
 // not fit, covf[f] = 1 and k_texels scans the fixation's whole list instead.
 #define GM_MAX_CBINS 1024
+#ifndef CB_SHIFT
+#define CB_SHIFT 6  // coarse bins of 64 x 64 pixels (k_texels tiles are 32 x 16)
+#endif
+#ifndef CB_ITEMS_PER_TRI
+#define CB_ITEMS_PER_TRI 4  // coarse-bin list capacity per screen triangle (more: scan the whole list)
+#endif
 struct CoarseBins {
     int* items;   // [B][cap_items]
     int* off;     // [B][GM_MAX_CBINS + 1]
@@ -1636,8 +1642,8 @@ static int ensure_batch(gm_plan* p, int B, int W, int H, int64_t seg) {
         if ((rc = dev_alloc(&p->d_vbuf, (size_t)B * W * H))) return rc;
         p->cap_depth = (int64_t)B * W * H;
     }
-    if (B > p->cap_cB || 4 * p->cap_seg > p->cap_citems) {
-        const int64_t ci = 4 * std::max<int64_t>(p->cap_seg, seg);
+    if (B > p->cap_cB || CB_ITEMS_PER_TRI * p->cap_seg > p->cap_citems) {
+        const int64_t ci = CB_ITEMS_PER_TRI * std::max<int64_t>(p->cap_seg, seg);
         if ((rc = dev_alloc(&p->d_citems, (size_t)B * ci))) return rc;
         if ((rc = dev_alloc(&p->d_coff, (size_t)B * (GM_MAX_CBINS + 1)))) return rc;
         if ((rc = dev_alloc(&p->d_covf, (size_t)B))) return rc;
@@ -1656,7 +1662,7 @@ typedef void (*gm_progress_fn)(int64_t done, int64_t total, void* user);
 
 // Coarse-bin geometry for a W x H buffer: cb = 64 px, doubled until <= GM_MAX_CBINS bins.
 static CoarseBins coarse_bins(gm_plan* p, int W, int H) {
-    int shift = 6;
+    int shift = CB_SHIFT;
     while ((int64_t)((W + (1 << shift) - 1) >> shift) * ((H + (1 << shift) - 1) >> shift) > GM_MAX_CBINS) shift++;
     CoarseBins cb{p->d_citems, p->d_coff, p->d_covf, p->cap_citems, shift, (W + (1 << shift) - 1) >> shift,
                   (H + (1 << shift) - 1) >> shift};

@@ -1,4 +1,5 @@
-mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -q --timeout 600 -p no:cacheprovider -x > gpurun_out/pytest_gpu5.log 2>&1
-echo "pytest rc=$?" >> gpurun_out/pytest_gpu5.log
-timeout 600 python bench.py --steps 3 --warmup 3 --no-cpu > gpurun_out/bench5.log 2>&1
+mkdir -p gpurun_out; rm -f gpurun_out/variants.txt
+for v in _gazemap_b200 _v_cb5 _v_cb7; do
+  GAZEMAP_B200_SO=paper_2601_07571_b200/$v.so timeout 600 python bench.py --steps 3 --warmup 2 --fixations 30720 --no-cpu --no-e2e --no-stats > gpurun_out/bv_$v.log 2>&1
+  echo "$v $(grep -o '"phases_ms": {[^}]*}' gpurun_out/bv_$v.log) $(grep -o '"ms_per_step": [0-9.]*' gpurun_out/bv_$v.log)" >> gpurun_out/variants.txt
+done
