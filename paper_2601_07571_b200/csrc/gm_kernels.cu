@@ -470,6 +470,8 @@ struct DepthView {
     unsigned long long* stats;  // optional work counters (GM_STAT_*), nullptr = off
     float* vbuf;      // [B][H][W]: k_texels' inverse-depth bounds for tiles with many triangles
     int* key;         // [H][W] (ATTRS only): order key 2 t + fan of the triangle that wrote the texel
+    int* crowd;       // work items deferred to k_texels<CROWDED> (nullptr: handle them in place)
+    int* crowd_count; // [2]: deferred items, claimed items
 };
 
 // Work counters filled when GmConfig.flags & GM_FLAG_STATS (bench roofline).
@@ -904,6 +906,18 @@ struct __align__(16) TexelWarpSmem {
     int sel[TW_SEL + 32];
 };
 #define TX_DYN_SMEM (TW_WARPS * (int)sizeof(TexelWarpSmem))
+#define TC_SEL 512   // crowded tiles: overlap list sorted per pass (longer lists: several passes)
+#define TC_RES 64    // crowded tiles: nearest triangles staged in shared memory
+struct __align__(16) CrowdedWarpSmem {
+    TriF32 t32[TC_RES];
+    int sel[TC_SEL];
+    float key[TC_SEL];
+};
+#define TC_WARPS 4
+#ifndef CROWD_MIN
+#define CROWD_MIN 128  // tiles overlapping more triangles than this go to the crowded pass
+#endif
+#define TC_DYN_SMEM (TC_WARPS * (int)sizeof(CrowdedWarpSmem))
 
 // position of the k-th (0-based) set bit of w (k < popc(w))
 __device__ __forceinline__ int kth_set_bit(uint32_t w, int k) {
@@ -942,15 +956,14 @@ __device__ __forceinline__ int kth_set_bit(uint32_t w, int k) {
 //      reference's float64 pixel arithmetic (texel_depth, float64 record read
 //      from L1/L2) and the minimum is stored -- the value kernels.rasterize
 //      leaves in that pixel.
-template <bool ATTRS, bool STATS>
-__global__ void TX_BOUNDS k_texels(TriStore ts, DepthView dv, CoarseBins cb, int tiles_x,
-                                                          int tiles_per_fix, int64_t n_items,
-                                                          const GmFixExact* __restrict__ fixes, long long b0) {
-    extern __shared__ __align__(16) unsigned char tx_dyn[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    TexelWarpSmem& S = reinterpret_cast<TexelWarpSmem*>(tx_dyn)[warp];
-    const int64_t item = (int64_t)blockIdx.x * TW_WARPS + warp;
-    if (item >= n_items || *ts.fail <= b0) return;
+// One (fixation, tile) work item of k_texels.  T32/SEL: the warp's staging and
+// selection slices; KEY (crowded mode only): sort keys of SEL.
+template <bool ATTRS, bool STATS, bool CROWDED>
+__device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __restrict__ SEL, float* __restrict__ KEY,
+                                           int64_t item, const TriStore& ts, const DepthView& dv,
+                                           const CoarseBins& cb, int tiles_x, int tiles_per_fix,
+                                           const GmFixExact* __restrict__ fixes) {
+    const int lane = threadIdx.x & 31;
     const int f = (int)(item / tiles_per_fix);
     const int tile = (int)(item - (int64_t)f * tiles_per_fix);
     const int W = dv.W, H = dv.H;
@@ -1002,7 +1015,7 @@ __global__ void TX_BOUNDS k_texels(TriStore ts, DepthView dv, CoarseBins cb, int
                 sel = !(x1 < xb || x0 > xe || y1 < yb || y0 > ye);
             }
             const unsigned bal = __ballot_sync(FULL, sel);
-            if (sel) S.sel[cnt + __popc(bal & ((1u << lane) - 1u))] = i;
+            if (sel) SEL[cnt + __popc(bal & ((1u << lane) - 1u))] = i;
             cnt += __popc(bal);
             cursor += 32;
         }
@@ -1010,11 +1023,11 @@ __global__ void TX_BOUNDS k_texels(TriStore ts, DepthView dv, CoarseBins cb, int
         return cnt;  // may exceed TW_SEL by < 32 (S.sel has the room)
     };
 
-    // 2. stage S.sel[c0 .. c0 + kend) (float32 forms) in ascending min-depth order
+    // 2. stage SEL[c0 .. c0 + kend) (float32 forms) in ascending min-depth order
     const TriF32* segf = ts.t32 + (int64_t)f * ts.cap_seg;
     auto stage = [&](int c0, int kend) {
         __syncwarp();
-        const int gi = lane < kend ? S.sel[c0 + lane] : 0;
+        const int gi = lane < kend ? SEL[c0 + lane] : 0;
         float key = lane < kend ? -__ldg(&segf[gi].inv_minw) : CUDART_INF_F;  // ascending min depth
         int slot = lane;
 #pragma unroll
@@ -1035,7 +1048,7 @@ __global__ void TX_BOUNDS k_texels(TriStore ts, DepthView dv, CoarseBins cb, int
         const int src = __shfl_sync(FULL, gi, slot);
         if (lane < kend) {
             const uint4* from = reinterpret_cast<const uint4*>(segf + src);
-            uint4* to = reinterpret_cast<uint4*>(&S.t32[lane]);
+            uint4* to = reinterpret_cast<uint4*>(&T32[lane]);
 #pragma unroll
             for (int part = 0; part < 6; part++) to[part] = from[part];
         }
@@ -1070,13 +1083,15 @@ __global__ void TX_BOUNDS k_texels(TriStore ts, DepthView dv, CoarseBins cb, int
             bkey = key;
         }
     };
-    auto walk = [&](int kend, bool valid, int row, int colo, float& V, double& best, int& bkey) {
+    // triangle kk of the walk: staged in shared memory (kk < nst) or, crowded mode, from global
+    auto tri_at = [&](int kk, int nst) -> const TriF32& { return (!CROWDED || kk < nst) ? T32[kk] : segf[SEL[kk]]; };
+    auto walk = [&](int kend, int nst, bool valid, int row, int colo, float& V, double& best, int& bkey) {
         const int px = xb + colo, py = yb + row;
         int cs0 = -1, cs1 = -1;  // exact candidates (global record index) and their bounds
         float ch0 = 0.0f, ch1 = 0.0f;
         bool overflow = false;
         for (int kk = 0; kk < kend; kk++) {
-            const TriF32& t = S.t32[kk];
+            const TriF32& t = tri_at(kk, nst);
             const float inv_minw = t.inv_minw;
             if (__all_sync(FULL, !(inv_minw >= V))) break;  // nothing later can be nearer
             if (STATS) c_iter++;
@@ -1133,7 +1148,7 @@ __global__ void TX_BOUNDS k_texels(TriStore ts, DepthView dv, CoarseBins cb, int
             }
         } else {  // slow path: every staged triangle whose bbox covers the texel
             for (int k = 0; k < kend; k++) {
-                const TriF32& t = S.t32[k];
+                const TriF32& t = tri_at(k, nst);
                 if (px < (int)(t.bx & 0xffff) || px > (int)(t.bx >> 16) || py < (int)(t.by & 0xffff) ||
                     py > (int)(t.by >> 16))
                     continue;
@@ -1147,68 +1162,160 @@ __global__ void TX_BOUNDS k_texels(TriStore ts, DepthView dv, CoarseBins cb, int
 
     double* dep = dv.depth + (int64_t)f * W * H;
     int cursor = 0;
-    int nsel = gather(cursor);
-    int nsel_total = STATS ? nsel : 0;
-    if (cursor >= n && nsel <= TW_CAP) {
-        // common case: one staging serves every round, per-texel state in registers
-        if (nsel > 0) stage(0, nsel);
-        for (int r0 = 0; r0 < total; r0 += 32) {
-            const int q = r0 + lane;
-            const bool valid = q < total;
-            int row, colo;
-            texel_of(q, row, colo);
-            float V = valid ? 0.0f : CUDART_INF_F;
-            double best = CUDART_INF;
-            int bkey = INT_MAX;
-            if (nsel > 0) walk(nsel, valid, row, colo, V, best, bkey);
-            if (valid) {
-                dep[(int64_t)(yb + row) * W + xb + colo] = best;
-                if (ATTRS) dv.key[(int64_t)(yb + row) * W + xb + colo] = best < CUDART_INF ? bkey : -1;
+    int nsel_total = 0;
+    auto store = [&](int row, int colo, double best, int bkey) {
+        dep[(int64_t)(yb + row) * W + xb + colo] = best;
+        if (ATTRS) dv.key[(int64_t)(yb + row) * W + xb + colo] = best < CUDART_INF ? bkey : -1;
+    };
+    if (!CROWDED) {
+        int nsel = gather(cursor);
+        if (STATS) nsel_total = nsel;
+        if ((cursor < n || nsel > CROWD_MIN) && dv.crowd) {
+            // more than TW_CAP triangles: k_texels<CROWDED> sorts the whole list (deferred)
+            if (lane == 0) dv.crowd[atomicAdd(dv.crowd_count, 1)] = (int)item;
+            return;
+        }
+        if (cursor >= n && nsel <= TW_CAP) {
+            // common case: one staging serves every round, per-texel state in registers
+            if (nsel > 0) stage(0, nsel);
+            for (int r0 = 0; r0 < total; r0 += 32) {
+                const int q = r0 + lane;
+                const bool valid = q < total;
+                int row, colo;
+                texel_of(q, row, colo);
+                float V = valid ? 0.0f : CUDART_INF_F;
+                double best = CUDART_INF;
+                int bkey = INT_MAX;
+                if (nsel > 0) walk(nsel, nsel, valid, row, colo, V, best, bkey);
+                if (valid) store(row, colo, best, bkey);
+            }
+        } else {
+            // many triangles without a deferral list: chunk by chunk (each staged once),
+            // per-texel state kept in the depth array and the inverse-depth-bound buffer
+            float* vb = dv.vbuf + (int64_t)f * W * H;
+            bool first = true;
+            while (true) {
+                for (int c0 = 0; c0 < nsel; c0 += TW_CAP) {
+                    const int kend = min(TW_CAP, nsel - c0);
+                    stage(c0, kend);
+                    for (int r0 = 0; r0 < total; r0 += 32) {
+                        const int q = r0 + lane;
+                        const bool valid = q < total;
+                        int row, colo;
+                        texel_of(q, row, colo);
+                        const int64_t at = (int64_t)(yb + row) * W + xb + colo;
+                        float V = valid ? (first ? 0.0f : vb[at]) : CUDART_INF_F;
+                        double best = (valid && !first) ? dep[at] : CUDART_INF;
+                        int bkey = INT_MAX;
+                        if (ATTRS && valid && !first) bkey = dv.key[at];
+                        walk(kend, kend, valid, row, colo, V, best, bkey);
+                        if (valid) {
+                            dep[at] = best;
+                            vb[at] = V;
+                            if (ATTRS) dv.key[at] = best < CUDART_INF ? bkey : -1;
+                        }
+                    }
+                    first = false;
+                }
+                if (cursor >= n) break;
+                nsel = gather(cursor);
+                if (STATS) nsel_total += nsel;
+            }
+            if (first) {  // no triangle at all
+                for (int r0 = 0; r0 < total; r0 += 32) {
+                    const int q = r0 + lane;
+                    int row, colo;
+                    texel_of(q, row, colo);
+                    if (q < total) store(row, colo, CUDART_INF, -1);
+                }
             }
         }
     } else {
-        // many triangles: chunk by chunk (each staged once), per-texel state kept in
-        // the depth array and the inverse-depth-bound buffer between chunks
+        // crowded tile: gather the whole overlap list (TC_SEL at a time), sort it by
+        // ascending min depth, stage the nearest TC_RES float32 forms; the walk reads
+        // any later one from global memory.  The nearest certain cover then proves
+        // (V) that every later triangle is behind it, so a texel's walk usually ends
+        // in the first chunk -- nested surfaces cost one sort, not one pass each.
         float* vb = dv.vbuf + (int64_t)f * W * H;
         bool first = true;
-        while (true) {
-            for (int c0 = 0; c0 < nsel; c0 += TW_CAP) {
-                const int kend = min(TW_CAP, nsel - c0);
-                stage(c0, kend);
-                for (int r0 = 0; r0 < total; r0 += 32) {
-                    const int q = r0 + lane;
-                    const bool valid = q < total;
-                    int row, colo;
-                    texel_of(q, row, colo);
-                    const int64_t at = (int64_t)(yb + row) * W + xb + colo;
-                    float V = valid ? (first ? 0.0f : vb[at]) : CUDART_INF_F;
-                    double best = (valid && !first) ? dep[at] : CUDART_INF;
-                    int bkey = INT_MAX;
-                    if (ATTRS && valid && !first) bkey = dv.key[at];
-                    walk(kend, valid, row, colo, V, best, bkey);
-                    if (valid) {
-                        dep[at] = best;
-                        vb[at] = V;
-                        if (ATTRS) dv.key[at] = best < CUDART_INF ? bkey : -1;
-                    }
+        do {
+            int cnt = 0;
+            while (cursor < n && cnt < TC_SEL - 32) {
+                int i = cursor + lane;
+                bool sel = false;
+                if (i < n) {
+                    if (clist) i = clist[i];
+                    const uint2 bbx = segb[i];
+                    const int x0 = bbx.x & 0xffff, x1 = bbx.x >> 16, y0 = bbx.y & 0xffff, y1 = bbx.y >> 16;
+                    sel = !(x1 < xb || x0 > xe || y1 < yb || y0 > ye);
                 }
-                first = false;
+                const unsigned bal = __ballot_sync(FULL, sel);
+                if (sel) {
+                    const int at = cnt + __popc(bal & ((1u << lane) - 1u));
+                    SEL[at] = i;
+                    KEY[at] = -__ldg(&segf[i].inv_minw);
+                }
+                cnt += __popc(bal);
+                cursor += 32;
             }
-            if (cursor >= n) break;
-            nsel = gather(cursor);
-            if (STATS) nsel_total += nsel;
-        }
-        if (first) {  // no triangle at all
+            if (STATS) nsel_total += cnt;
+            int P = 32;
+            while (P < cnt) P <<= 1;
+            for (int k = cnt + lane; k < P; k += 32) {
+                KEY[k] = CUDART_INF_F;
+                SEL[k] = -1;
+            }
+            __syncwarp();
+            // warp bitonic sort of (KEY, SEL) ascending, P <= TC_SEL
+            for (int size = 2; size <= P; size <<= 1) {
+                for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                    for (int a = lane; a < P; a += 32) {
+                        const int b = a ^ stride;
+                        if (b > a) {
+                            const float ka = KEY[a], kb = KEY[b];
+                            const int sa = SEL[a], sb = SEL[b];
+                            const bool up = (a & size) == 0;
+                            const bool gt = ka > kb || (ka == kb && sa > sb);
+                            if (gt == up) {
+                                KEY[a] = kb;
+                                KEY[b] = ka;
+                                SEL[a] = sb;
+                                SEL[b] = sa;
+                            }
+                        }
+                    }
+                    __syncwarp();
+                }
+            }
+            const int ns = min(cnt, TC_RES);
+            for (int k = lane; k < ns; k += 32) {
+                const uint4* from = reinterpret_cast<const uint4*>(segf + SEL[k]);
+                uint4* to = reinterpret_cast<uint4*>(&T32[k]);
+#pragma unroll
+                for (int part = 0; part < 6; part++) to[part] = from[part];
+            }
+            __syncwarp();
+            const bool last = cursor >= n;
             for (int r0 = 0; r0 < total; r0 += 32) {
                 const int q = r0 + lane;
+                const bool valid = q < total;
                 int row, colo;
                 texel_of(q, row, colo);
-                if (q < total) {
-                    dep[(int64_t)(yb + row) * W + xb + colo] = CUDART_INF;
-                    if (ATTRS) dv.key[(int64_t)(yb + row) * W + xb + colo] = -1;
+                const int64_t at = (int64_t)(yb + row) * W + xb + colo;
+                float V = valid ? (first ? 0.0f : vb[at]) : CUDART_INF_F;
+                double best = (valid && !first) ? dep[at] : CUDART_INF;
+                int bkey = INT_MAX;
+                if (ATTRS && valid && !first) bkey = dv.key[at];
+                if (cnt > 0) walk(cnt, ns, valid, row, colo, V, best, bkey);
+                if (valid) {
+                    dep[at] = best;
+                    if (!last) vb[at] = V;
+                    if (ATTRS) dv.key[at] = best < CUDART_INF ? bkey : -1;
                 }
             }
-        }
+            first = false;
+            __syncwarp();
+        } while (cursor < n);
     }
     if (STATS) {
         const bool l0 = lane == 0;
@@ -1220,6 +1327,33 @@ __global__ void TX_BOUNDS k_texels(TriStore ts, DepthView dv, CoarseBins cb, int
         stat_add(dv.stats, GM_STAT_PAIRS, c_pairs);
         stat_add(dv.stats, GM_STAT_COVERED, c_cov);
         stat_add(dv.stats, GM_STAT_TX_EDGE, c_edge);
+    }
+}
+
+template <bool ATTRS, bool STATS, bool CROWDED>
+__global__ void TX_BOUNDS k_texels(TriStore ts, DepthView dv, CoarseBins cb, int tiles_x,
+                                   int tiles_per_fix, int64_t n_items,
+                                   const GmFixExact* __restrict__ fixes, long long b0) {
+    extern __shared__ __align__(16) unsigned char tx_dyn[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (*ts.fail <= b0) return;
+    if (!CROWDED) {
+        const int64_t item = (int64_t)blockIdx.x * TW_WARPS + warp;
+        if (item < n_items)
+            texel_item<ATTRS, STATS, false>(reinterpret_cast<TexelWarpSmem*>(tx_dyn)[warp].t32,
+                                            reinterpret_cast<TexelWarpSmem*>(tx_dyn)[warp].sel, nullptr, item, ts, dv,
+                                            cb, tiles_x, tiles_per_fix, fixes);
+        return;
+    }
+    // crowded tiles (deferred by the pass above): persistent warps over the list
+    CrowdedWarpSmem& C = reinterpret_cast<CrowdedWarpSmem*>(tx_dyn)[warp];
+    const int n_crowd = *dv.crowd_count;
+    for (;;) {
+        int w = 0;
+        if (lane == 0) w = atomicAdd(dv.crowd_count + 1, 1);
+        w = __shfl_sync(0xffffffffu, w, 0);
+        if (w >= n_crowd) break;
+        texel_item<ATTRS, STATS, true>(C.t32, C.sel, C.key, dv.crowd[w], ts, dv, cb, tiles_x, tiles_per_fix, fixes);
     }
 }
 
@@ -1372,6 +1506,9 @@ struct gm_plan {
     std::vector<int64_t> tstart, nsamp;
     std::vector<uint8_t> include;
     int* d_key = nullptr;  // [H][W] raster_pass(attrs): order key of the winning triangle
+    int* d_crowd = nullptr;        // [B * tiles] k_texels items deferred to the crowded pass
+    int* d_crowd_count = nullptr;  // [2]
+    int64_t cap_crowd = 0;
     int64_t cap_key = 0;
 };
 
@@ -1406,9 +1543,12 @@ extern "C" int gm_plan_create(int device, gm_plan** out) {
         return set_err(GM_ERR_CUDA, cudaGetErrorString(e));
     }
     cudaDeviceGetAttribute(&p->sms, cudaDevAttrMultiProcessorCount, device);
-    CK(cudaFuncSetAttribute(k_texels<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
-    CK(cudaFuncSetAttribute(k_texels<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
-    CK(cudaFuncSetAttribute(k_texels<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels<false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels<false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels<true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels<false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels<true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_DYN_SMEM));
     CK(cudaMalloc(&p->d_max, sizeof(unsigned long long)));
     CK(cudaMalloc(&p->d_stats, GM_STAT_STRIPES * GM_STAT_N * sizeof(unsigned long long)));
     CK(cudaMemset(p->d_stats, 0, GM_STAT_STRIPES * GM_STAT_N * sizeof(unsigned long long)));
@@ -1437,6 +1577,7 @@ extern "C" void gm_plan_destroy(gm_plan* p) {
     cudaFree(p->d_fix_all); cudaFree(p->d_cull_all); cudaFree(p->d_flush);
     cudaFree(p->d_depth); cudaFree(p->d_mask); cudaFree(p->d_vbuf);
     cudaFree(p->d_citems); cudaFree(p->d_coff); cudaFree(p->d_covf); cudaFree(p->d_key);
+    cudaFree(p->d_crowd); cudaFree(p->d_crowd_count);
     cudaStreamDestroy(p->stream);
     delete p;
 }
@@ -1650,6 +1791,12 @@ static int ensure_batch(gm_plan* p, int B, int W, int H, int64_t seg) {
         p->cap_citems = ci;
         p->cap_cB = B;
     }
+    const int64_t n_tiles = (int64_t)B * ((W + TW - 1) / TW) * ((H + TH - 1) / TH);
+    if (n_tiles > p->cap_crowd) {
+        if ((rc = dev_alloc(&p->d_crowd, (size_t)n_tiles))) return rc;
+        if (!p->d_crowd_count && (rc = dev_alloc(&p->d_crowd_count, 2))) return rc;
+        p->cap_crowd = n_tiles;
+    }
     const int64_t lw = std::max<int64_t>(p->n_supers, 1) * ((B + 31) / 32);
     if (lw > p->cap_lvl1) {
         if ((rc = dev_alloc(&p->d_lvl1, (size_t)lw))) return rc;
@@ -1667,6 +1814,23 @@ static CoarseBins coarse_bins(gm_plan* p, int W, int H) {
     CoarseBins cb{p->d_citems, p->d_coff, p->d_covf, p->cap_citems, shift, (W + (1 << shift) - 1) >> shift,
                   (H + (1 << shift) - 1) >> shift};
     return cb;
+}
+
+
+// k_texels over `items` (fixation, tile) work items, then the crowded tiles the
+// first pass deferred (k_texels<CROWDED>, persistent, larger shared slices).
+template <bool ATTRS, bool STATS>
+static int launch_texels(gm_plan* p, cudaStream_t s, const TriStore& ts, DepthView dv, const CoarseBins& cb,
+                         int tiles_x, int tiles_per_fix, int64_t items, const GmFixExact* fix, long long b0) {
+    dv.crowd = p->d_crowd;
+    dv.crowd_count = p->d_crowd_count;
+    CK(cudaMemsetAsync(p->d_crowd_count, 0, 2 * sizeof(int), s));
+    k_texels<ATTRS, STATS, false><<<(unsigned)((items + TW_WARPS - 1) / TW_WARPS), TW_WARPS * 32, TX_DYN_SMEM, s>>>(
+        ts, dv, cb, tiles_x, tiles_per_fix, items, fix, b0);
+    k_texels<ATTRS, STATS, true><<<p->sms * 5, TC_WARPS * 32, TC_DYN_SMEM, s>>>(ts, dv, cb, tiles_x, tiles_per_fix,
+                                                                              items, fix, b0);
+    CK(cudaGetLastError());
+    return GM_OK;
 }
 
 static inline double wall_ms() {
@@ -1709,9 +1873,9 @@ static int enqueue_batch(gm_plan* p, const GmFixExact* d_fix, const GmFixCull* d
         const int64_t items = (int64_t)nb * tiles_x * tiles_y;
         CoarseBins cbins = coarse_bins(p, W, H);
         k_coarse<<<nb, 256, 0, s>>>(ts, cbins, p->d_fail, b0);
-        auto kt = dv.stats ? k_texels<false, true> : k_texels<false, false>;
-        kt<<<(unsigned)((items + TW_WARPS - 1) / TW_WARPS), TW_WARPS * 32, TX_DYN_SMEM, s>>>(
-            ts, dv, cbins, tiles_x, tiles_x * tiles_y, items, d_fix, b0);
+        int trc = dv.stats ? launch_texels<false, true>(p, s, ts, dv, cbins, tiles_x, tiles_x * tiles_y, items, d_fix, b0)
+                           : launch_texels<false, false>(p, s, ts, dv, cbins, tiles_x, tiles_x * tiles_y, items, d_fix, b0);
+        if (trc) return trc;
         if (ev) CK(cudaEventRecord(ev[3], s));
         auto ks = dv.stats ? k_samples<true> : k_samples<false>;
         ks<<<grid, 256, 0, s>>>(p->d_px, p->d_py, p->d_pz, p->d_chunk, p->d_lvl1, p->d_lorder2, p->d_work + 1, p->N,
@@ -2148,15 +2312,8 @@ static int raster_pass(gm_plan* p, int W, int H, bool attrs) {
     CoarseBins cbins = coarse_bins(p, W, H);
     k_coarse<<<1, 256, 0, s>>>(ts, cbins, p->d_fail, 0);
     const int64_t items = (int64_t)tiles_x * tiles_y;
-    const unsigned grid = (unsigned)((items + TW_WARPS - 1) / TW_WARPS);
-    if (attrs)
-        k_texels<true, false><<<grid, TW_WARPS * 32, TX_DYN_SMEM, s>>>(ts, dv, cbins, tiles_x, tiles_x * tiles_y, items,
-                                                                p->d_fix, 0);
-    else
-        k_texels<false, false><<<grid, TW_WARPS * 32, TX_DYN_SMEM, s>>>(ts, dv, cbins, tiles_x, tiles_x * tiles_y, items,
-                                                                 p->d_fix, 0);
-    CK(cudaGetLastError());
-    return GM_OK;
+    return attrs ? launch_texels<true, false>(p, s, ts, dv, cbins, tiles_x, tiles_x * tiles_y, items, p->d_fix, 0)
+                 : launch_texels<false, false>(p, s, ts, dv, cbins, tiles_x, tiles_x * tiles_y, items, p->d_fix, 0);
 }
 
 // kernels.rasterize for the plan's occluders under fixation `fx` (18 floats):

@@ -1,5 +1,6 @@
 mkdir -p gpurun_out; rm -f gpurun_out/variants.txt
-for v in _gazemap_b200 _v_cb5 _v_cb7; do
+for rep in 1 2; do
+for v in _gazemap_b200 _v_head; do
   GAZEMAP_B200_SO=paper_2601_07571_b200/$v.so timeout 600 python bench.py --steps 3 --warmup 2 --fixations 30720 --no-cpu --no-e2e --no-stats > gpurun_out/bv_$v.log 2>&1
-  echo "$v $(grep -o '"phases_ms": {[^}]*}' gpurun_out/bv_$v.log) $(grep -o '"ms_per_step": [0-9.]*' gpurun_out/bv_$v.log)" >> gpurun_out/variants.txt
-done
+  echo "c2 $v $(grep -o '"texels": [0-9.]*' gpurun_out/bv_$v.log) $(grep -o '"ms_per_step": [0-9.]*' gpurun_out/bv_$v.log)" >> gpurun_out/variants.txt
+done; done
