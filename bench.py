@@ -213,9 +213,13 @@ def run_ours(args, rank, world):
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
-        dist.init_process_group("nccl")
-    device = int(os.environ.get("LOCAL_RANK", 0)) if world > 1 else 0
+        # GM_BENCH_DEVICE_MOD / GM_BENCH_BACKEND let a 1-GPU box exercise the multi-rank
+        # path (ranks sharing a device over gloo); the product run is NCCL, one GPU per rank
+        ndev = int(os.environ.get("GM_BENCH_DEVICE_MOD", "0")) or torch.cuda.device_count()
+        local = int(os.environ.get("LOCAL_RANK", rank)) % max(ndev, 1)
+        torch.cuda.set_device(local)
+        dist.init_process_group(os.environ.get("GM_BENCH_BACKEND", "nccl"))
+    device = local if world > 1 else 0
 
     scene, k, fx, filtering, desc = workload(args.config, args.fixations, rank)
     cfg = gm.GenerationConfig(k=k, filtering_enabled=filtering)
@@ -344,7 +348,7 @@ def run_ours(args, rank, world):
     ach = dom_flops / (times[dom] / 1e3) / 1e12 if times[dom] else None
     # DRAM bytes per launch of the dominant kernel from the committed ncu --set full capture
     # (profiles/r1_ncu_traffic.json, written by tools/ncu_traffic.py), per launch like `achieved`
-    traffic, hbm = None, None
+    traffic, hbm, issue = None, None, None
     tpath = ROOT / "profiles" / "r1_ncu_traffic.json"
     kname = {"k_samples<mark>": "k_mark", "k_samples<accumulate>": "k_samples"}.get(dom, dom)
     if tpath.exists():
@@ -356,8 +360,12 @@ def run_ours(args, rank, world):
             hbm_peak = peaks.get("hbm_gbs", 7700.0)
             hbm = {"achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak,
                    "launch_ms": launch_ms, "fixations_per_launch": tk["fixations_per_launch"]}
+            if "ipc" in tk:  # the bound that does apply: instruction issue (4 warp-instr/cycle/SM)
+                issue = {"ipc": tk["ipc"], "peak_ipc": 4.0, "frac": tk["ipc"] / 4.0,
+                         "issue_slots_busy": tk["issue_pct_of_peak"] / 100.0, "source": "ncu --set full"}
     roof = {"bound": "fp64", "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s",
-            "frac": (ach / fp64_peak) if ach else None, "traffic": traffic, "hbm": hbm, "kernel": dom,
+            "frac": (ach / fp64_peak) if ach else None, "traffic": traffic, "hbm": hbm, "issue": issue,
+            "kernel": dom,
             "kernel_ms_per_step": times[dom], "kernel_share": times[dom] / step_ms,
             "algorithmic_flops_per_step": dom_flops,
             "peak_kind": "nominal FP64 FMA peak at max SM clock (MEASURED_PEAKS.json has no FP64 figure)",

@@ -119,3 +119,24 @@ def test_render_rejects_unnormalized():
     scene, sm, dm, cam, q, fr, _ = _render_setup()
     with pytest.raises(gm.ConfigError):
         gm.render_heatmap(scene, gm.DensityMap(dm.values, 1.0, False), sm, cam, q, fr)
+
+
+def test_host_depth_match_vs_oracle():
+    """is_visible's depth test (C++ host, gm_depth_match) against the oracle's
+    restatement of kernels.depth_match on random buffers with holes and edges."""
+    from oracle import oracle as O
+    from paper_2601_07571_b200 import _native
+
+    rng = np.random.default_rng(5)
+    lib = _native.load()
+    for H, W in ((8, 8), (1, 7), (5, 1), (1, 1), (16, 9)):
+        depth = rng.uniform(1.0, 1.01, (H, W))
+        depth[rng.uniform(size=(H, W)) < 0.15] = np.inf
+        depth[rng.uniform(size=(H, W)) < 0.15] += 0.5
+        depth = np.ascontiguousarray(depth)
+        for _ in range(300):
+            fx, fy = rng.uniform(-1.0, W + 1.0), rng.uniform(-1.0, H + 1.0)
+            d = float(rng.choice([1.0, 1.005, 1.3, 1.5, 2.0]))
+            eps = float(rng.choice([1e-3, 5e-3, 0.2]))
+            got = bool(lib.gm_depth_match(_native.dptr(depth), H, W, fx, fy, d, eps))
+            assert got == O.depth_match(depth, fx, fy, d, eps), (H, W, fx, fy, d, eps)

@@ -16,13 +16,14 @@ import sys
 
 def main(path, batch):
     out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv", "--metrics",
-                          "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum"],
+                          "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,"
+                          "sm__inst_executed.avg.per_cycle_active,sm__inst_issued.avg.pct_of_peak_sustained_active"],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units = rows[0], rows[1]
     ki = hdr.index("Kernel Name")
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ms": 1.0, "us": 1e-3, "ns": 1e-6}
-    acc = collections.defaultdict(lambda: [0, 0.0, 0.0])
+    acc = collections.defaultdict(lambda: [0, 0.0, 0.0, 0.0, 0.0])
     for r in rows[2:]:
         name = r[ki].split("(")[0].replace("void ", "").split("<")[0]
         rd = float(r[hdr.index("dram__bytes_read.sum")]) * scale[units[hdr.index("dram__bytes_read.sum")]]
@@ -32,8 +33,11 @@ def main(path, batch):
         a[0] += 1
         a[1] += rd + wr
         a[2] += t
+        a[3] += float(r[hdr.index("sm__inst_executed.avg.per_cycle_active")])
+        a[4] += float(r[hdr.index("sm__inst_issued.avg.pct_of_peak_sustained_active")])
     res = {k: {"launches": n, "dram_bytes_per_launch": b / n, "ms_per_launch_cold": t / n,
-               "fixations_per_launch": batch} for k, (n, b, t) in acc.items()}
+               "ipc": ipc / n, "issue_pct_of_peak": iss / n, "fixations_per_launch": batch}
+           for k, (n, b, t, ipc, iss) in acc.items()}
     print(json.dumps({"source": path, "how": "ncu --set full --clock-control none (serialised, cold cache)",
                       "kernels": res}, indent=1))
 
