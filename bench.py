@@ -279,8 +279,8 @@ def run_ours(args, rank, world):
     value = world * N * F / (step_ms / 1e3)
     tm = tms[-1]
     # per step: k_set_i64, then per batch k_tri_setup, k_level1, k_fix32, k_mark, k_coarse, k_texels,
-    # k_samples (+ 4 CUB radix-sort kernels ordering the super-chunks); then k_max
-    launches = int(tm.batches) * 7 + 2
+    # k_texels<crowded>, k_samples (+ 4 CUB radix-sort kernels ordering the super-chunks); then k_max
+    launches = int(tm.batches) * 8 + 2
     library_launches = int(tm.batches) * 4
 
     # ---- e2e through the public API (host table in, host values out) -----

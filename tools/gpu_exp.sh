@@ -1,6 +1,6 @@
-mkdir -p gpurun_out
-timeout 600 python bench.py --steps 2 --warmup 2 --fixations 20480 --no-cpu > gpurun_out/bench7.log 2>&1
-GM_BENCH_BACKEND=gloo GM_BENCH_DEVICE_MOD=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29531 bench.py --gpus 2 --steps 2 --warmup 1 --fixations 8192 > gpurun_out/bench7_2rank.log 2>&1
-echo "rc=$?" >> gpurun_out/bench7_2rank.log
-timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29532 bench.py --impl reference --gpus 2 --steps 1 --warmup 1 --cpu-fixations 20 > gpurun_out/bench7_ref2.log 2>&1
-echo "rc=$?" >> gpurun_out/bench7_ref2.log
+mkdir -p gpurun_out; rm -f gpurun_out/variants.txt
+for rep in 1 2; do
+for v in _v_ck1 _gazemap_b200 _v_ck4 _v_ck8; do
+  GAZEMAP_B200_SO=paper_2601_07571_b200/$v.so timeout 600 python bench.py --steps 3 --warmup 2 --fixations 30720 --no-cpu --no-e2e --no-stats > gpurun_out/bv_$v.log 2>&1
+  echo "c2 $v $(grep -o '"phases_ms": {[^}]*}' gpurun_out/bv_$v.log | cut -c1-120) $(grep -o '"ms_per_step": [0-9.]*' gpurun_out/bv_$v.log)" >> gpurun_out/variants.txt
+done; done
