@@ -74,3 +74,26 @@ def test_dynamic_accumulate_fixation_and_plan_restored():
         gm.accumulate_fixation(dm, scene, sm, f, cfg)
     for oid in ids:
         np.testing.assert_allclose(dm.values[oid], dyn.values[oid], rtol=RTOL, atol=0)
+
+
+def test_dynamic_log_roundtrip(tmp_path):
+    """The same dynamic session written as a fixation log (pose-override groups,
+    gaze.py:130-188 schema), parsed by the C++ ingestion, generated on the GPU."""
+    scene, ids = _scene()
+    lines = ["# dynamic session"]
+    for f, row in enumerate(G["fix"]):
+        toks = [repr(float(v)) for v in row]
+        for ff, oi, v in zip(G["spec_f"], G["spec_o"], G["spec_v"]):
+            if ff == f:
+                toks.append(ids[oi] if oi >= 0 else "not_in_scene")
+                toks.extend(repr(float(x)) for x in v)
+        lines.append(" ".join(toks))
+    p = tmp_path / "dyn.log"
+    p.write_text("\n".join(lines) + "\n")
+    fx = gm.parse_fixation_log(p)
+    assert len(fx) == len(G["fix"]) and sum(bool(f.overrides) for f in fx) == len(set(G["spec_f"].tolist()))
+    cfg = gm.GenerationConfig(k=float(G["k"]))
+    sm = gm.build_sampled_meshes(scene, cfg.k)
+    dm = gm.generate(scene, sm, fx, cfg)
+    for i, oid in enumerate(ids):
+        np.testing.assert_allclose(dm.values[oid], G[f"val_on{i}"], rtol=RTOL, atol=0)
