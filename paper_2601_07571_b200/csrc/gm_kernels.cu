@@ -38,9 +38,9 @@
 // launch bounds of the hot kernels; -DTX_MINB=n etc. (build variants) cap
 // their registers for n CTAs per SM
 #ifdef TX_MINB
-#define TX_BOUNDS __launch_bounds__(TW_WARPS * 32, TX_MINB)
+#define TX_BOUNDS __launch_bounds__(TX_MAX_THREADS, TX_MINB)
 #else
-#define TX_BOUNDS __launch_bounds__(TW_WARPS * 32)
+#define TX_BOUNDS __launch_bounds__(TX_MAX_THREADS)
 #endif
 #ifdef KS_MINB
 #define KS_BOUNDS __launch_bounds__(256, KS_MINB)
@@ -900,7 +900,9 @@ __global__ void KS_BOUNDS k_samples(const double* __restrict__ px, const double*
 
 #define TW_CAP 32
 #define TW_SEL 128  // overlapping triangles remembered per tile (more: rescanned per round)
-#define TW_WARPS 4
+#ifndef TW_WARPS
+#define TW_WARPS 4  // warps (independent tile items) per k_texels CTA
+#endif
 struct __align__(16) TexelWarpSmem {
     TriF32 t32[TW_CAP];  // staged, in ascending min-depth order
     int sel[TW_SEL + 32];
@@ -913,11 +915,17 @@ struct __align__(16) CrowdedWarpSmem {
     int sel[TC_SEL];
     float key[TC_SEL];
 };
-#define TC_WARPS 4
+#ifndef TC_WARPS
+#define TC_WARPS 4  // warps per CTA of the crowded pass
+#endif
+#ifndef CROWD_DEPTH
+#define CROWD_DEPTH 10  // ... and whose triangle bboxes cover the tile more than this many times
+#endif
 #ifndef CROWD_MIN
 #define CROWD_MIN 128  // tiles overlapping more triangles than this go to the crowded pass
 #endif
 #define TC_DYN_SMEM (TC_WARPS * (int)sizeof(CrowdedWarpSmem))
+#define TX_MAX_THREADS (32 * (TW_WARPS > TC_WARPS ? TW_WARPS : TC_WARPS))
 
 // position of the k-th (0-based) set bit of w (k < popc(w))
 __device__ __forceinline__ int kth_set_bit(uint32_t w, int k) {
@@ -1003,6 +1011,7 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
     unsigned long long c_pairs = 0, c_cov = 0, c_iter = 0, c_edge = 0;
 
     // 1. triangles overlapping the tile -> S.sel (scan cursor resumes if > TW_SEL)
+    int cover = 0;  // this lane's share of the selected bboxes' area inside the tile (depth complexity)
     auto gather = [&](int& cursor) {
         int cnt = 0;
         while (cursor < n && cnt < TW_SEL) {
@@ -1013,6 +1022,7 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
                 const uint2 bbx = segb[i];
                 const int x0 = bbx.x & 0xffff, x1 = bbx.x >> 16, y0 = bbx.y & 0xffff, y1 = bbx.y >> 16;
                 sel = !(x1 < xb || x0 > xe || y1 < yb || y0 > ye);
+                if (sel) cover += (min(x1, xe) - max(x0, xb) + 1) * (min(y1, ye) - max(y0, yb) + 1);
             }
             const unsigned bal = __ballot_sync(FULL, sel);
             if (sel) SEL[cnt + __popc(bal & ((1u << lane) - 1u))] = i;
@@ -1170,7 +1180,11 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
     if (!CROWDED) {
         int nsel = gather(cursor);
         if (STATS) nsel_total = nsel;
-        if ((cursor < n || nsel > CROWD_MIN) && dv.crowd) {
+        // deep tiles (overlapping surfaces: the selected bboxes cover the tile more than
+        // CROWD_DEPTH times) profit from the sorted crowded pass; wide ones (many
+        // side-by-side triangles) stay here
+        if ((cursor < n || nsel > CROWD_MIN) && dv.crowd &&
+            __reduce_add_sync(FULL, (unsigned)cover) > (unsigned)(CROWD_DEPTH * TW * TH)) {
             // more than TW_CAP triangles: k_texels<CROWDED> sorts the whole list (deferred)
             if (lane == 0) dv.crowd[atomicAdd(dv.crowd_count, 1)] = (int)item;
             return;
@@ -1827,7 +1841,7 @@ static int launch_texels(gm_plan* p, cudaStream_t s, const TriStore& ts, DepthVi
     CK(cudaMemsetAsync(p->d_crowd_count, 0, 2 * sizeof(int), s));
     k_texels<ATTRS, STATS, false><<<(unsigned)((items + TW_WARPS - 1) / TW_WARPS), TW_WARPS * 32, TX_DYN_SMEM, s>>>(
         ts, dv, cb, tiles_x, tiles_per_fix, items, fix, b0);
-    k_texels<ATTRS, STATS, true><<<p->sms * 5, TC_WARPS * 32, TC_DYN_SMEM, s>>>(ts, dv, cb, tiles_x, tiles_per_fix,
+    k_texels<ATTRS, STATS, true><<<p->sms * (20 / TC_WARPS), TC_WARPS * 32, TC_DYN_SMEM, s>>>(ts, dv, cb, tiles_x, tiles_per_fix,
                                                                               items, fix, b0);
     CK(cudaGetLastError());
     return GM_OK;
