@@ -901,7 +901,7 @@ __global__ void KS_BOUNDS k_samples(const double* __restrict__ px, const double*
 #define TW_CAP 32
 #define TW_SEL 128  // overlapping triangles remembered per tile (more: rescanned per round)
 #ifndef TW_WARPS
-#define TW_WARPS 4  // warps (independent tile items) per k_texels CTA
+#define TW_WARPS 2  // warps (independent tile items) per k_texels CTA
 #endif
 struct __align__(16) TexelWarpSmem {
     TriF32 t32[TW_CAP];  // staged, in ascending min-depth order
