@@ -35,6 +35,9 @@
 #include "gm_types.h"
 
 #define GM_MAX_BATCH 1024
+#ifndef SAMPLE_GRID_MULT
+#define SAMPLE_GRID_MULT 1  // persistent sample-pass grid = resident CTAs x this
+#endif
 // launch bounds of the hot kernels; -DTX_MINB=n etc. (build variants) cap
 // their registers for n CTAs per SM
 #ifdef TX_MINB
@@ -1871,7 +1874,12 @@ static int enqueue_batch(gm_plan* p, const GmFixExact* d_fix, const GmFixCull* d
     }
     if (ev) CK(cudaEventRecord(ev[1], s));
     if (p->n_chunks > 0 && accumulate) {
-        const int grid = p->sms * 8;  // persistent: 8 CTAs x 8 warps per SM
+        // persistent sample passes: exactly the resident CTAs (work is claimed dynamically;
+        // a second wave would only start late and idle)
+        int occ_m = 0, occ_s = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_m, k_mark, 256, 0));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, dv.stats ? k_samples<true> : k_samples<false>, 256, 0));
+        const int grid_m = p->sms * std::max(occ_m, 1) * SAMPLE_GRID_MULT, grid_s = p->sms * std::max(occ_s, 1) * SAMPLE_GRID_MULT;
         CK(cudaMemsetAsync(p->d_mask, 0, sizeof(uint32_t) * (size_t)nb * H * wwords, s));
         CK(cudaMemsetAsync(p->d_work, 0, 2 * sizeof(int), s));
         k_level1<<<blocks_for(p->n_supers, 8), 256, 0, s>>>(p->d_super, p->n_supers, d_cull, nb, p->d_lvl1,
@@ -1880,7 +1888,7 @@ static int enqueue_batch(gm_plan* p, const GmFixExact* d_fix, const GmFixCull* d
         CK(cub::DeviceRadixSort::SortPairsDescending(p->d_sort_tmp, tb, p->d_lcount, p->d_lcount2, p->d_lorder,
                                                      p->d_lorder2, (int)p->n_supers, 0, 11, s));
         k_fix32<<<blocks_for(nb, 128), 128, 0, s>>>(d_fix, nb, p->pmax, 1.0 / inv_sigma, p->d_fix32);
-        k_mark<<<grid, 256, 0, s>>>(p->d_pxf, p->d_pyf, p->d_pzf, p->d_px, p->d_py, p->d_pz, p->d_chunk, p->d_lvl1,
+        k_mark<<<grid_m, 256, 0, s>>>(p->d_pxf, p->d_pyf, p->d_pzf, p->d_px, p->d_py, p->d_pz, p->d_chunk, p->d_lvl1,
                                     p->d_lorder2, p->d_work, p->N, p->n_chunks, p->n_supers, d_fix, p->d_fix32,
                                     d_cull, nb, dv, inv_sigma, p->d_cbits, p->d_fail, b0);
         if (ev) CK(cudaEventRecord(ev[2], s));
@@ -1892,7 +1900,7 @@ static int enqueue_batch(gm_plan* p, const GmFixExact* d_fix, const GmFixCull* d
         if (trc) return trc;
         if (ev) CK(cudaEventRecord(ev[3], s));
         auto ks = dv.stats ? k_samples<true> : k_samples<false>;
-        ks<<<grid, 256, 0, s>>>(p->d_px, p->d_py, p->d_pz, p->d_chunk, p->d_lvl1, p->d_lorder2, p->d_work + 1, p->N,
+        ks<<<grid_s, 256, 0, s>>>(p->d_px, p->d_py, p->d_pz, p->d_chunk, p->d_lvl1, p->d_lorder2, p->d_work + 1, p->N,
                                 p->n_chunks, p->n_supers, d_fix, d_cull, nb, dv, inv_sigma, cfg->eps_abs,
                                 cfg->eps_rel, p->d_values, p->d_cbits, p->d_fail, b0);
     } else if (ev) {

@@ -1,5 +1,5 @@
 mkdir -p gpurun_out; rm -f gpurun_out/variants.txt
-for v in _gazemap_b200 _v_tc1 _v_tc2 _v_tw1 _v_tw2; do
+for v in _v_head _gazemap_b200 _v_g2 _v_head _gazemap_b200; do
   GAZEMAP_B200_SO=paper_2601_07571_b200/$v.so timeout 600 python bench.py --steps 2 --warmup 2 --fixations 30720 --no-cpu --no-e2e --no-stats > gpurun_out/bv_$v.log 2>&1
   echo "c2 $v $(grep -o '"texels": [0-9.]*' gpurun_out/bv_$v.log) $(grep -o '"ms_per_step": [0-9.]*' gpurun_out/bv_$v.log)" >> gpurun_out/variants.txt
   GAZEMAP_B200_SO=paper_2601_07571_b200/$v.so timeout 600 python bench.py --config c2off --steps 2 --warmup 2 --fixations 30720 --no-cpu --no-e2e --no-stats > gpurun_out/bvo_$v.log 2>&1
