@@ -53,6 +53,16 @@ def parse():
     return ap.parse_args()
 
 
+def shard_of(name: str, fx: np.ndarray, rank: int, world: int):
+    """(this rank's fixations, total fixations of the job, scaling mode)."""
+    if name == "c4":
+        from paper_2601_07571_b200.sharding import shard_range
+
+        a, b = shard_range(len(fx), rank, world)
+        return np.ascontiguousarray(fx[a:b]), len(fx), "strong"
+    return fx, len(fx) * world, "weak"
+
+
 def workload(name: str, n_fix: int, rank: int):
     import workloads as W
 
@@ -69,6 +79,8 @@ def workload(name: str, n_fix: int, rank: int):
         k = 1000.0 * int(name[3:])
         fx = W.room_fixations(n_fix or 10_000, seed=1 + 1000 * rank, scene=scene)
     elif name == "c4":
+        # strong scaling: one 50 x 20k session stream, each rank its contiguous shard
+        # (sharded by the caller, see shard_of)
         scene = W.room_scene()
         k = 10_000.0
         fx = W.session_fixations(scene=scene)
@@ -221,7 +233,8 @@ def run_ours(args, rank, world):
         dist.init_process_group(os.environ.get("GM_BENCH_BACKEND", "nccl"))
     device = local if world > 1 else 0
 
-    scene, k, fx, filtering, desc = workload(args.config, args.fixations, rank)
+    scene, k, fx_all, filtering, desc = workload(args.config, args.fixations, rank)
+    fx, total_F, scaling = shard_of(args.config, fx_all, rank, world)
     cfg = gm.GenerationConfig(k=k, filtering_enabled=filtering)
     sampled = gm.build_sampled_meshes(scene, k, device=device)
     plan = gm.ScenePlan(scene, sampled, scene.object_ids, device=device)
@@ -276,7 +289,7 @@ def run_ours(args, rank, world):
         tt = torch.tensor([step_ms], device=f"cuda:{device}", dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         step_ms = float(tt.item())
-    value = world * N * F / (step_ms / 1e3)
+    value = N * total_F / (step_ms / 1e3)
     tm = tms[-1]
     # per step: k_set_i64, then per batch k_tri_setup, k_level1, k_fix32, k_mark, k_coarse, k_texels,
     # k_texels<crowded>, k_samples (+ 4 CUB radix-sort kernels ordering the super-chunks); then k_max
@@ -293,7 +306,8 @@ def run_ours(args, rank, world):
         if world > 1:
             from paper_2601_07571_b200.sharding import generate_sharded
 
-            full = np.concatenate([workload(args.config, args.fixations, r)[2] for r in range(world)])
+            full = fx_all if scaling == "strong" else np.concatenate(
+                [workload(args.config, args.fixations, r)[2] for r in range(world)])
 
             def e2e_call():
                 return generate_sharded(scene, sampled, full, cfg, device=device)
@@ -315,7 +329,7 @@ def run_ours(args, rank, world):
             tt = torch.tensor([e_t], device=f"cuda:{device}", dtype=torch.float64)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             e_t = float(tt.item())
-        e2e = {"value": world * N * F / e_t, "unit": UNIT, "h2d_bytes_per_step": int(F * (208 + 80)),
+        e2e = {"value": N * total_F / e_t, "unit": UNIT, "h2d_bytes_per_step": int(F * (208 + 80)),
                "d2h_bytes_per_step": int(N * 8), "ms_per_step": e_t * 1e3,
                "path": "paper_2601_07571_b200.generate (fixation table in host memory -> values dict)"
                if world == 1 else "paper_2601_07571_b200.sharding.generate_sharded (NCCL all-reduce)",
@@ -383,10 +397,11 @@ def run_ours(args, rank, world):
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": desc, "samples": int(N), "triangles": int(plan._lib.gm_plan_num_triangles(plan._h)),
-                       "fixations_per_gpu": int(F), "zbuffer": cfg.zbuffer_resolution, "filtering": filtering,
+                       "fixations_per_gpu": int(F), "fixations_total": int(total_F),
+                       "zbuffer": cfg.zbuffer_resolution, "filtering": filtering,
                        "parallelism": f"fixation-sharded x{world}, NCCL sum all-reduce" if world > 1 else "single GPU",
                        "l2": "flushed (512 MiB write) before every timed step",
                        "timing": "CUDA events on the plan stream around each full generation (+ all-reduce)"},

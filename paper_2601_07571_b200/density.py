@@ -266,11 +266,12 @@ class ScenePlan:
         _native.check(self._lib.gm_plan_sync(self._h), "gm_plan_sync")
 
     def split(self, flat: np.ndarray, sampled_meshes: dict) -> dict:
+        """Per-object values: disjoint views of `flat` (a fresh buffer per call), no copy."""
         out = {}
         for oid, sm in sampled_meshes.items():
             if oid in self.slices:
                 a, b = self.slices[oid]
-                out[oid] = flat[a:b].copy()
+                out[oid] = flat[a:b]
             else:
                 out[oid] = np.zeros(sm.total_samples)
         return out
