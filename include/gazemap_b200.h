@@ -46,7 +46,7 @@ typedef struct GmConfig {
     int32_t zbuffer_resolution; /* square z-buffer side, 1..65535 */
     int32_t filtering;          /* 1: 4-sigma crop frustum, 0: full frustum */
     int32_t batch;              /* fixations per GPU batch, 0 = auto */
-    int32_t flags;              /* reserved, 0 */
+    int32_t flags;              /* 0, or GM_FLAG_* below */
 } GmConfig;
 
 /* Timings.phases (density.py:94-103), measured with CUDA events. */
@@ -63,6 +63,11 @@ typedef struct GmTimings {
     int64_t batches;
     int64_t retries;      /* passes resumed after a screen-triangle segment overflow */
 } GmTimings;
+
+/* GmConfig.flags */
+#define GM_FLAG_STATS 1       /* count work (gm_plan_stats); untimed diagnostics */
+#define GM_FLAG_ONE_STREAM 2  /* batches on one stream (default for > 400k occluder triangles) */
+#define GM_FLAG_TWO_STREAMS 4 /* overlap consecutive batches on two streams (default otherwise) */
 
 typedef struct gm_plan gm_plan;
 typedef void (*gm_progress_fn)(int64_t done, int64_t total, void* user);

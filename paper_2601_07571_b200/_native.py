@@ -48,6 +48,8 @@ FIX_EXACT_DOUBLES = 26
 FIX_CULL_FLOATS = 20
 
 GM_FLAG_STATS = 1
+GM_FLAG_ONE_STREAM = 2
+GM_FLAG_TWO_STREAMS = 4
 STAT_NAMES = ["l1_tests", "l2_tests", "exact_evals", "ndc_candidates", "cone_candidates", "visible",
               "texels", "texel_pairs", "covered_pairs", "reserved9", "tx_tiles", "tx_staged", "tx_list", "tx_iter",
               "tx_edge"]

@@ -496,6 +496,11 @@ enum {
     GM_STAT_N = 16
 };
 #define GM_FLAG_STATS 1
+#define GM_FLAG_ONE_STREAM 2   // force batches onto one stream/buffer set
+#define GM_FLAG_TWO_STREAMS 4  // force the two-stream batch pipeline
+#ifndef GM_OVERLAP_MAX_TRIS
+#define GM_OVERLAP_MAX_TRIS 400000  // default: overlap batches for scenes up to this many occluders
+#endif
 #define GM_STAT_STRIPES 128  // counter copies (summed by gm_plan_stats): keeps the stats pass free of atomic hot spots
 
 // Warp-aggregated add of a per-lane count to stripe (block % GM_STAT_STRIPES)
@@ -1451,6 +1456,27 @@ static int dev_alloc(T** p, size_t n) {
 
 #define GM_RING 3  // pinned host setup slots in flight
 
+// Everything one batch of fixations owns on the device.  A plan holds two sets
+// (the plan's own fields and `alt`); consecutive batches alternate between them
+// and between two streams, so batch i + 1's occluder setup, marking and texel
+// kernels overlap batch i's tail.  Only the accumulation pass (k_samples) is
+// chained across batches (event), which keeps the per-sample log order.
+#define GM_BATCH_FIELDS(X)                                                                            \
+    X(cudaStream_t, stream) X(uint32_t*, d_lvl1) X(uint32_t*, d_cbits) X(int64_t, cap_cbits)           \
+    X(int*, d_lcount) X(int*, d_lorder) X(int*, d_lcount2) X(int*, d_lorder2) X(int64_t, cap_sort)     \
+    X(int*, d_work) X(void*, d_sort_tmp) X(size_t, sort_tmp_bytes) X(int64_t, cap_lvl1) X(int, cap_B)  \
+    X(GmFixExact*, d_fix) X(GmFixCull*, d_cull) X(GmFixF32*, d_fix32) X(GmScreenTri*, d_tris)          \
+    X(TriF32*, d_t32) X(uint2*, d_bbox) X(int*, d_count) X(int64_t, cap_seg) X(int64_t, cap_seg_B)     \
+    X(double*, d_depth) X(float*, d_vbuf) X(uint32_t*, d_mask) X(int64_t, cap_depth) X(int64_t, cap_mask) \
+    X(int*, d_citems) X(int*, d_coff) X(int*, d_covf) X(int64_t, cap_citems) X(int64_t, cap_cB)         \
+    X(int*, d_crowd) X(int*, d_crowd_count) X(int64_t, cap_crowd)
+
+struct BatchBufs {
+#define GM_X(T, n) T n{};
+    GM_BATCH_FIELDS(GM_X)
+#undef GM_X
+};
+
 struct gm_plan {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -1527,7 +1553,26 @@ struct gm_plan {
     int* d_crowd_count = nullptr;  // [2]
     int64_t cap_crowd = 0;
     int64_t cap_key = 0;
+    int64_t cap_cbits = 0, cap_sort = 0;  // (per batch-buffer set, swapped with alt)
+    int cap_ring = 0;
+    BatchBufs alt;                   // the second batch-buffer set (and stream)
+    cudaEvent_t ev_order = nullptr;  // last accumulation pass enqueued (chains k_samples across streams)
 };
+
+// Exchange the plan's batch buffers (and stream) with the alternate set.
+static void swap_batch_bufs(gm_plan* p) {
+#define GM_X(T, n) std::swap(p->n, p->alt.n);
+    GM_BATCH_FIELDS(GM_X)
+#undef GM_X
+}
+
+// Free one set's scene-sized batch buffers (sizes depend on n_supers / n_chunks).
+static void free_scene_batch_bufs(gm_plan* p) {
+    cudaFree(p->d_lvl1); cudaFree(p->d_cbits); cudaFree(p->d_lcount); cudaFree(p->d_lorder);
+    cudaFree(p->d_lcount2); cudaFree(p->d_lorder2); cudaFree(p->d_sort_tmp);
+    p->d_lvl1 = nullptr; p->d_cbits = nullptr; p->d_lcount = p->d_lorder = p->d_lcount2 = p->d_lorder2 = nullptr;
+    p->d_sort_tmp = nullptr; p->sort_tmp_bytes = 0; p->cap_lvl1 = 0; p->cap_cbits = 0; p->cap_sort = 0;
+}
 
 static void plan_free_scene(gm_plan* p) {
     cudaFree(p->d_tw); cudaFree(p->d_tsph); cudaFree(p->d_csph);
@@ -1535,10 +1580,10 @@ static void plan_free_scene(gm_plan* p) {
     cudaFree(p->d_pxf); cudaFree(p->d_pyf); cudaFree(p->d_pzf);
     p->d_pxf = p->d_pyf = p->d_pzf = nullptr;
     cudaFree(p->d_chunk); cudaFree(p->d_values); cudaFree(p->d_super);
-    cudaFree(p->d_lvl1); cudaFree(p->d_cbits); cudaFree(p->d_lcount); cudaFree(p->d_lorder); cudaFree(p->d_lcount2);
-    cudaFree(p->d_lorder2); cudaFree(p->d_sort_tmp);
-    p->d_lvl1 = nullptr; p->d_cbits = nullptr; p->d_lcount = p->d_lorder = p->d_lcount2 = p->d_lorder2 = nullptr;
-    p->d_sort_tmp = nullptr; p->sort_tmp_bytes = 0; p->cap_lvl1 = 0;
+    free_scene_batch_bufs(p);
+    swap_batch_bufs(p);
+    free_scene_batch_bufs(p);
+    swap_batch_bufs(p);
     p->d_tw = nullptr; p->d_tsph = p->d_csph = p->d_chunk = p->d_super = nullptr;
     p->d_px = p->d_py = p->d_pz = p->d_values = nullptr;
     p->T = p->n_clu = p->N = p->n_chunks = p->n_supers = 0;
@@ -1573,6 +1618,7 @@ extern "C" int gm_plan_create(int device, gm_plan** out) {
     CK(cudaMalloc(&p->d_maxcount, sizeof(int)));
     CK(cudaMalloc(&p->d_ntris, sizeof(unsigned long long)));
     CK(cudaMalloc(&p->d_work, 2 * sizeof(int)));
+    CK(cudaEventCreateWithFlags(&p->ev_order, cudaEventDisableTiming));
     for (int r = 0; r < GM_RING; r++) CK(cudaEventCreateWithFlags(&p->h_ev[r], cudaEventDisableTiming));
     unsigned hc = std::thread::hardware_concurrency();
     p->host_threads = hc > 0 ? (int)hc : 8;
@@ -1580,22 +1626,36 @@ extern "C" int gm_plan_create(int device, gm_plan** out) {
     return GM_OK;
 }
 
+// Free one batch-buffer set (the plan's own fields) and its stream.
+static void free_batch_set(gm_plan* p) {
+    if (p->stream) cudaStreamSynchronize(p->stream);
+    free_scene_batch_bufs(p);
+    cudaFree(p->d_fix); cudaFree(p->d_cull); cudaFree(p->d_fix32); cudaFree(p->d_work);
+    cudaFree(p->d_tris); cudaFree(p->d_t32); cudaFree(p->d_bbox); cudaFree(p->d_count);
+    cudaFree(p->d_depth); cudaFree(p->d_mask); cudaFree(p->d_vbuf);
+    cudaFree(p->d_citems); cudaFree(p->d_coff); cudaFree(p->d_covf);
+    cudaFree(p->d_crowd); cudaFree(p->d_crowd_count);
+    if (p->stream) cudaStreamDestroy(p->stream);
+    p->stream = nullptr;
+}
+
 extern "C" void gm_plan_destroy(gm_plan* p) {
     if (!p) return;
     cudaSetDevice(p->device);
     cudaStreamSynchronize(p->stream);
+    if (p->alt.stream) cudaStreamSynchronize(p->alt.stream);
     plan_free_scene(p);
-    cudaFree(p->d_fix); cudaFree(p->d_cull); cudaFree(p->d_fix32);
     for (int r = 0; r < GM_RING; r++) {
         cudaFreeHost(p->h_fix[r]); cudaFreeHost(p->h_cull[r]); cudaEventDestroy(p->h_ev[r]);
     }
-    cudaFree(p->d_tris); cudaFree(p->d_t32); cudaFree(p->d_bbox); cudaFree(p->d_count); cudaFree(p->d_fail); cudaFree(p->d_maxcount); cudaFree(p->d_ntris); cudaFree(p->d_work);
+    cudaFree(p->d_fail); cudaFree(p->d_maxcount); cudaFree(p->d_ntris);
     cudaFree(p->d_scan_tmp); cudaFree(p->d_max); cudaFree(p->d_stats);
     cudaFree(p->d_fix_all); cudaFree(p->d_cull_all); cudaFree(p->d_flush);
-    cudaFree(p->d_depth); cudaFree(p->d_mask); cudaFree(p->d_vbuf);
-    cudaFree(p->d_citems); cudaFree(p->d_coff); cudaFree(p->d_covf); cudaFree(p->d_key);
-    cudaFree(p->d_crowd); cudaFree(p->d_crowd_count);
-    cudaStreamDestroy(p->stream);
+    cudaFree(p->d_key);
+    if (p->ev_order) cudaEventDestroy(p->ev_order);
+    free_batch_set(p);
+    swap_batch_bufs(p);
+    free_batch_set(p);
     delete p;
 }
 
@@ -1660,18 +1720,6 @@ extern "C" int gm_plan_set_scene(gm_plan* p, int n_obj, const int64_t* tri_count
     if ((rc = dev_alloc(&p->d_pzf, (size_t)N))) return rc;
     if ((rc = dev_alloc(&p->d_chunk, (size_t)p->n_chunks))) return rc;
     if ((rc = dev_alloc(&p->d_super, (size_t)p->n_supers))) return rc;
-    if ((rc = dev_alloc(&p->d_lcount, (size_t)p->n_supers))) return rc;
-    if ((rc = dev_alloc(&p->d_lorder, (size_t)p->n_supers))) return rc;
-    if ((rc = dev_alloc(&p->d_lcount2, (size_t)p->n_supers))) return rc;
-    if ((rc = dev_alloc(&p->d_lorder2, (size_t)p->n_supers))) return rc;
-    if ((rc = dev_alloc(&p->d_cbits, (size_t)std::max<int64_t>(p->n_chunks, 1) * 32))) return rc;
-    {
-        size_t tb = 0;
-        cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, p->d_lcount, p->d_lcount2, p->d_lorder,
-                                                  p->d_lorder2, (int)std::max<int64_t>(p->n_supers, 1), 0, 11);
-        if ((rc = dev_alloc((char**)&p->d_sort_tmp, tb + 16))) return rc;
-        p->sort_tmp_bytes = tb + 16;
-    }
     if ((rc = dev_alloc(&p->d_values, (size_t)N))) return rc;
     p->n_obj = n_obj;
     p->tstart = tstart;
@@ -1766,20 +1814,35 @@ extern "C" int64_t gm_plan_num_samples(gm_plan* p) { return p ? p->N : -1; }
 extern "C" int64_t gm_plan_num_triangles(gm_plan* p) { return p ? p->T : -1; }
 extern "C" double* gm_plan_values_device(gm_plan* p) { return p ? p->d_values : nullptr; }
 
-static int ensure_batch(gm_plan* p, int B, int W, int H, int64_t seg) {
+static int ensure_batch_set(gm_plan* p, int B, int W, int H, int64_t seg) {
     int rc;
+    if (!p->stream) {
+        cudaError_t e = cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking);
+        if (e != cudaSuccess) return set_err(GM_ERR_CUDA, cudaGetErrorString(e));
+    }
+    if (!p->d_work && (rc = dev_alloc(&p->d_work, 2))) return rc;
     if (B > p->cap_B) {
         if ((rc = dev_alloc(&p->d_fix, (size_t)B))) return rc;
         if ((rc = dev_alloc(&p->d_cull, (size_t)B))) return rc;
         if ((rc = dev_alloc(&p->d_count, (size_t)B))) return rc;
         if ((rc = dev_alloc(&p->d_fix32, (size_t)B))) return rc;
-        for (int r = 0; r < GM_RING; r++) {
-            cudaFreeHost(p->h_fix[r]);
-            cudaFreeHost(p->h_cull[r]);
-            CK(cudaMallocHost(&p->h_fix[r], sizeof(GmFixExact) * B));
-            CK(cudaMallocHost(&p->h_cull[r], sizeof(GmFixCull) * B));
-        }
         p->cap_B = B;
+    }
+    if (p->n_supers > p->cap_sort) {
+        if ((rc = dev_alloc(&p->d_lcount, (size_t)p->n_supers))) return rc;
+        if ((rc = dev_alloc(&p->d_lorder, (size_t)p->n_supers))) return rc;
+        if ((rc = dev_alloc(&p->d_lcount2, (size_t)p->n_supers))) return rc;
+        if ((rc = dev_alloc(&p->d_lorder2, (size_t)p->n_supers))) return rc;
+        size_t tb = 0;
+        cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, p->d_lcount, p->d_lcount2, p->d_lorder,
+                                                  p->d_lorder2, (int)std::max<int64_t>(p->n_supers, 1), 0, 11);
+        if ((rc = dev_alloc((char**)&p->d_sort_tmp, tb + 16))) return rc;
+        p->sort_tmp_bytes = tb + 16;
+        p->cap_sort = p->n_supers;
+    }
+    if (p->n_chunks * 32 > p->cap_cbits) {
+        if ((rc = dev_alloc(&p->d_cbits, (size_t)p->n_chunks * 32))) return rc;
+        p->cap_cbits = p->n_chunks * 32;
     }
     if (seg > p->cap_seg || (int64_t)B * seg > p->cap_seg_B) {
         int64_t cs = std::max(seg, p->cap_seg);
@@ -1820,6 +1883,27 @@ static int ensure_batch(gm_plan* p, int B, int W, int H, int64_t seg) {
         p->cap_lvl1 = lw;
     }
     return GM_OK;
+}
+
+// Both batch-buffer sets (the alternate one only when `both`), plus the pinned
+// host ring that feeds either.
+static int ensure_batch(gm_plan* p, int B, int W, int H, int64_t seg, bool both = false) {
+    int rc;
+    if (B > p->cap_ring) {
+        for (int r = 0; r < GM_RING; r++) {
+            cudaFreeHost(p->h_fix[r]);
+            cudaFreeHost(p->h_cull[r]);
+            CK(cudaMallocHost(&p->h_fix[r], sizeof(GmFixExact) * B));
+            CK(cudaMallocHost(&p->h_cull[r], sizeof(GmFixCull) * B));
+        }
+        p->cap_ring = B;
+    }
+    if ((rc = ensure_batch_set(p, B, W, H, seg))) return rc;
+    if (!both) return GM_OK;
+    swap_batch_bufs(p);
+    rc = ensure_batch_set(p, B, W, H, std::max(seg, p->alt.cap_seg));
+    swap_batch_bufs(p);
+    return rc;
 }
 
 typedef void (*gm_progress_fn)(int64_t done, int64_t total, void* user);
@@ -1899,10 +1983,13 @@ static int enqueue_batch(gm_plan* p, const GmFixExact* d_fix, const GmFixCull* d
                            : launch_texels<false, false>(p, s, ts, dv, cbins, tiles_x, tiles_x * tiles_y, items, d_fix, b0);
         if (trc) return trc;
         if (ev) CK(cudaEventRecord(ev[3], s));
+        // accumulation passes run in batch order across the two streams (log order per sample)
+        CK(cudaStreamWaitEvent(s, p->ev_order, 0));
         auto ks = dv.stats ? k_samples<true> : k_samples<false>;
         ks<<<grid_s, 256, 0, s>>>(p->d_px, p->d_py, p->d_pz, p->d_chunk, p->d_lvl1, p->d_lorder2, p->d_work + 1, p->N,
                                 p->n_chunks, p->n_supers, d_fix, d_cull, nb, dv, inv_sigma, cfg->eps_abs,
                                 cfg->eps_rel, p->d_values, p->d_cbits, p->d_fail, b0);
+        CK(cudaEventRecord(p->ev_order, s));
     } else if (ev) {
         CK(cudaEventRecord(ev[2], s));
         CK(cudaEventRecord(ev[3], s));
@@ -1937,9 +2024,29 @@ static int run_batches(gm_plan* p, const double* fx, int64_t F, const GmConfig* 
     B = std::max(B, 1);
     GmSetupConsts consts;
     gm_setup_consts(cfg->theta, cfg->filtering, W, H, &consts);
-    int rc = ensure_batch(p, B, W, H, std::max<int64_t>(p->cap_seg, 16384));
+    // two-stream batch overlap fills kernel tails on scenes with light batches (C2:
+    // -14%); on very large scenes every kernel already fills the GPU and concurrent
+    // batches only thrash L2 (C5: +14%), so they run on one stream
+    const bool two = (cfg->flags & GM_FLAG_TWO_STREAMS) ||
+                     (!(cfg->flags & GM_FLAG_ONE_STREAM) && p->T <= GM_OVERLAP_MAX_TRIS);
+    int rc = ensure_batch(p, B, W, H, std::max<int64_t>(p->cap_seg, 16384), two);
     if (rc) return rc;
-    cudaStream_t s = p->stream;
+    cudaStream_t s = p->stream;          // primary stream (even batches)
+    cudaStream_t s2 = p->alt.stream;     // odd batches
+    cudaEvent_t ev_fork = nullptr;
+    CK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+    auto fork = [&]() -> int {  // everything enqueued on s so far precedes what s2 runs next
+        if (!two) return GM_OK;
+        CK(cudaEventRecord(ev_fork, s));
+        CK(cudaStreamWaitEvent(s2, ev_fork, 0));
+        return GM_OK;
+    };
+    auto join = [&]() -> int {  // s waits for everything enqueued on s2
+        if (!two) return GM_OK;
+        CK(cudaEventRecord(ev_fork, s2));
+        CK(cudaStreamWaitEvent(s, ev_fork, 0));
+        return GM_OK;
+    };
     cudaEvent_t ev_start = nullptr, ev_end = nullptr;
     std::vector<cudaEvent_t> evs;
     auto cleanup = [&]() {
@@ -1947,7 +2054,8 @@ static int run_batches(gm_plan* p, const double* fx, int64_t F, const GmConfig* 
         evs.clear();
         if (ev_start) cudaEventDestroy(ev_start);
         if (ev_end) cudaEventDestroy(ev_end);
-        ev_start = ev_end = nullptr;
+        if (ev_fork) cudaEventDestroy(ev_fork);
+        ev_start = ev_end = ev_fork = nullptr;
     };
     if (device_ms) {
         CK(cudaEventCreate(&ev_start));
@@ -1966,9 +2074,22 @@ static int run_batches(gm_plan* p, const double* fx, int64_t F, const GmConfig* 
         k_set_i64<<<1, 1, 0, s>>>(p->d_fail, LLONG_MAX);
         CK(cudaMemsetAsync(p->d_maxcount, 0, sizeof(int), s));
         CK(cudaMemsetAsync(p->d_ntris, 0, sizeof(unsigned long long), s));
+        CK(cudaEventRecord(p->ev_order, s));  // the first accumulation pass follows the resets
+        if ((rc = fork())) return rc;
         int slot = 0;
-        for (int64_t b0 = start; b0 < F; b0 += B) {
+        int parity = 0;
+        for (int64_t b0 = start; b0 < F; b0 += B, parity ^= (two ? 1 : 0)) {
             int nb = (int)std::min<int64_t>(B, F - b0);
+            // odd batches run on the alternate buffer set and stream
+            struct SwapGuard {
+                gm_plan* p;
+                bool on;
+                ~SwapGuard() {
+                    if (on) swap_batch_bufs(p);
+                }
+            } guard{p, parity == 1};
+            if (parity) swap_batch_bufs(p);
+            cudaStream_t s = p->stream;
             const GmFixExact* d_fix = p->d_fix;
             const GmFixCull* d_cull = p->d_cull;
             if (prepared) {
@@ -2013,6 +2134,7 @@ static int run_batches(gm_plan* p, const double* fx, int64_t F, const GmConfig* 
                 if (failed == LLONG_MAX) progress(b0 + nb, F, user);
             }
         }
+        if ((rc = join())) return rc;
         long long failed = LLONG_MAX;
         int maxcount = 0;
         unsigned long long ntris = 0;
@@ -2025,7 +2147,8 @@ static int run_batches(gm_plan* p, const double* fx, int64_t F, const GmConfig* 
         // grow the per-fixation segments and resume at the first failed batch
         int64_t want = std::max<int64_t>(2 * p->cap_seg, (int64_t)maxcount + maxcount / 4 + 64);
         p->cap_seg = 0;
-        rc = ensure_batch(p, B, W, H, want);
+        p->alt.cap_seg = 0;
+        rc = ensure_batch(p, B, W, H, want, two);
         if (rc) {
             cleanup();
             return rc;

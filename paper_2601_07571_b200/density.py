@@ -163,12 +163,14 @@ class ScenePlan:
 
     # ----------------------------------------------------------------- ops
     def accumulate(self, fixations, config: GenerationConfig, reset: bool = True, progress=None,
-                   timers: Timings | None = None, batch: int = 0) -> None:
-        """Add the fixations' contributions to the device values."""
+                   timers: Timings | None = None, batch: int = 0, flags: int = 0) -> None:
+        """Add the fixations' contributions to the device values (`flags`:
+        GmConfig.flags, e.g. _native.GM_FLAG_ONE_STREAM)."""
         table = fixation_table(fixations)
         F = len(table)
         cfg = _native.GmConfig(float(config.theta), float(config.epsilon_abs), float(config.epsilon_rel),
-                               int(config.zbuffer_resolution), int(bool(config.filtering_enabled)), int(batch), 0)
+                               int(config.zbuffer_resolution), int(bool(config.filtering_enabled)), int(batch),
+                               int(flags))
         tm = _native.GmTimings()
         bad = np.zeros(1, np.int64)
         cb = _native.PROGRESS_FN(0)

@@ -88,6 +88,21 @@ def test_room_determinism_and_additivity(room):
     assert full.global_max > 0
 
 
+def test_room_one_vs_two_streams_bitwise(room):
+    """The two-stream batch pipeline keeps every sample's accumulation in log
+    order: identical bits to one stream, for several batch sizes."""
+    from paper_2601_07571_b200 import _native
+
+    scene, k, fx, sampled, cfg, plan = room
+    outs = []
+    for flags, batch in ((_native.GM_FLAG_ONE_STREAM, 0), (_native.GM_FLAG_TWO_STREAMS, 0),
+                         (_native.GM_FLAG_TWO_STREAMS, 257), (_native.GM_FLAG_ONE_STREAM, 257)):
+        plan.accumulate(fx, cfg, reset=True, batch=batch, flags=flags)
+        outs.append(plan.read())
+    for o in outs[1:]:
+        np.testing.assert_array_equal(o.view(np.uint64), outs[0].view(np.uint64))
+
+
 def test_room_filtered_vs_unfiltered(room):
     """Per fixation, filtering changes nothing but the z-buffer footprint: a
     sample's weight is identical in both paths (same Gaussian, bitwise) unless
