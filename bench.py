@@ -364,7 +364,8 @@ def run_ours(args, rank, world):
     # (profiles/r1_ncu_traffic.json, written by tools/ncu_traffic.py), per launch like `achieved`
     traffic, hbm, issue = None, None, None
     tpath = ROOT / "profiles" / "r1_ncu_traffic.json"
-    kname = {"k_samples<mark>": "k_mark", "k_samples<accumulate>": "k_samples"}.get(dom, dom)
+    kname = {"k_samples<mark>": "k_mark", "k_samples<accumulate>": "k_samples<0>",
+             "k_texels": "k_texels<0, 0, 0>"}.get(dom, dom)
     if tpath.exists():
         tk = json.loads(tpath.read_text())["kernels"].get(kname)
         if tk and int(tm.batches):

@@ -1,6 +1,5 @@
-mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -q --timeout 600 -p no:cacheprovider -x > gpurun_out/pytest_gpu7.log 2>&1
-echo "pytest rc=$?" >> gpurun_out/pytest_gpu7.log
-timeout 600 python bench.py --steps 3 --warmup 3 --no-cpu > gpurun_out/bench8.log 2>&1
-timeout 600 python bench.py --config c5 --steps 2 --warmup 2 --no-cpu --no-e2e > gpurun_out/bench8_c5.log 2>&1
-timeout 600 python bench.py --config c3k100 --steps 2 --warmup 2 --no-cpu > gpurun_out/bench8_c3.log 2>&1
+mkdir -p gpurun_out; rm -f gpurun_out/variants.txt
+for b in 1024 512 768 1024; do
+  timeout 600 python bench.py --steps 2 --warmup 2 --batch $b --no-cpu --no-e2e --no-stats > gpurun_out/bb_$b.log 2>&1
+  echo "c2 b$b $(grep -o '"ms_per_step": [0-9.]*' gpurun_out/bb_$b.log)" >> gpurun_out/variants.txt
+done

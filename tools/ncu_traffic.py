@@ -25,7 +25,7 @@ def main(path, batch):
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ms": 1.0, "us": 1e-3, "ns": 1e-6}
     acc = collections.defaultdict(lambda: [0, 0.0, 0.0, 0.0, 0.0])
     for r in rows[2:]:
-        name = r[ki].split("(")[0].replace("void ", "").split("<")[0]
+        name = r[ki].split("(")[0].replace("void ", "")  # template arguments kept: k_texels<0, 0, 0>
         rd = float(r[hdr.index("dram__bytes_read.sum")]) * scale[units[hdr.index("dram__bytes_read.sum")]]
         wr = float(r[hdr.index("dram__bytes_write.sum")]) * scale[units[hdr.index("dram__bytes_write.sum")]]
         t = float(r[hdr.index("gpu__time_duration.sum")]) * scale[units[hdr.index("gpu__time_duration.sum")]]
