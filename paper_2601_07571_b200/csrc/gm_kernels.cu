@@ -1,21 +1,24 @@
 // gm_kernels.cu -- sm_100a kernels and the C-ABI of the B200 density-map path.
 //
 // Path and where each piece lives:
-//   a1-a6  sampling: k_layout (Heron area -> r -> count), CUB scan (offsets),
-//          k_positions (index -> row/col -> barycentric -> world, FMA-chain
-//          transform like OpenBLAS), k_world_tris
-//   a8-a10 per-fixation setup: host, gm_setup.cpp (glibc trig, bit-exact)
+//   a1-a6   sampling: k_layout (Heron area -> r -> count), CUB scan (offsets),
+//           k_positions (index -> row/col -> barycentric -> world, FMA-chain
+//           transform like OpenBLAS), k_world_tris                      [here]
+//   a8-a10  per-fixation setup: host, gm_setup.cpp (glibc trig, bit-exact)
 //   a11-a12 occluders: k_tri_setup (conservative cone cull, exact camera
-//          transform + near clip + projection + _raster_tri setup) into
-//          per-fixation screen-triangle segments
-//   a13-a15 k_samples<true>: sample-major, one warp per 32-sample chunk,
-//          fixation culling by warp ballot, exact NDC filter + 4-sigma cone,
-//          marks the <= 9 texels depth_match will read;
-//          k_texels: fixation-major per 64x64 tile, evaluates only marked
-//          texels (min over covering screen triangles, reference pixel
-//          arithmetic) from shared-memory sub-bins;
-//          k_samples<false>: depth_match + Gaussian, accumulated in log order
-//   a16    k_max / k_normalize
+//           transform + near clip + projection + _raster_tri setup) into
+//           per-fixation screen-triangle segments; k_coarse bins   [here]
+//   a13-a15 gm_samples.cuh: k_level1 ballots, k_mark (float32 superset of the
+//           NDC filter + 4-sigma cone, marks the <= 9 texels depth_match
+//           reads, level-3 candidate words), k_samples (exact filter,
+//           depth_match, Gaussian, accumulated in log order)
+//   a12     gm_texels.cuh: k_texels, the marked texels' min depth (float32
+//           selection with rigorous bounds, exact float64 evaluation)
+//   a16     k_max / k_normalize                                          [here]
+//   a17     the plan: scene upload, two-stream double-buffered batch pipeline,
+//           C-ABI entry points                                           [here]
+//   seam    gm_raster.cuh: general-camera rasterize (+ attributes), heatmap
+//           renderer, cull_mask
 // Exactness: compiled with -fmad=false; see gm_device.cuh.
 #include <cub/cub.cuh>
 #include <cuda_runtime.h>
@@ -557,827 +560,9 @@ __device__ __forceinline__ bool depth_test(const DepthView& dv, int f, double gx
     return best <= eps;
 }
 
-// Sample-major pass over a batch of fixations (kernels.py:288-340).  A warp
-// owns 32 consecutive samples; lane l tests fixation g+l against the chunk
-// sphere, the ballot gives the fixations that can touch the chunk, and those
-// are applied in log order.
-//   MARK = true : set the mask bits of the 3x3 texel block depth_match reads
-//                 for every candidate that passes the NDC filter and the cone.
-//   MARK = false: depth_match on those texels and accumulate; the value slot
-//                 lives in a register, so per-sample accumulation order is the
-//                 reference's (density.py:223-226): deterministic, no atomics.
-// The cone test (kernels.py:330-339) runs before depth_match (:326): every
-// condition is conjunctive and side-effect free, so the contributing set and
-// the weights are unchanged.
-// Level 1 of the sample-side fixation cull, once per batch: warp per
-// super-chunk (8 chunks = 256 consecutive samples), lane-parallel sphere tests
-// against all fixations of the batch -> lvl1[sc][g] ballots and the number of
-// fixations that can touch the super-chunk (the work estimate used to order
-// the sample passes, heaviest first).
-__global__ void __launch_bounds__(256) k_level1(const float4* __restrict__ supers, int64_t n_supers,
-                                                const GmFixCull* __restrict__ culls, int B,
-                                                uint32_t* __restrict__ lvl1, int* __restrict__ count,
-                                                int* __restrict__ order, const long long* __restrict__ fail,
-                                                long long b0) {
-    const int lane = threadIdx.x & 31;
-    const int64_t sc = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (sc >= n_supers) return;
-    const int ngroups = (B + 31) >> 5;
-    int total = 0;
-    if (*fail > b0) {
-        const float4 ssph = supers[sc];
-        for (int g = 0; g < ngroups; g++) {
-            const int myf = g * 32 + lane;
-            const unsigned m = __ballot_sync(0xffffffffu, myf < B && sphere_visible(culls[myf], ssph, false));
-            if (lane == 0) lvl1[sc * ngroups + g] = m;
-            total += __popc(m);
-        }
-    }
-    if (lane == 0) {
-        count[sc] = total;
-        order[sc] = (int)sc;
-    }
-}
+#include "gm_samples.cuh"
 
-// float32 view of a fixation for the marking pass, with a rigorous bound E on
-// |camera coordinate in float32 - exact| over every sample of the plan.
-struct __align__(16) GmFixF32 {
-    float rot[9], trans[3], gaze[3];
-    float p00, p11, p02, p12;
-    float near_lo, far_hi;
-    float E;        // absolute bound on the float32 camera-coordinate error (m)
-    float sig16;    // 16 sigma^2 (ratio^2 <= 16 <=> |p x g|^2 <= 16 sigma^2 d1^2)
-};  // 96 B
-
-// float32 copies of the sample positions and max |coordinate| (bit-pattern
-// atomicMax, exact for non-negative doubles)
-__global__ void k_to_f32(const double* __restrict__ px, const double* __restrict__ py, const double* __restrict__ pz,
-                         int64_t N, float* __restrict__ fx, float* __restrict__ fy, float* __restrict__ fz,
-                         unsigned long long* __restrict__ amax) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    double m = 0.0;
-    if (i < N) {
-        const double x = px[i], y = py[i], z = pz[i];
-        fx[i] = (float)x;
-        fy[i] = (float)y;
-        fz[i] = (float)z;
-        m = fmax(fabs(x), fmax(fabs(y), fabs(z)));
-    }
-    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if ((threadIdx.x & 31) == 0 && m > 0.0) atomicMax(amax, (unsigned long long)__double_as_longlong(m));
-}
-
-__global__ void k_fix32(const GmFixExact* __restrict__ ex, int nb, double pmax, double sigma,
-                        GmFixF32* __restrict__ out) {
-    const int f = blockIdx.x * blockDim.x + threadIdx.x;
-    if (f >= nb) return;
-    const GmFixExact& F = ex[f];
-    GmFixF32 o;
-    double tmax = 0.0;
-    for (int i = 0; i < 9; i++) o.rot[i] = (float)F.rot[i];
-    for (int i = 0; i < 3; i++) {
-        o.trans[i] = (float)F.trans[i];
-        o.gaze[i] = (float)F.gaze[i];
-        tmax = fmax(tmax, fabs(F.trans[i]));
-    }
-    o.p00 = (float)F.p00;
-    o.p11 = (float)F.p11;
-    o.p02 = (float)F.p02;
-    o.p12 = (float)F.p12;
-    o.near_lo = (float)F.near_lo;
-    o.far_hi = (float)F.far_hi;
-    // fma chain of 3 products + translation, every operand rounded to float32:
-    // |x32 - x| <= ~8 * 2^-24 * (3 pmax + |t|); E is > 2x that
-    o.E = (float)(1e-6 * (3.0 * pmax + tmax) + 1e-30);
-    o.sig16 = (float)(16.0 * sigma * sigma);
-    out[f] = o;
-}
-
-// The marking pass: for every (sample, fixation) that can be a depth-test
-// candidate (kernels.py:305-339: NDC crop filter and 4-sigma cone), set the
-// mask bits of the texels depth_match may read.  Float32 with rigorous error
-// bounds -- a superset of the exact candidates and of their exact 3x3 blocks
-// (rint is monotone: the exact rint(g) lies in [rint(g32 - dg), rint(g32 + dg)])
-// -- and the exact float64 computation for the rare lanes whose bounds are too
-// loose (samples within ~E of the camera plane).  Marking extra texels only
-// costs texel work; every texel an exact depth test reads is marked.
-__global__ void KM_BOUNDS k_mark(const float* __restrict__ pxf, const float* __restrict__ pyf,
-                                              const float* __restrict__ pzf, const double* __restrict__ px,
-                                              const double* __restrict__ py, const double* __restrict__ pz,
-                                              const float4* __restrict__ chunks, const uint32_t* __restrict__ lvl1,
-                                              const int* __restrict__ order, int* __restrict__ work, int64_t N,
-                                              int64_t n_chunks, int64_t n_supers, const GmFixExact* __restrict__ fixes,
-                                              const GmFixF32* __restrict__ fix32, const GmFixCull* __restrict__ culls,
-                                              int B, DepthView dv, double inv_sigma, uint32_t* __restrict__ cbits,
-                                              const long long* __restrict__ fail, long long b0) {
-    if (*fail <= b0) return;
-    const int lane = threadIdx.x & 31;
-    const int ngroups = (B + 31) >> 5;
-    const int W = dv.W, H = dv.H;
-    const float Wf = (float)W, Hf = (float)H;
-    const float lo = -1.0f - (float)GM_NDC_SLACK, hi = 1.0f + (float)GM_NDC_SLACK;
-    const int64_t n_items = n_supers * 8;
-    for (;;) {
-        int item = 0;
-        if (lane == 0) item = atomicAdd(work, 1);
-        item = __shfl_sync(0xffffffffu, item, 0);
-        if (item >= n_items) break;
-        const int64_t sc = order[item >> 3];
-        const int64_t ch = sc * 8 + (item & 7);
-        if (ch >= n_chunks) continue;
-        const unsigned l1 = lane < ngroups ? lvl1[sc * ngroups + lane] : 0u;
-        if (!__any_sync(0xffffffffu, l1 != 0u)) continue;
-        const int64_t i = ch * 32 + lane;
-        const bool valid = i < N;
-        float wx = 0.0f, wy = 0.0f, wz = 0.0f;
-        if (valid) {
-            wx = pxf[i];
-            wy = pyf[i];
-            wz = pzf[i];
-        }
-        const float4 sph = chunks[ch];
-        for (int gi = 0; gi < ngroups; gi++) {
-            const unsigned sm = __shfl_sync(0xffffffffu, l1, gi);
-            if (!sm) continue;
-            const int g = gi * 32;
-            const bool pass = ((sm >> lane) & 1u) && sphere_visible(culls[g + lane], sph, false);
-            unsigned mask = __ballot_sync(0xffffffffu, pass);
-            unsigned my_bits = 0;  // fixations (bit j of group gi) for which this lane is a candidate
-            while (mask) {
-                const int j = __ffs(mask) - 1;
-                mask &= mask - 1;
-                if (!valid) continue;
-                const int f = g + j;
-                const GmFixF32& Q = fix32[f];
-                const float E = Q.E;
-                const float x = __fmaf_rn(Q.rot[2], wz, __fmaf_rn(Q.rot[1], wy, __fmaf_rn(Q.rot[0], wx, Q.trans[0])));
-                const float y = __fmaf_rn(Q.rot[5], wz, __fmaf_rn(Q.rot[4], wy, __fmaf_rn(Q.rot[3], wx, Q.trans[1])));
-                const float z = __fmaf_rn(Q.rot[8], wz, __fmaf_rn(Q.rot[7], wy, __fmaf_rn(Q.rot[6], wx, Q.trans[2])));
-                const float w = -z;
-                if (w + E <= 0.0f) continue;                               // exact w <= 0
-                if (w + E < Q.near_lo || w - E > Q.far_hi) continue;      // exact depth outside the slab
-                const float wl = w - E;
-                float bxlo, bxhi, bylo, byhi;  // range of the exact g (texel coordinates)
-                bool exact = !(wl > 1e-3f * fabsf(w) + 1e-12f);
-                if (!exact) {
-                    // NDC (kernels.py:314-319) with bound dq on |q32 - q_exact|
-                    const float nx = __fmaf_rn(Q.p00, x, Q.p02 * z), ny = __fmaf_rn(Q.p11, y, Q.p12 * z);
-                    const float qx = nx / w, qy = ny / w;
-                    const float en_x = (fabsf(Q.p00) + fabsf(Q.p02)) * E + 4e-7f * (fabsf(Q.p00 * x) + fabsf(Q.p02 * z));
-                    const float en_y = (fabsf(Q.p11) + fabsf(Q.p12)) * E + 4e-7f * (fabsf(Q.p11 * y) + fabsf(Q.p12 * z));
-                    const float dqx = (en_x + fabsf(qx) * E) / wl + 1e-6f * fabsf(qx) + 1e-7f;
-                    const float dqy = (en_y + fabsf(qy) * E) / wl + 1e-6f * fabsf(qy) + 1e-7f;
-                    if (qx + dqx < lo || qx - dqx > hi || qy + dqy < lo || qy - dqy > hi) continue;
-                    // cone (kernels.py:330-339): d1 > 0 and ratio^2 <= 16
-                    const float d1 = __fmaf_rn(x, Q.gaze[0], __fmaf_rn(y, Q.gaze[1], z * Q.gaze[2]));
-                    const float ed1 = 2.0f * E + 4e-7f * (fabsf(x) + fabsf(y) + fabsf(z));
-                    if (d1 + ed1 <= 0.0f) continue;
-                    const float cx3 = y * Q.gaze[2] - z * Q.gaze[1], cy3 = z * Q.gaze[0] - x * Q.gaze[2];
-                    const float cz3 = x * Q.gaze[1] - y * Q.gaze[0];
-                    const float cr = sqrtf(__fmaf_rn(cx3, cx3, __fmaf_rn(cy3, cy3, cz3 * cz3)));
-                    const float ecr = 3.0f * E + 1e-6f * (fabsf(x) + fabsf(y) + fabsf(z));
-                    const float crl = cr - ecr, d1h = d1 + ed1;
-                    if (crl > 0.0f && crl * crl > Q.sig16 * (1.0f + 1e-4f) * d1h * d1h) continue;
-                    const float gx = (qx + 1.0f) * 0.5f * Wf - 0.5f, gy = (1.0f - qy) * 0.5f * Hf - 0.5f;
-                    const float dgx = dqx * 0.5f * Wf + 1e-4f + 1e-6f * fabsf(gx);
-                    const float dgy = dqy * 0.5f * Hf + 1e-4f + 1e-6f * fabsf(gy);
-                    if (dgx > 2.0f || dgy > 2.0f) {
-                        exact = true;
-                    } else {
-                        bxlo = gx - dgx;
-                        bxhi = gx + dgx;
-                        bylo = gy - dgy;
-                        byhi = gy + dgy;
-                    }
-                }
-                int cxlo, cxhi, cylo, cyhi;
-                if (exact) {
-                    // the exact float64 test of k_samples, for this lane only
-                    const GmFixExact& F = fixes[f];
-                    const double X = px[i], Y = py[i], Z = pz[i];
-                    const double xx = F.rot[0] * X + F.rot[1] * Y + F.rot[2] * Z + F.trans[0];
-                    const double yy = F.rot[3] * X + F.rot[4] * Y + F.rot[5] * Z + F.trans[1];
-                    const double zz = F.rot[6] * X + F.rot[7] * Y + F.rot[8] * Z + F.trans[2];
-                    const double ww = -zz;
-                    if (ww <= 0.0 || ww < F.near_lo || ww > F.far_hi) continue;
-                    const double ndx = (F.p00 * xx + F.p02 * zz) / ww, ndy = (F.p11 * yy + F.p12 * zz) / ww;
-                    const double l = -1.0 - GM_NDC_SLACK, h = 1.0 + GM_NDC_SLACK;
-                    if (ndx < l || ndx > h || ndy < l || ndy > h) continue;
-                    const double d1 = xx * F.gaze[0] + yy * F.gaze[1] + zz * F.gaze[2];
-                    if (d1 <= 0.0) continue;
-                    double d2sq = xx * xx + yy * yy + zz * zz - d1 * d1;
-                    if (d2sq < 0.0) d2sq = 0.0;
-                    if (d2sq * inv_sigma * inv_sigma / (d1 * d1) > 16.0) continue;
-                    const double gxe = (ndx + 1.0) * 0.5 * (double)W - 0.5, gye = (1.0 - ndy) * 0.5 * (double)H - 0.5;
-                    long long rx = x86_i64(rint(gxe)), ry = x86_i64(rint(gye));
-                    cxlo = cxhi = (int)max(min(rx, (long long)W - 1), 0LL);
-                    cylo = cyhi = (int)max(min(ry, (long long)H - 1), 0LL);
-                } else {
-                    cxlo = (int)fminf(fmaxf(rintf(bxlo), 0.0f), (float)(W - 1));
-                    cxhi = (int)fminf(fmaxf(rintf(bxhi), 0.0f), (float)(W - 1));
-                    cylo = (int)fminf(fmaxf(rintf(bylo), 0.0f), (float)(H - 1));
-                    cyhi = (int)fminf(fmaxf(rintf(byhi), 0.0f), (float)(H - 1));
-                }
-                const int bx0 = max(cxlo - 1, 0), bx1 = min(cxhi + 1, W - 1);
-                const int by0 = max(cylo - 1, 0), by1 = min(cyhi + 1, H - 1);
-                my_bits |= 1u << j;
-                uint32_t* m = dv.mask + (int64_t)f * H * dv.wwords;
-                const unsigned long long bits = ((1ull << (bx1 - bx0 + 1)) - 1ull) << (bx0 & 31);
-                const int w0 = bx0 >> 5;
-                for (int yy = by0; yy <= by1; yy++) {
-                    uint32_t* row = m + (int64_t)yy * dv.wwords + w0;
-                    atomicOr(row, (uint32_t)bits);
-                    if (bits >> 32) atomicOr(row + 1, (uint32_t)(bits >> 32));
-                }
-            }
-            // level 3 for the accumulation pass: the fixations of this group with at
-            // least one (float32-superset) candidate in this chunk
-            const unsigned word = __reduce_or_sync(0xffffffffu, my_bits);
-            if (lane == 0) cbits[ch * 32 + gi] = word;
-        }
-    }
-}
-
-template <bool STATS>
-__global__ void KS_BOUNDS k_samples(const double* __restrict__ px, const double* __restrict__ py,
-                                                 const double* __restrict__ pz, const float4* __restrict__ chunks,
-                                                 const uint32_t* __restrict__ lvl1, const int* __restrict__ order,
-                                                 int* __restrict__ work, int64_t N, int64_t n_chunks,
-                                                 int64_t n_supers, const GmFixExact* __restrict__ fixes,
-                                                 const GmFixCull* __restrict__ culls, int B, DepthView dv,
-                                                 double inv_sigma, double eps_abs, double eps_rel,
-                                                 double* __restrict__ values, const uint32_t* __restrict__ cbits,
-                                                 const long long* __restrict__ fail, long long b0) {
-    if (*fail <= b0) return;  // this batch overflowed the triangle store: the host redoes it
-    const int lane = threadIdx.x & 31;
-    const int ngroups = (B + 31) >> 5;  // <= 32 (B <= GM_MAX_BATCH)
-    const int W = dv.W, H = dv.H;
-    const double Wd = (double)W, Hd = (double)H;
-    const double lo = -1.0 - GM_NDC_SLACK, hi = 1.0 + GM_NDC_SLACK;
-    const int64_t n_items = n_supers * 8;
-    unsigned c_l1 = 0, c_l2 = 0, c_exact = 0, c_ndc = 0, c_cand = 0, c_vis = 0;
-    // persistent warps; items = chunks of the super-chunks in descending-work
-    // order (k_level1 + radix sort), claimed one at a time
-    for (;;) {
-        int item = 0;
-        if (lane == 0) item = atomicAdd(work, 1);
-        item = __shfl_sync(0xffffffffu, item, 0);
-        if (item >= n_items) break;
-        const int64_t sc = order[item >> 3];
-        const int64_t ch = sc * 8 + (item & 7);
-        if (ch >= n_chunks) continue;
-        const unsigned l1 = lane < ngroups ? lvl1[sc * ngroups + lane] : 0u;  // lane g: group g
-        if (STATS) c_l1 += 1;
-        if (!__any_sync(0xffffffffu, l1 != 0u)) continue;
-        {
-        const int64_t i = ch * 32 + lane;
-        const bool valid = i < N;
-        double wx = 0.0, wy = 0.0, wz = 0.0, v = 0.0;
-        if (valid) {
-            wx = px[i];
-            wy = py[i];
-            wz = pz[i];
-            v = values[i];
-        }
-        for (int gi = 0; gi < ngroups; gi++) {
-            const unsigned sm = __shfl_sync(0xffffffffu, l1, gi);
-            if (!sm) continue;
-            const int g = gi * 32;
-            // levels 2 + 3 (k_mark): the fixations of this group with a candidate in the chunk
-            if (STATS) c_l2 += (sm >> lane) & 1u;
-            unsigned mask = cbits[ch * 32 + gi];
-            while (mask) {
-                const int j = __ffs(mask) - 1;
-                mask &= mask - 1;
-                if (!valid) continue;
-                const int f = g + j;
-                const GmFixExact& F = fixes[f];
-                if (STATS) c_exact++;
-                // kernels.py:305-319
-                double x = F.rot[0] * wx + F.rot[1] * wy + F.rot[2] * wz + F.trans[0];
-                double y = F.rot[3] * wx + F.rot[4] * wy + F.rot[5] * wz + F.trans[1];
-                double z = F.rot[6] * wx + F.rot[7] * wy + F.rot[8] * wz + F.trans[2];
-                double w = -z;
-                if (w <= 0.0) continue;
-                double d = w;
-                if (d < F.near_lo || d > F.far_hi) continue;
-                double ndc_x = (F.p00 * x + F.p02 * z) / w;
-                double ndc_y = (F.p11 * y + F.p12 * z) / w;
-                if (ndc_x < lo || ndc_x > hi) continue;
-                if (ndc_y < lo || ndc_y > hi) continue;
-                if (STATS) c_ndc++;
-                // kernels.py:330-339 (moved before the depth test)
-                double d1 = x * F.gaze[0] + y * F.gaze[1] + z * F.gaze[2];
-                if (d1 <= 0.0) continue;
-                double d2sq = x * x + y * y + z * z - d1 * d1;
-                if (d2sq < 0.0) d2sq = 0.0;
-                double ratio_sq = d2sq * inv_sigma * inv_sigma / (d1 * d1);
-                if (ratio_sq > 16.0) continue;
-                if (STATS) c_cand++;
-                // texel coordinates (kernels.py:327, :231-232, :267-276)
-                double gx = (ndc_x + 1.0) * 0.5 * Wd - 0.5;
-                double gy = (1.0 - ndc_y) * 0.5 * Hd - 0.5;
-                long long cx = x86_i64(rint(gx));
-                if (cx < 0) cx = 0;
-                else if (cx > W - 1) cx = W - 1;
-                long long cy = x86_i64(rint(gy));
-                if (cy < 0) cy = 0;
-                else if (cy > H - 1) cy = H - 1;
-                int bx0 = (int)max(cx - 1, 0LL), bx1 = (int)min(cx + 1, (long long)W - 1);
-                int by0 = (int)max(cy - 1, 0LL), by1 = (int)min(cy + 1, (long long)H - 1);
-                // kernels.py:323-329
-                double eps = eps_abs;
-                if (eps_rel * d > eps) eps = eps_rel * d;
-                if (!depth_test(dv, f, gx, gy, bx0, bx1, by0, by1, d, eps)) continue;
-                if (STATS) c_vis++;
-                v += F.amp * exp(-0.5 * ratio_sq);  // kernels.py:340
-            }
-        }
-        if (valid) values[i] = v;
-        }
-    }
-    if (STATS) {
-        stat_add(dv.stats, GM_STAT_L1_TESTS, lane == 0 ? c_l1 * (unsigned long long)B : 0ull);
-        stat_add(dv.stats, GM_STAT_L2_TESTS, c_l2);
-        stat_add(dv.stats, GM_STAT_EXACT, c_exact);
-        stat_add(dv.stats, GM_STAT_NDC, c_ndc);
-        stat_add(dv.stats, GM_STAT_CANDIDATES, c_cand);
-        stat_add(dv.stats, GM_STAT_VISIBLE, c_vis);
-    }
-}
-
-#define TW_CAP 32
-#define TW_SEL 128  // overlapping triangles remembered per tile (more: rescanned per round)
-#ifndef TW_WARPS
-#define TW_WARPS 2  // warps (independent tile items) per k_texels CTA
-#endif
-struct __align__(16) TexelWarpSmem {
-    TriF32 t32[TW_CAP];  // staged, in ascending min-depth order
-    int sel[TW_SEL + 32];
-};
-#define TX_DYN_SMEM (TW_WARPS * (int)sizeof(TexelWarpSmem))
-#define TC_SEL 512   // crowded tiles: overlap list sorted per pass (longer lists: several passes)
-#define TC_RES 64    // crowded tiles: nearest triangles staged in shared memory
-struct __align__(16) CrowdedWarpSmem {
-    TriF32 t32[TC_RES];
-    int sel[TC_SEL];
-    float key[TC_SEL];
-};
-#ifndef TC_WARPS
-#define TC_WARPS 4  // warps per CTA of the crowded pass
-#endif
-#ifndef CROWD_DEPTH
-#define CROWD_DEPTH 10  // ... and whose triangle bboxes cover the tile more than this many times
-#endif
-#ifndef CROWD_MIN
-#define CROWD_MIN 128  // tiles overlapping more triangles than this go to the crowded pass
-#endif
-#define TC_DYN_SMEM (TC_WARPS * (int)sizeof(CrowdedWarpSmem))
-#define TX_MAX_THREADS (32 * (TW_WARPS > TC_WARPS ? TW_WARPS : TC_WARPS))
-
-// position of the k-th (0-based) set bit of w (k < popc(w))
-__device__ __forceinline__ int kth_set_bit(uint32_t w, int k) {
-    int base = 0;
-#pragma unroll
-    for (int half = 16; half >= 1; half >>= 1) {
-        const uint32_t low = w & ((1u << half) - 1u);
-        const int c = __popc(low);
-        if (k >= c) {
-            k -= c;
-            w >>= half;
-            base += half;
-        } else {
-            w = low;
-        }
-    }
-    return base;
-}
-
-// Fixation-major evaluation of the marked texels.  Every warp is an
-// independent work item (fixation, 32x16-pixel tile): no CTA barriers, no
-// atomics, per-texel state in registers.
-//   1. the tile's triangles are gathered from its coarse bin (bbox-filtered);
-//   2. their float32 forms (TriF32, built once per screen triangle by
-//      k_tri_setup: edge-function and inverse-depth planes with rigorous error
-//      bounds) are staged in the warp's shared slice TW_CAP at a time, in
-//      ascending min-depth order;
-//   3. lanes take the marked texels (compacted, 32 per round) and walk the
-//      sorted triangles with uniform float32 tests: "certainly written"
-//      (inside by more than the bound, inverse depth certainly within
-//      (1/far', 1/near')) or "maybe written".  V, the largest certain lower
-//      bound of the inverse depth, proves depth <= 1/V, so a maybe-triangle
-//      whose inverse-depth upper bound is < V can never be the minimum, and
-//      once a triangle's 1/minw bound is < V no later one can be (stop);
-//   4. the surviving candidates (normally one) are evaluated exactly with the
-//      reference's float64 pixel arithmetic (texel_depth, float64 record read
-//      from L1/L2) and the minimum is stored -- the value kernels.rasterize
-//      leaves in that pixel.
-// One (fixation, tile) work item of k_texels.  T32/SEL: the warp's staging and
-// selection slices; KEY (crowded mode only): sort keys of SEL.
-template <bool ATTRS, bool STATS, bool CROWDED>
-__device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __restrict__ SEL, float* __restrict__ KEY,
-                                           int64_t item, const TriStore& ts, const DepthView& dv,
-                                           const CoarseBins& cb, int tiles_x, int tiles_per_fix,
-                                           const GmFixExact* __restrict__ fixes) {
-    const int lane = threadIdx.x & 31;
-    const int f = (int)(item / tiles_per_fix);
-    const int tile = (int)(item - (int64_t)f * tiles_per_fix);
-    const int W = dv.W, H = dv.H;
-    const int xb = (tile % tiles_x) * TW, yb = (tile / tiles_x) * TH;
-    const unsigned FULL = 0xffffffffu;
-    // marked texels: lane r < TH holds the mask word of row yb + r
-    uint32_t wr = 0;
-    if (lane < TH && yb + lane < H) wr = dv.mask[((int64_t)f * H + yb + lane) * dv.wwords + (xb >> 5)];
-    const int cnt_r = __popc(wr);
-    int pref = cnt_r;  // inclusive prefix over rows
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_up_sync(FULL, pref, o);
-        if (lane >= o) pref += v;
-    }
-    const int total = __shfl_sync(FULL, pref, 31);
-    if (total == 0) return;
-    const int pref_ex = pref - cnt_r;
-    const GmFixExact& F = fixes[f];
-    const double near_ = F.near_, far_ = F.far_;
-    // written iff near' <= 1/inv_w <= far' (kernels.py:123-127): certainly inside
-    // [inv_far_hi, inv_near_lo], certainly outside beyond [inv_far_lo, inv_near_hi]
-    const float inv_near = (float)(1.0 / near_), inv_far = (float)(1.0 / far_);
-    const float inv_near_lo = inv_near * (1.0f - 1e-5f), inv_near_hi = inv_near * (1.0f + 1e-5f);
-    const float inv_far_lo = inv_far * (1.0f - 1e-5f), inv_far_hi = inv_far * (1.0f + 1e-5f);
-    const GmScreenTri* seg = ts.tris + (int64_t)f * ts.cap_seg;
-    const uint2* segb = ts.bbox + (int64_t)f * ts.cap_seg;
-    const int* clist = nullptr;
-    int n = min(ts.count[f], (int)ts.cap_seg);
-    if (!cb.ovf[f]) {
-        const int* off = cb.off + (int64_t)f * (GM_MAX_CBINS + 1);
-        const int bb = (yb >> cb.shift) * cb.ncx + (xb >> cb.shift);
-        clist = cb.items + (int64_t)f * cb.cap_items + off[bb];
-        n = off[bb + 1] - off[bb];
-    }
-    const int xe = xb + TW - 1, ye = yb + TH - 1;
-    unsigned long long c_pairs = 0, c_cov = 0, c_iter = 0, c_edge = 0;
-
-    // 1. triangles overlapping the tile -> S.sel (scan cursor resumes if > TW_SEL)
-    int cover = 0;  // this lane's share of the selected bboxes' area inside the tile (depth complexity)
-    auto gather = [&](int& cursor) {
-        int cnt = 0;
-        while (cursor < n && cnt < TW_SEL) {
-            int i = cursor + lane;
-            bool sel = false;
-            if (i < n) {
-                if (clist) i = clist[i];
-                const uint2 bbx = segb[i];
-                const int x0 = bbx.x & 0xffff, x1 = bbx.x >> 16, y0 = bbx.y & 0xffff, y1 = bbx.y >> 16;
-                sel = !(x1 < xb || x0 > xe || y1 < yb || y0 > ye);
-                if (sel) cover += (min(x1, xe) - max(x0, xb) + 1) * (min(y1, ye) - max(y0, yb) + 1);
-            }
-            const unsigned bal = __ballot_sync(FULL, sel);
-            if (sel) SEL[cnt + __popc(bal & ((1u << lane) - 1u))] = i;
-            cnt += __popc(bal);
-            cursor += 32;
-        }
-        __syncwarp();
-        return cnt;  // may exceed TW_SEL by < 32 (S.sel has the room)
-    };
-
-    // 2. stage SEL[c0 .. c0 + kend) (float32 forms) in ascending min-depth order
-    const TriF32* segf = ts.t32 + (int64_t)f * ts.cap_seg;
-    auto stage = [&](int c0, int kend) {
-        __syncwarp();
-        const int gi = lane < kend ? SEL[c0 + lane] : 0;
-        float key = lane < kend ? -__ldg(&segf[gi].inv_minw) : CUDART_INF_F;  // ascending min depth
-        int slot = lane;
-#pragma unroll
-        for (int size = 2; size <= 32; size <<= 1) {
-#pragma unroll
-            for (int stride = size >> 1; stride > 0; stride >>= 1) {
-                const float ok = __shfl_xor_sync(FULL, key, stride);
-                const int os = __shfl_xor_sync(FULL, slot, stride);
-                const bool keep_min = ((lane & stride) == 0) == ((lane & size) == 0);
-                const bool less = ok < key || (ok == key && os < slot);
-                if (keep_min ? less : !less && !(ok == key && os == slot)) {
-                    key = ok;
-                    slot = os;
-                }
-            }
-        }
-        // lane = rank; it copies the record of sorted position `lane`
-        const int src = __shfl_sync(FULL, gi, slot);
-        if (lane < kend) {
-            const uint4* from = reinterpret_cast<const uint4*>(segf + src);
-            uint4* to = reinterpret_cast<uint4*>(&T32[lane]);
-#pragma unroll
-            for (int part = 0; part < 6; part++) to[part] = from[part];
-        }
-        __syncwarp();
-    };
-
-    // texel of compact id q: (row, tile-local column)
-    auto texel_of = [&](int q, int& row, int& colo) {
-        row = 0;
-#pragma unroll
-        for (int step = TH / 2; step > 0; step >>= 1) {
-            const int cand = row + step;
-            const int pc = __shfl_sync(FULL, pref_ex, cand & 31);
-            if (cand < TH && pc <= q) row = cand;
-        }
-        const uint32_t w_row = __shfl_sync(FULL, wr, row);
-        const int k_in_row = q - __shfl_sync(FULL, pref_ex, row);
-        colo = q < total ? kth_set_bit(w_row, k_in_row) : 0;
-    };
-
-    // 3 + 4 for the staged chunk (kend triangles) and one texel: updates V, best
-    // kernels.py:128-129 writes iff d < depth[py, px]: among equal minima the
-    // first triangle in rasterization order (key 2 t + fan) owns the texel
-    auto take = [&](double d, int cs, double& best, int& bkey) {
-        if (!ATTRS) {
-            if (d < best) best = d;
-            return;
-        }
-        const int key = (int)(seg[cs].tl >> 3);
-        if (d < best || (d == best && d < CUDART_INF && key < bkey)) {
-            best = d;
-            bkey = key;
-        }
-    };
-    // triangle kk of the walk: staged in shared memory (kk < nst) or, crowded mode, from global
-    auto tri_at = [&](int kk, int nst) -> const TriF32& { return (!CROWDED || kk < nst) ? T32[kk] : segf[SEL[kk]]; };
-    auto walk = [&](int kend, int nst, bool valid, int row, int colo, float& V, double& best, int& bkey) {
-        const int px = xb + colo, py = yb + row;
-        int cs0 = -1, cs1 = -1;  // exact candidates (global record index) and their bounds
-        float ch0 = 0.0f, ch1 = 0.0f;
-        bool overflow = false;
-        for (int kk = 0; kk < kend; kk++) {
-            const TriF32& t = tri_at(kk, nst);
-            const float inv_minw = t.inv_minw;
-            if (__all_sync(FULL, !(inv_minw >= V))) break;  // nothing later can be nearer
-            if (STATS) c_iter++;
-            const uint32_t tbx = t.bx, tby = t.by;
-            if (!(inv_minw >= V) || px < (int)(tbx & 0xffff) || px > (int)(tbx >> 16) || py < (int)(tby & 0xffff) ||
-                py > (int)(tby >> 16))
-                continue;
-            if (STATS) c_edge++;
-            const float fx = (float)(px - t.ox) + 0.5f, fy = (float)(py - t.oy) + 0.5f;  // bbox-local centre
-            bool maybe = true, certain = true;
-#pragma unroll
-            for (int i = 0; i < 3; i++) {
-                const float e = __fmaf_rn(t.a[i], fx, __fmaf_rn(t.b[i], fy, t.c[i]));
-                maybe = maybe && (e >= -t.tol[i]);
-                certain = certain && (e > t.tol[i]);
-            }
-            if (!maybe) continue;
-            const float iwv = __fmaf_rn(t.A, fx, __fmaf_rn(t.B, fy, t.C));
-            const float lo = iwv - t.tolw, hi = iwv + t.tolw;
-            if (!(hi > 0.0f) || lo > inv_near_hi || hi < inv_far_lo) continue;  // certainly not written
-            if (certain && lo > 0.0f && hi <= inv_near_lo && lo >= inv_far_hi && lo * (1.0f - 1e-6f) > V)
-                V = lo * (1.0f - 1e-6f);
-            if (hi >= V) {
-                if (cs0 < 0) {
-                    cs0 = t.gidx;
-                    ch0 = hi;
-                } else if (cs1 < 0) {
-                    cs1 = t.gidx;
-                    ch1 = hi;
-                } else if (ch0 < V) {  // a stale candidate can be replaced
-                    cs0 = t.gidx;
-                    ch0 = hi;
-                } else if (ch1 < V) {
-                    cs1 = t.gidx;
-                    ch1 = hi;
-                } else {
-                    overflow = true;
-                }
-            }
-        }
-        if (!valid) return;
-        if (!overflow) {
-            if (cs0 >= 0 && ch0 >= V) {
-                const double d = texel_depth(seg[cs0], px, py, near_, far_);
-                if (STATS) c_pairs++;
-                if (STATS) c_cov += d < CUDART_INF;
-                take(d, cs0, best, bkey);
-            }
-            if (cs1 >= 0 && ch1 >= V) {
-                const double d = texel_depth(seg[cs1], px, py, near_, far_);
-                if (STATS) c_pairs++;
-                if (STATS) c_cov += d < CUDART_INF;
-                take(d, cs1, best, bkey);
-            }
-        } else {  // slow path: every staged triangle whose bbox covers the texel
-            for (int k = 0; k < kend; k++) {
-                const TriF32& t = tri_at(k, nst);
-                if (px < (int)(t.bx & 0xffff) || px > (int)(t.bx >> 16) || py < (int)(t.by & 0xffff) ||
-                    py > (int)(t.by >> 16))
-                    continue;
-                const double d = texel_depth(seg[t.gidx], px, py, near_, far_);
-                if (STATS) c_pairs++;
-                if (STATS) c_cov += d < CUDART_INF;
-                take(d, t.gidx, best, bkey);
-            }
-        }
-    };
-
-    double* dep = dv.depth + (int64_t)f * W * H;
-    int cursor = 0;
-    int nsel_total = 0;
-    auto store = [&](int row, int colo, double best, int bkey) {
-        dep[(int64_t)(yb + row) * W + xb + colo] = best;
-        if (ATTRS) dv.key[(int64_t)(yb + row) * W + xb + colo] = best < CUDART_INF ? bkey : -1;
-    };
-    if (!CROWDED) {
-        int nsel = gather(cursor);
-        if (STATS) nsel_total = nsel;
-        // deep tiles (overlapping surfaces: the selected bboxes cover the tile more than
-        // CROWD_DEPTH times) profit from the sorted crowded pass; wide ones (many
-        // side-by-side triangles) stay here
-        if ((cursor < n || nsel > CROWD_MIN) && dv.crowd &&
-            __reduce_add_sync(FULL, (unsigned)cover) > (unsigned)(CROWD_DEPTH * TW * TH)) {
-            // more than TW_CAP triangles: k_texels<CROWDED> sorts the whole list (deferred)
-            if (lane == 0) dv.crowd[atomicAdd(dv.crowd_count, 1)] = (int)item;
-            return;
-        }
-        if (cursor >= n && nsel <= TW_CAP) {
-            // common case: one staging serves every round, per-texel state in registers
-            if (nsel > 0) stage(0, nsel);
-            for (int r0 = 0; r0 < total; r0 += 32) {
-                const int q = r0 + lane;
-                const bool valid = q < total;
-                int row, colo;
-                texel_of(q, row, colo);
-                float V = valid ? 0.0f : CUDART_INF_F;
-                double best = CUDART_INF;
-                int bkey = INT_MAX;
-                if (nsel > 0) walk(nsel, nsel, valid, row, colo, V, best, bkey);
-                if (valid) store(row, colo, best, bkey);
-            }
-        } else {
-            // many triangles without a deferral list: chunk by chunk (each staged once),
-            // per-texel state kept in the depth array and the inverse-depth-bound buffer
-            float* vb = dv.vbuf + (int64_t)f * W * H;
-            bool first = true;
-            while (true) {
-                for (int c0 = 0; c0 < nsel; c0 += TW_CAP) {
-                    const int kend = min(TW_CAP, nsel - c0);
-                    stage(c0, kend);
-                    for (int r0 = 0; r0 < total; r0 += 32) {
-                        const int q = r0 + lane;
-                        const bool valid = q < total;
-                        int row, colo;
-                        texel_of(q, row, colo);
-                        const int64_t at = (int64_t)(yb + row) * W + xb + colo;
-                        float V = valid ? (first ? 0.0f : vb[at]) : CUDART_INF_F;
-                        double best = (valid && !first) ? dep[at] : CUDART_INF;
-                        int bkey = INT_MAX;
-                        if (ATTRS && valid && !first) bkey = dv.key[at];
-                        walk(kend, kend, valid, row, colo, V, best, bkey);
-                        if (valid) {
-                            dep[at] = best;
-                            vb[at] = V;
-                            if (ATTRS) dv.key[at] = best < CUDART_INF ? bkey : -1;
-                        }
-                    }
-                    first = false;
-                }
-                if (cursor >= n) break;
-                nsel = gather(cursor);
-                if (STATS) nsel_total += nsel;
-            }
-            if (first) {  // no triangle at all
-                for (int r0 = 0; r0 < total; r0 += 32) {
-                    const int q = r0 + lane;
-                    int row, colo;
-                    texel_of(q, row, colo);
-                    if (q < total) store(row, colo, CUDART_INF, -1);
-                }
-            }
-        }
-    } else {
-        // crowded tile: gather the whole overlap list (TC_SEL at a time), sort it by
-        // ascending min depth, stage the nearest TC_RES float32 forms; the walk reads
-        // any later one from global memory.  The nearest certain cover then proves
-        // (V) that every later triangle is behind it, so a texel's walk usually ends
-        // in the first chunk -- nested surfaces cost one sort, not one pass each.
-        float* vb = dv.vbuf + (int64_t)f * W * H;
-        bool first = true;
-        do {
-            int cnt = 0;
-            while (cursor < n && cnt < TC_SEL - 32) {
-                int i = cursor + lane;
-                bool sel = false;
-                if (i < n) {
-                    if (clist) i = clist[i];
-                    const uint2 bbx = segb[i];
-                    const int x0 = bbx.x & 0xffff, x1 = bbx.x >> 16, y0 = bbx.y & 0xffff, y1 = bbx.y >> 16;
-                    sel = !(x1 < xb || x0 > xe || y1 < yb || y0 > ye);
-                }
-                const unsigned bal = __ballot_sync(FULL, sel);
-                if (sel) {
-                    const int at = cnt + __popc(bal & ((1u << lane) - 1u));
-                    SEL[at] = i;
-                    KEY[at] = -__ldg(&segf[i].inv_minw);
-                }
-                cnt += __popc(bal);
-                cursor += 32;
-            }
-            if (STATS) nsel_total += cnt;
-            int P = 32;
-            while (P < cnt) P <<= 1;
-            for (int k = cnt + lane; k < P; k += 32) {
-                KEY[k] = CUDART_INF_F;
-                SEL[k] = -1;
-            }
-            __syncwarp();
-            // warp bitonic sort of (KEY, SEL) ascending, P <= TC_SEL
-            for (int size = 2; size <= P; size <<= 1) {
-                for (int stride = size >> 1; stride > 0; stride >>= 1) {
-                    for (int a = lane; a < P; a += 32) {
-                        const int b = a ^ stride;
-                        if (b > a) {
-                            const float ka = KEY[a], kb = KEY[b];
-                            const int sa = SEL[a], sb = SEL[b];
-                            const bool up = (a & size) == 0;
-                            const bool gt = ka > kb || (ka == kb && sa > sb);
-                            if (gt == up) {
-                                KEY[a] = kb;
-                                KEY[b] = ka;
-                                SEL[a] = sb;
-                                SEL[b] = sa;
-                            }
-                        }
-                    }
-                    __syncwarp();
-                }
-            }
-            const int ns = min(cnt, TC_RES);
-            for (int k = lane; k < ns; k += 32) {
-                const uint4* from = reinterpret_cast<const uint4*>(segf + SEL[k]);
-                uint4* to = reinterpret_cast<uint4*>(&T32[k]);
-#pragma unroll
-                for (int part = 0; part < 6; part++) to[part] = from[part];
-            }
-            __syncwarp();
-            const bool last = cursor >= n;
-            for (int r0 = 0; r0 < total; r0 += 32) {
-                const int q = r0 + lane;
-                const bool valid = q < total;
-                int row, colo;
-                texel_of(q, row, colo);
-                const int64_t at = (int64_t)(yb + row) * W + xb + colo;
-                float V = valid ? (first ? 0.0f : vb[at]) : CUDART_INF_F;
-                double best = (valid && !first) ? dep[at] : CUDART_INF;
-                int bkey = INT_MAX;
-                if (ATTRS && valid && !first) bkey = dv.key[at];
-                if (cnt > 0) walk(cnt, ns, valid, row, colo, V, best, bkey);
-                if (valid) {
-                    dep[at] = best;
-                    if (!last) vb[at] = V;
-                    if (ATTRS) dv.key[at] = best < CUDART_INF ? bkey : -1;
-                }
-            }
-            first = false;
-            __syncwarp();
-        } while (cursor < n);
-    }
-    if (STATS) {
-        const bool l0 = lane == 0;
-        stat_add(dv.stats, GM_STAT_TEXELS, l0 ? (unsigned long long)total : 0ull);
-        stat_add(dv.stats, GM_STAT_TX_TILES, l0 ? 1ull : 0ull);
-        stat_add(dv.stats, GM_STAT_TX_STAGED, l0 ? (unsigned long long)nsel_total : 0ull);
-        stat_add(dv.stats, GM_STAT_TX_LIST, l0 ? (unsigned long long)n : 0ull);
-        stat_add(dv.stats, GM_STAT_TX_ITER, l0 ? c_iter : 0ull);
-        stat_add(dv.stats, GM_STAT_PAIRS, c_pairs);
-        stat_add(dv.stats, GM_STAT_COVERED, c_cov);
-        stat_add(dv.stats, GM_STAT_TX_EDGE, c_edge);
-    }
-}
-
-template <bool ATTRS, bool STATS, bool CROWDED>
-__global__ void TX_BOUNDS k_texels(TriStore ts, DepthView dv, CoarseBins cb, int tiles_x,
-                                   int tiles_per_fix, int64_t n_items,
-                                   const GmFixExact* __restrict__ fixes, long long b0) {
-    extern __shared__ __align__(16) unsigned char tx_dyn[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (*ts.fail <= b0) return;
-    if (!CROWDED) {
-        const int64_t item = (int64_t)blockIdx.x * TW_WARPS + warp;
-        if (item < n_items)
-            texel_item<ATTRS, STATS, false>(reinterpret_cast<TexelWarpSmem*>(tx_dyn)[warp].t32,
-                                            reinterpret_cast<TexelWarpSmem*>(tx_dyn)[warp].sel, nullptr, item, ts, dv,
-                                            cb, tiles_x, tiles_per_fix, fixes);
-        return;
-    }
-    // crowded tiles (deferred by the pass above): persistent warps over the list
-    CrowdedWarpSmem& C = reinterpret_cast<CrowdedWarpSmem*>(tx_dyn)[warp];
-    const int n_crowd = *dv.crowd_count;
-    for (;;) {
-        int w = 0;
-        if (lane == 0) w = atomicAdd(dv.crowd_count + 1, 1);
-        w = __shfl_sync(0xffffffffu, w, 0);
-        if (w >= n_crowd) break;
-        texel_item<ATTRS, STATS, true>(C.t32, C.sel, C.key, dv.crowd[w], ts, dv, cb, tiles_x, tiles_per_fix, fixes);
-    }
-}
+#include "gm_texels.cuh"
 
 // Mark every texel of fixation slot 0 (the kernel-seam full z-buffer port).
 __global__ void k_mark_all(uint32_t* __restrict__ mask, int W, int H, int wwords) {
@@ -2487,345 +1672,7 @@ extern "C" int gm_plan_depth_buffer(gm_plan* p, const double* fx, double theta, 
     return GM_OK;
 }
 
-// ------------------------------------------- general camera: raster + heatmap
-
-// kernels.py:140-192 for triangle t, fan k, at pixel (px, py), with the vertex
-// attributes (identity rows, interpolated along clipped edges, swapped with
-// the winding) -- the with_attrs branch of _raster_tri (:130-137): returns the
-// perspective-correct barycentrics bary[3] the reference stores.  Same float64
-// operation order as the reference (no FMA).
-__device__ bool raster_attrs(const double* tw, const GmFixExact& F, int W, int H, int k, int px, int py,
-                             double bary[3]) {
-    double vin[3][6];
-    for (int v = 0; v < 3; v++) {
-        const double wx = tw[3 * v], wy = tw[3 * v + 1], wz = tw[3 * v + 2];
-        for (int i = 0; i < 3; i++)
-            vin[v][i] = F.rot[3 * i] * wx + F.rot[3 * i + 1] * wy + F.rot[3 * i + 2] * wz + F.trans[i];
-        for (int c = 0; c < 3; c++) vin[v][3 + c] = c == v ? 1.0 : 0.0;
-    }
-    double vout[4][6];
-    int nv = 0;
-    const double nn = F.near_;
-    for (int i = 0; i < 3; i++) {
-        const int j = (i + 1) % 3;
-        const double cz = vin[i][2], nz = vin[j][2];
-        const bool cin = cz <= -nn, nin = nz <= -nn;
-        if (cin) {
-            for (int c = 0; c < 6; c++) vout[nv][c] = vin[i][c];
-            nv++;
-        }
-        if (cin != nin) {
-            const double t = (-nn - cz) / (nz - cz);
-            for (int c = 0; c < 6; c++) vout[nv][c] = vin[i][c] + t * (vin[j][c] - vin[i][c]);
-            nv++;
-        }
-    }
-    if (k > nv - 3) return false;
-    const double half_w = 0.5 * (double)W, half_h = 0.5 * (double)H;
-    double sx[3], sy[3], iw[3], at[3][3];
-    for (int m = 0; m < 3; m++) {
-        const int src = m == 0 ? 0 : k + m;
-        const double x = vout[src][0], y = vout[src][1], z = vout[src][2];
-        const double w = -z;
-        if (w <= 0.0) return false;
-        const double ndc_x = (F.p00 * x + F.p02 * z) / w;
-        const double ndc_y = (F.p11 * y + F.p12 * z) / w;
-        sx[m] = (ndc_x + 1.0) * half_w;
-        sy[m] = (1.0 - ndc_y) * half_h;
-        iw[m] = 1.0 / w;
-        for (int c = 0; c < 3; c++) at[m][c] = vout[src][3 + c];
-    }
-    double area = edge_fn(sx[0], sy[0], sx[1], sy[1], sx[2], sy[2]);
-    if (area == 0.0) return false;
-    if (area < 0.0) {
-        double t;
-        t = sx[1]; sx[1] = sx[2]; sx[2] = t;
-        t = sy[1]; sy[1] = sy[2]; sy[2] = t;
-        t = iw[1]; iw[1] = iw[2]; iw[2] = t;
-        for (int c = 0; c < 3; c++) {
-            t = at[1][c]; at[1][c] = at[2][c]; at[2][c] = t;
-        }
-        area = -area;
-    }
-    const double inv_area = 1.0 / area;
-    const double cx = (double)px + 0.5, cy = (double)py + 0.5;
-    const double w0 = edge_fn(sx[1], sy[1], sx[2], sy[2], cx, cy);
-    const double w1 = edge_fn(sx[2], sy[2], sx[0], sy[0], cx, cy);
-    const double w2 = edge_fn(sx[0], sy[0], sx[1], sy[1], cx, cy);
-    const double l0 = w0 * inv_area, l1 = w1 * inv_area, l2 = w2 * inv_area;
-    const double inv_w = l0 * iw[0] + l1 * iw[1] + l2 * iw[2];
-    const double d = 1.0 / inv_w;
-    for (int c = 0; c < 3; c++) bary[c] = (l0 * at[0][c] * iw[0] + l1 * at[1][c] * iw[1] + l2 * at[2][c] * iw[2]) * d;
-    return true;
-}
-
-// tri_id / bary of every pixel from the winning order key (reference
-// initial values -1 / 0 where nothing is drawn).
-__global__ void k_attrs(const int* __restrict__ key, const double* __restrict__ tw, const GmFixExact* __restrict__ fix,
-                        int W, int H, int32_t* __restrict__ tri_id, double* __restrict__ bary) {
-    const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (q >= (int64_t)W * H) return;
-    const int kk = key[q];
-    double b[3] = {0.0, 0.0, 0.0};
-    int id = -1;
-    if (kk >= 0) {
-        const int t = kk >> 1;
-        if (raster_attrs(tw + 9 * (int64_t)t, fix[0], W, H, kk & 1, (int)(q % W), (int)(q / W), b)) id = t;
-    }
-    tri_id[q] = id;
-    bary[3 * q] = b[0];
-    bary[3 * q + 1] = b[1];
-    bary[3 * q + 2] = b[2];
-}
-
-// render.py:150-182 piecewise-linear field over each triangle's sample grid,
-// then ColorMap.rgb (render.py:44-50: clip, ** gamma, np.interp per channel)
-// and np.round(rgb * 255) -> uint8; background black.
-struct GmColorMap {
-    double xs[16], cols[16][3];
-    int n;
-    double gamma;
-};
-
-__device__ double np_interp(double x, const GmColorMap& cm, int c) {
-    // numpy arr_interp (compiled_base.c) with precomputed slopes
-    const int n = cm.n;
-    if (isnan(x)) return x;
-    if (x < cm.xs[0]) return cm.cols[0][c];
-    if (x > cm.xs[n - 1]) return cm.cols[n - 1][c];
-    int j = 0;
-    while (j + 1 < n && cm.xs[j + 1] <= x) j++;
-    if (j == n - 1) return cm.cols[j][c];
-    if (cm.xs[j] == x) return cm.cols[j][c];
-    const double slope = (cm.cols[j + 1][c] - cm.cols[j][c]) / (cm.xs[j + 1] - cm.xs[j]);
-    double r = slope * (x - cm.xs[j]) + cm.cols[j][c];
-    if (isnan(r)) {
-        r = slope * (x - cm.xs[j + 1]) + cm.cols[j + 1][c];
-        if (isnan(r) && cm.cols[j][c] == cm.cols[j + 1][c]) r = cm.cols[j][c];
-    }
-    return r;
-}
-
-__device__ double np_scalar_power(double v, double g) {
-    // numpy fast_scalar_power special exponents, else libm pow
-    if (g == 1.0) return v;
-    if (g == 2.0) return v * v;
-    if (g == 0.5) return sqrt(v);
-    if (g == -1.0) return 1.0 / v;
-    if (g == 0.0) return 1.0;
-    return pow(v, g);
-}
-
-__global__ void k_heat(const int32_t* __restrict__ tri_id, const double* __restrict__ bary, int64_t npix,
-                       const int64_t* __restrict__ res, const int64_t* __restrict__ base,
-                       const double* __restrict__ values, GmColorMap cm, uint8_t* __restrict__ img) {
-    const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (q >= npix) return;
-    const int t = tri_id[q];
-    if (t < 0) {
-        img[3 * q] = img[3 * q + 1] = img[3 * q + 2] = 0;
-        return;
-    }
-    const double w1 = bary[3 * q], w3 = bary[3 * q + 2];
-    const int64_t ri = res[t];
-    const double rr = (double)ri;
-    const double R = fmin(fmax(rr * (1.0 - w3), 0.0), rr);
-    const double C = fmin(fmax(rr * w1, 0.0), R);
-    int64_t r0 = x86_i64(floor(R));
-    if (r0 > ri - 1) r0 = ri - 1;
-    const double fr = R - (double)r0;
-    int64_t c0 = x86_i64(floor(C));
-    if (c0 > r0) c0 = r0;
-    double fc = C - (double)c0;
-    const bool upper = (fc > fr) && (c0 < r0);
-    if (!upper) fc = fmin(fc, fr);
-    const int64_t b = base[t];
-    auto sv = [&](int64_t row, int64_t col) { return values[b + row * (row + 1) / 2 + col]; };
-    double v;
-    if (!upper) {
-        v = (1.0 - fr) * sv(r0, c0) + (fr - fc) * sv(r0 + 1, c0) + fc * sv(r0 + 1, c0 + 1);
-    } else {
-        int64_t c0u = r0 - 1 > 0 ? r0 - 1 : 0;
-        if (c0 < c0u) c0u = c0;
-        v = (1.0 - fc) * sv(r0, c0u) + (fc - fr) * sv(r0, c0u + 1) + fr * sv(r0 + 1, c0u + 1);
-    }
-    const double x = np_scalar_power(fmin(fmax(v, 0.0), 1.0), cm.gamma);
-    for (int c = 0; c < 3; c++) img[3 * q + c] = (uint8_t)(int)rint(np_interp(x, cm, c) * 255.0);
-}
-
-// kernels.cull_mask (kernels.py:195-216): drop a triangle only when all three
-// vertices are outside one plane (a x + b y + c z + d < 0, no FMA).
-__global__ void k_cull_mask(const double* __restrict__ tris, int64_t T, const double* __restrict__ planes, int np,
-                            uint8_t* __restrict__ keep) {
-    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (t >= T) return;
-    const double* v = tris + 9 * t;
-    uint8_t k = 1;
-    for (int p = 0; p < np; p++) {
-        const double a = planes[4 * p], b = planes[4 * p + 1], c = planes[4 * p + 2], d = planes[4 * p + 3];
-        bool outside = true;
-        for (int q = 0; q < 3; q++)
-            if (a * v[3 * q] + b * v[3 * q + 1] + c * v[3 * q + 2] + d >= 0.0) {
-                outside = false;
-                break;
-            }
-        if (outside) {
-            k = 0;
-            break;
-        }
-    }
-    keep[t] = k;
-}
-
-extern "C" int gm_cull_mask(int device, const double* tris, int64_t T, const double* planes, int n_planes,
-                            uint8_t* keep) {
-    if (T < 0 || (T > 0 && (!tris || !keep)) || n_planes < 0 || n_planes > 64 || (n_planes && !planes))
-        return set_err(GM_ERR_ARG, "bad arguments");
-    if (T == 0) return GM_OK;
-    int rc = use_device(device);
-    if (rc) return rc;
-    double *d_t = nullptr, *d_p = nullptr;
-    uint8_t* d_k = nullptr;
-    CK(cudaMalloc(&d_t, sizeof(double) * 9 * T));
-    CK(cudaMalloc(&d_p, sizeof(double) * 4 * (n_planes + 1)));
-    CK(cudaMalloc(&d_k, (size_t)T));
-    CK(cudaMemcpy(d_t, tris, sizeof(double) * 9 * T, cudaMemcpyHostToDevice));
-    if (n_planes) CK(cudaMemcpy(d_p, planes, sizeof(double) * 4 * n_planes, cudaMemcpyHostToDevice));
-    k_cull_mask<<<blocks_for(T, 256), 256>>>(d_t, T, d_p, n_planes, d_k);
-    CK(cudaGetLastError());
-    CK(cudaMemcpy(keep, d_k, (size_t)T, cudaMemcpyDeviceToHost));
-    cudaFree(d_t); cudaFree(d_p); cudaFree(d_k);
-    return GM_OK;
-}
-
-// A throwaway plan holding world triangles only (no samples).
-static int plan_with_world_tris(int device, const double* tris, int64_t T, gm_plan** out) {
-    int rc = gm_plan_create(device, out);
-    if (rc) return rc;
-    gm_plan* p = *out;
-    p->T = T;
-    p->n_clu = (T + 31) / 32;
-    if (T == 0) return GM_OK;
-    if ((rc = dev_alloc(&p->d_tw, (size_t)T * 9))) return rc;
-    if ((rc = dev_alloc(&p->d_tsph, (size_t)T))) return rc;
-    if ((rc = dev_alloc(&p->d_csph, (size_t)p->n_clu))) return rc;
-    cudaStream_t s = p->stream;
-    CK(cudaMemcpyAsync(p->d_tw, tris, sizeof(double) * 9 * T, cudaMemcpyHostToDevice, s));
-    k_tri_spheres<<<blocks_for(T, 256), 256, 0, s>>>(p->d_tw, T, p->d_tsph);
-    k_group_spheres<<<blocks_for(p->n_clu, 128), 128, 0, s>>>(p->d_tsph, nullptr, nullptr, nullptr, T, p->d_csph, 32);
-    CK(cudaGetLastError());
-    return GM_OK;
-}
-
-static int camera_record(gm_plan* p, const double* rot, const double* trans, double p00, double p11, double p02,
-                         double p12, double near_, double far_) {
-    GmFixExact e;
-    memset(&e, 0, sizeof(e));
-    for (int i = 0; i < 9; i++) e.rot[i] = rot[i];
-    for (int i = 0; i < 3; i++) e.trans[i] = trans[i];
-    e.p00 = p00;
-    e.p11 = p11;
-    e.p02 = p02;
-    e.p12 = p12;
-    e.near_ = near_;
-    e.far_ = far_;
-    GmFixCull c;
-    memset(&c, 0, sizeof(c));
-    c.cos_t = -3.0f;  // no occluder cull: kernels.rasterize sees every triangle it is given
-    c.cos_s = -3.0f;
-    int rc = ensure_batch(p, 1, 1, 1, std::max<int64_t>(p->cap_seg, 4096));
-    if (rc) return rc;
-    CK(cudaMemcpyAsync(p->d_fix, &e, sizeof(e), cudaMemcpyHostToDevice, p->stream));
-    CK(cudaMemcpyAsync(p->d_cull, &c, sizeof(c), cudaMemcpyHostToDevice, p->stream));
-    CK(cudaStreamSynchronize(p->stream));
-    return GM_OK;
-}
-
-extern "C" int gm_rasterize(int device, const double* tris, int64_t T, const double* rot, const double* trans,
-                            double p00, double p11, double p02, double p12, int W, int H, double near_, double far_,
-                            double* depth, int32_t* tri_id, double* bary) {
-    if (T < 0 || (T > 0 && !tris) || !rot || !trans || !depth || W < 1 || H < 1 || W > 65535 || H > 65535 ||
-        T >= (1LL << 28))
-        return set_err(GM_ERR_ARG, "bad arguments");
-    gm_plan* p = nullptr;
-    int rc = plan_with_world_tris(device, tris, T, &p);
-    const bool attrs = tri_id != nullptr || bary != nullptr;
-    int32_t* d_id = nullptr;
-    double* d_bary = nullptr;
-    if (!rc) rc = camera_record(p, rot, trans, p00, p11, p02, p12, near_, far_);
-    if (!rc) rc = raster_pass(p, W, H, attrs);
-    if (!rc && attrs) {
-        const int64_t n = (int64_t)W * H;
-        rc = dev_alloc(&d_id, (size_t)n);
-        if (!rc) rc = dev_alloc(&d_bary, (size_t)n * 3);
-        if (!rc) {
-            k_attrs<<<blocks_for(n, 256), 256, 0, p->stream>>>(p->d_key, p->d_tw, p->d_fix, W, H, d_id, d_bary);
-            if (cudaGetLastError() != cudaSuccess) rc = set_err(GM_ERR_CUDA, "k_attrs launch failed");
-        }
-        if (!rc && tri_id && cudaMemcpyAsync(tri_id, d_id, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, p->stream))
-            rc = set_err(GM_ERR_CUDA, "copy tri_id");
-        if (!rc && bary && cudaMemcpyAsync(bary, d_bary, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, p->stream))
-            rc = set_err(GM_ERR_CUDA, "copy bary");
-    }
-    if (!rc && cudaMemcpyAsync(depth, p->d_depth, sizeof(double) * W * H, cudaMemcpyDeviceToHost, p->stream))
-        rc = set_err(GM_ERR_CUDA, "copy depth");
-    if (p) cudaStreamSynchronize(p->stream);
-    cudaFree(d_id);
-    cudaFree(d_bary);
-    if (p) gm_plan_destroy(p);
-    return rc;
-}
-
-extern "C" int gm_render_heatmap(int device, const double* tris, int64_t T, const double* rot, const double* trans,
-                                 double p00, double p11, double p02, double p12, int W, int H, double near_,
-                                 double far_, const int64_t* res, const int64_t* base, const double* values,
-                                 int64_t N, const double* stops, const double* colors, int n_stops, double gamma,
-                                 uint8_t* img) {
-    if (T < 0 || (T > 0 && (!tris || !res || !base)) || !rot || !trans || !img || W < 1 || H < 1 || W > 65535 ||
-        H > 65535 || n_stops < 2 || n_stops > 16 || !stops || !colors || N < 0 || (N > 0 && !values) ||
-        T >= (1LL << 28))
-        return set_err(GM_ERR_ARG, "bad arguments");
-    GmColorMap cm;
-    memset(&cm, 0, sizeof(cm));
-    cm.n = n_stops;
-    cm.gamma = gamma;
-    for (int i = 0; i < n_stops; i++) {
-        cm.xs[i] = stops[i];
-        for (int c = 0; c < 3; c++) cm.cols[i][c] = colors[3 * i + c];
-    }
-    gm_plan* p = nullptr;
-    int rc = plan_with_world_tris(device, tris, T, &p);
-    const int64_t n = (int64_t)W * H;
-    int32_t* d_id = nullptr;
-    double *d_bary = nullptr, *d_vals = nullptr;
-    int64_t *d_res = nullptr, *d_base = nullptr;
-    uint8_t* d_img = nullptr;
-    if (!rc) rc = camera_record(p, rot, trans, p00, p11, p02, p12, near_, far_);
-    if (!rc) rc = raster_pass(p, W, H, true);
-    if (!rc) rc = dev_alloc(&d_id, (size_t)n);
-    if (!rc) rc = dev_alloc(&d_bary, (size_t)n * 3);
-    if (!rc) rc = dev_alloc(&d_img, (size_t)n * 3);
-    if (!rc) rc = dev_alloc(&d_vals, (size_t)std::max<int64_t>(N, 1));
-    if (!rc) rc = dev_alloc(&d_res, (size_t)std::max<int64_t>(T, 1));
-    if (!rc) rc = dev_alloc(&d_base, (size_t)std::max<int64_t>(T, 1));
-    if (!rc) {
-        cudaStream_t s = p->stream;
-        if (N) cudaMemcpyAsync(d_vals, values, sizeof(double) * N, cudaMemcpyHostToDevice, s);
-        if (T) {
-            cudaMemcpyAsync(d_res, res, sizeof(int64_t) * T, cudaMemcpyHostToDevice, s);
-            cudaMemcpyAsync(d_base, base, sizeof(int64_t) * T, cudaMemcpyHostToDevice, s);
-        }
-        k_attrs<<<blocks_for(n, 256), 256, 0, s>>>(p->d_key, p->d_tw, p->d_fix, W, H, d_id, d_bary);
-        k_heat<<<blocks_for(n, 256), 256, 0, s>>>(d_id, d_bary, n, d_res, d_base, d_vals, cm, d_img);
-        if (cudaGetLastError() != cudaSuccess) rc = set_err(GM_ERR_CUDA, "render kernels failed to launch");
-        if (!rc && cudaMemcpyAsync(img, d_img, (size_t)n * 3, cudaMemcpyDeviceToHost, s))
-            rc = set_err(GM_ERR_CUDA, "copy image");
-        if (!rc && cudaStreamSynchronize(s)) rc = set_err(GM_ERR_CUDA, "render failed");
-    }
-    cudaFree(d_id); cudaFree(d_bary); cudaFree(d_img); cudaFree(d_vals); cudaFree(d_res); cudaFree(d_base);
-    if (p) gm_plan_destroy(p);
-    return rc;
-}
+#include "gm_raster.cuh"
 
 // The NDC-filtered candidate lists (kernels.py:302-319) of F fixations over
 // the plan's samples.  out is F x cap (int64, unsorted within a fixation),

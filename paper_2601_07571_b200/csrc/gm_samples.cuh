@@ -1,0 +1,354 @@
+// gm_samples.cuh -- the sample-major passes (included once by gm_kernels.cu):
+// level-1 super-chunk ballots, the float32 marking pass k_mark and the
+// exact accumulation pass k_samples (kernels.py:288-340).
+#pragma once
+
+// Sample-major pass over a batch of fixations (kernels.py:288-340).  A warp
+// owns 32 consecutive samples; lane l tests fixation g+l against the chunk
+// sphere, the ballot gives the fixations that can touch the chunk, and those
+// are applied in log order.
+//   MARK = true : set the mask bits of the 3x3 texel block depth_match reads
+//                 for every candidate that passes the NDC filter and the cone.
+//   MARK = false: depth_match on those texels and accumulate; the value slot
+//                 lives in a register, so per-sample accumulation order is the
+//                 reference's (density.py:223-226): deterministic, no atomics.
+// The cone test (kernels.py:330-339) runs before depth_match (:326): every
+// condition is conjunctive and side-effect free, so the contributing set and
+// the weights are unchanged.
+// Level 1 of the sample-side fixation cull, once per batch: warp per
+// super-chunk (8 chunks = 256 consecutive samples), lane-parallel sphere tests
+// against all fixations of the batch -> lvl1[sc][g] ballots and the number of
+// fixations that can touch the super-chunk (the work estimate used to order
+// the sample passes, heaviest first).
+__global__ void __launch_bounds__(256) k_level1(const float4* __restrict__ supers, int64_t n_supers,
+                                                const GmFixCull* __restrict__ culls, int B,
+                                                uint32_t* __restrict__ lvl1, int* __restrict__ count,
+                                                int* __restrict__ order, const long long* __restrict__ fail,
+                                                long long b0) {
+    const int lane = threadIdx.x & 31;
+    const int64_t sc = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (sc >= n_supers) return;
+    const int ngroups = (B + 31) >> 5;
+    int total = 0;
+    if (*fail > b0) {
+        const float4 ssph = supers[sc];
+        for (int g = 0; g < ngroups; g++) {
+            const int myf = g * 32 + lane;
+            const unsigned m = __ballot_sync(0xffffffffu, myf < B && sphere_visible(culls[myf], ssph, false));
+            if (lane == 0) lvl1[sc * ngroups + g] = m;
+            total += __popc(m);
+        }
+    }
+    if (lane == 0) {
+        count[sc] = total;
+        order[sc] = (int)sc;
+    }
+}
+
+// float32 view of a fixation for the marking pass, with a rigorous bound E on
+// |camera coordinate in float32 - exact| over every sample of the plan.
+struct __align__(16) GmFixF32 {
+    float rot[9], trans[3], gaze[3];
+    float p00, p11, p02, p12;
+    float near_lo, far_hi;
+    float E;        // absolute bound on the float32 camera-coordinate error (m)
+    float sig16;    // 16 sigma^2 (ratio^2 <= 16 <=> |p x g|^2 <= 16 sigma^2 d1^2)
+};  // 96 B
+
+// float32 copies of the sample positions and max |coordinate| (bit-pattern
+// atomicMax, exact for non-negative doubles)
+__global__ void k_to_f32(const double* __restrict__ px, const double* __restrict__ py, const double* __restrict__ pz,
+                         int64_t N, float* __restrict__ fx, float* __restrict__ fy, float* __restrict__ fz,
+                         unsigned long long* __restrict__ amax) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    double m = 0.0;
+    if (i < N) {
+        const double x = px[i], y = py[i], z = pz[i];
+        fx[i] = (float)x;
+        fy[i] = (float)y;
+        fz[i] = (float)z;
+        m = fmax(fabs(x), fmax(fabs(y), fabs(z)));
+    }
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0 && m > 0.0) atomicMax(amax, (unsigned long long)__double_as_longlong(m));
+}
+
+__global__ void k_fix32(const GmFixExact* __restrict__ ex, int nb, double pmax, double sigma,
+                        GmFixF32* __restrict__ out) {
+    const int f = blockIdx.x * blockDim.x + threadIdx.x;
+    if (f >= nb) return;
+    const GmFixExact& F = ex[f];
+    GmFixF32 o;
+    double tmax = 0.0;
+    for (int i = 0; i < 9; i++) o.rot[i] = (float)F.rot[i];
+    for (int i = 0; i < 3; i++) {
+        o.trans[i] = (float)F.trans[i];
+        o.gaze[i] = (float)F.gaze[i];
+        tmax = fmax(tmax, fabs(F.trans[i]));
+    }
+    o.p00 = (float)F.p00;
+    o.p11 = (float)F.p11;
+    o.p02 = (float)F.p02;
+    o.p12 = (float)F.p12;
+    o.near_lo = (float)F.near_lo;
+    o.far_hi = (float)F.far_hi;
+    // fma chain of 3 products + translation, every operand rounded to float32:
+    // |x32 - x| <= ~8 * 2^-24 * (3 pmax + |t|); E is > 2x that
+    o.E = (float)(1e-6 * (3.0 * pmax + tmax) + 1e-30);
+    o.sig16 = (float)(16.0 * sigma * sigma);
+    out[f] = o;
+}
+
+// The marking pass: for every (sample, fixation) that can be a depth-test
+// candidate (kernels.py:305-339: NDC crop filter and 4-sigma cone), set the
+// mask bits of the texels depth_match may read.  Float32 with rigorous error
+// bounds -- a superset of the exact candidates and of their exact 3x3 blocks
+// (rint is monotone: the exact rint(g) lies in [rint(g32 - dg), rint(g32 + dg)])
+// -- and the exact float64 computation for the rare lanes whose bounds are too
+// loose (samples within ~E of the camera plane).  Marking extra texels only
+// costs texel work; every texel an exact depth test reads is marked.
+__global__ void KM_BOUNDS k_mark(const float* __restrict__ pxf, const float* __restrict__ pyf,
+                                              const float* __restrict__ pzf, const double* __restrict__ px,
+                                              const double* __restrict__ py, const double* __restrict__ pz,
+                                              const float4* __restrict__ chunks, const uint32_t* __restrict__ lvl1,
+                                              const int* __restrict__ order, int* __restrict__ work, int64_t N,
+                                              int64_t n_chunks, int64_t n_supers, const GmFixExact* __restrict__ fixes,
+                                              const GmFixF32* __restrict__ fix32, const GmFixCull* __restrict__ culls,
+                                              int B, DepthView dv, double inv_sigma, uint32_t* __restrict__ cbits,
+                                              const long long* __restrict__ fail, long long b0) {
+    if (*fail <= b0) return;
+    const int lane = threadIdx.x & 31;
+    const int ngroups = (B + 31) >> 5;
+    const int W = dv.W, H = dv.H;
+    const float Wf = (float)W, Hf = (float)H;
+    const float lo = -1.0f - (float)GM_NDC_SLACK, hi = 1.0f + (float)GM_NDC_SLACK;
+    const int64_t n_items = n_supers * 8;
+    for (;;) {
+        int item = 0;
+        if (lane == 0) item = atomicAdd(work, 1);
+        item = __shfl_sync(0xffffffffu, item, 0);
+        if (item >= n_items) break;
+        const int64_t sc = order[item >> 3];
+        const int64_t ch = sc * 8 + (item & 7);
+        if (ch >= n_chunks) continue;
+        const unsigned l1 = lane < ngroups ? lvl1[sc * ngroups + lane] : 0u;
+        if (!__any_sync(0xffffffffu, l1 != 0u)) continue;
+        const int64_t i = ch * 32 + lane;
+        const bool valid = i < N;
+        float wx = 0.0f, wy = 0.0f, wz = 0.0f;
+        if (valid) {
+            wx = pxf[i];
+            wy = pyf[i];
+            wz = pzf[i];
+        }
+        const float4 sph = chunks[ch];
+        for (int gi = 0; gi < ngroups; gi++) {
+            const unsigned sm = __shfl_sync(0xffffffffu, l1, gi);
+            if (!sm) continue;
+            const int g = gi * 32;
+            const bool pass = ((sm >> lane) & 1u) && sphere_visible(culls[g + lane], sph, false);
+            unsigned mask = __ballot_sync(0xffffffffu, pass);
+            unsigned my_bits = 0;  // fixations (bit j of group gi) for which this lane is a candidate
+            while (mask) {
+                const int j = __ffs(mask) - 1;
+                mask &= mask - 1;
+                if (!valid) continue;
+                const int f = g + j;
+                const GmFixF32& Q = fix32[f];
+                const float E = Q.E;
+                const float x = __fmaf_rn(Q.rot[2], wz, __fmaf_rn(Q.rot[1], wy, __fmaf_rn(Q.rot[0], wx, Q.trans[0])));
+                const float y = __fmaf_rn(Q.rot[5], wz, __fmaf_rn(Q.rot[4], wy, __fmaf_rn(Q.rot[3], wx, Q.trans[1])));
+                const float z = __fmaf_rn(Q.rot[8], wz, __fmaf_rn(Q.rot[7], wy, __fmaf_rn(Q.rot[6], wx, Q.trans[2])));
+                const float w = -z;
+                if (w + E <= 0.0f) continue;                               // exact w <= 0
+                if (w + E < Q.near_lo || w - E > Q.far_hi) continue;      // exact depth outside the slab
+                const float wl = w - E;
+                float bxlo, bxhi, bylo, byhi;  // range of the exact g (texel coordinates)
+                bool exact = !(wl > 1e-3f * fabsf(w) + 1e-12f);
+                if (!exact) {
+                    // NDC (kernels.py:314-319) with bound dq on |q32 - q_exact|
+                    const float nx = __fmaf_rn(Q.p00, x, Q.p02 * z), ny = __fmaf_rn(Q.p11, y, Q.p12 * z);
+                    const float qx = nx / w, qy = ny / w;
+                    const float en_x = (fabsf(Q.p00) + fabsf(Q.p02)) * E + 4e-7f * (fabsf(Q.p00 * x) + fabsf(Q.p02 * z));
+                    const float en_y = (fabsf(Q.p11) + fabsf(Q.p12)) * E + 4e-7f * (fabsf(Q.p11 * y) + fabsf(Q.p12 * z));
+                    const float dqx = (en_x + fabsf(qx) * E) / wl + 1e-6f * fabsf(qx) + 1e-7f;
+                    const float dqy = (en_y + fabsf(qy) * E) / wl + 1e-6f * fabsf(qy) + 1e-7f;
+                    if (qx + dqx < lo || qx - dqx > hi || qy + dqy < lo || qy - dqy > hi) continue;
+                    // cone (kernels.py:330-339): d1 > 0 and ratio^2 <= 16
+                    const float d1 = __fmaf_rn(x, Q.gaze[0], __fmaf_rn(y, Q.gaze[1], z * Q.gaze[2]));
+                    const float ed1 = 2.0f * E + 4e-7f * (fabsf(x) + fabsf(y) + fabsf(z));
+                    if (d1 + ed1 <= 0.0f) continue;
+                    const float cx3 = y * Q.gaze[2] - z * Q.gaze[1], cy3 = z * Q.gaze[0] - x * Q.gaze[2];
+                    const float cz3 = x * Q.gaze[1] - y * Q.gaze[0];
+                    const float cr = sqrtf(__fmaf_rn(cx3, cx3, __fmaf_rn(cy3, cy3, cz3 * cz3)));
+                    const float ecr = 3.0f * E + 1e-6f * (fabsf(x) + fabsf(y) + fabsf(z));
+                    const float crl = cr - ecr, d1h = d1 + ed1;
+                    if (crl > 0.0f && crl * crl > Q.sig16 * (1.0f + 1e-4f) * d1h * d1h) continue;
+                    const float gx = (qx + 1.0f) * 0.5f * Wf - 0.5f, gy = (1.0f - qy) * 0.5f * Hf - 0.5f;
+                    const float dgx = dqx * 0.5f * Wf + 1e-4f + 1e-6f * fabsf(gx);
+                    const float dgy = dqy * 0.5f * Hf + 1e-4f + 1e-6f * fabsf(gy);
+                    if (dgx > 2.0f || dgy > 2.0f) {
+                        exact = true;
+                    } else {
+                        bxlo = gx - dgx;
+                        bxhi = gx + dgx;
+                        bylo = gy - dgy;
+                        byhi = gy + dgy;
+                    }
+                }
+                int cxlo, cxhi, cylo, cyhi;
+                if (exact) {
+                    // the exact float64 test of k_samples, for this lane only
+                    const GmFixExact& F = fixes[f];
+                    const double X = px[i], Y = py[i], Z = pz[i];
+                    const double xx = F.rot[0] * X + F.rot[1] * Y + F.rot[2] * Z + F.trans[0];
+                    const double yy = F.rot[3] * X + F.rot[4] * Y + F.rot[5] * Z + F.trans[1];
+                    const double zz = F.rot[6] * X + F.rot[7] * Y + F.rot[8] * Z + F.trans[2];
+                    const double ww = -zz;
+                    if (ww <= 0.0 || ww < F.near_lo || ww > F.far_hi) continue;
+                    const double ndx = (F.p00 * xx + F.p02 * zz) / ww, ndy = (F.p11 * yy + F.p12 * zz) / ww;
+                    const double l = -1.0 - GM_NDC_SLACK, h = 1.0 + GM_NDC_SLACK;
+                    if (ndx < l || ndx > h || ndy < l || ndy > h) continue;
+                    const double d1 = xx * F.gaze[0] + yy * F.gaze[1] + zz * F.gaze[2];
+                    if (d1 <= 0.0) continue;
+                    double d2sq = xx * xx + yy * yy + zz * zz - d1 * d1;
+                    if (d2sq < 0.0) d2sq = 0.0;
+                    if (d2sq * inv_sigma * inv_sigma / (d1 * d1) > 16.0) continue;
+                    const double gxe = (ndx + 1.0) * 0.5 * (double)W - 0.5, gye = (1.0 - ndy) * 0.5 * (double)H - 0.5;
+                    long long rx = x86_i64(rint(gxe)), ry = x86_i64(rint(gye));
+                    cxlo = cxhi = (int)max(min(rx, (long long)W - 1), 0LL);
+                    cylo = cyhi = (int)max(min(ry, (long long)H - 1), 0LL);
+                } else {
+                    cxlo = (int)fminf(fmaxf(rintf(bxlo), 0.0f), (float)(W - 1));
+                    cxhi = (int)fminf(fmaxf(rintf(bxhi), 0.0f), (float)(W - 1));
+                    cylo = (int)fminf(fmaxf(rintf(bylo), 0.0f), (float)(H - 1));
+                    cyhi = (int)fminf(fmaxf(rintf(byhi), 0.0f), (float)(H - 1));
+                }
+                const int bx0 = max(cxlo - 1, 0), bx1 = min(cxhi + 1, W - 1);
+                const int by0 = max(cylo - 1, 0), by1 = min(cyhi + 1, H - 1);
+                my_bits |= 1u << j;
+                uint32_t* m = dv.mask + (int64_t)f * H * dv.wwords;
+                const unsigned long long bits = ((1ull << (bx1 - bx0 + 1)) - 1ull) << (bx0 & 31);
+                const int w0 = bx0 >> 5;
+                for (int yy = by0; yy <= by1; yy++) {
+                    uint32_t* row = m + (int64_t)yy * dv.wwords + w0;
+                    atomicOr(row, (uint32_t)bits);
+                    if (bits >> 32) atomicOr(row + 1, (uint32_t)(bits >> 32));
+                }
+            }
+            // level 3 for the accumulation pass: the fixations of this group with at
+            // least one (float32-superset) candidate in this chunk
+            const unsigned word = __reduce_or_sync(0xffffffffu, my_bits);
+            if (lane == 0) cbits[ch * 32 + gi] = word;
+        }
+    }
+}
+
+template <bool STATS>
+__global__ void KS_BOUNDS k_samples(const double* __restrict__ px, const double* __restrict__ py,
+                                                 const double* __restrict__ pz, const float4* __restrict__ chunks,
+                                                 const uint32_t* __restrict__ lvl1, const int* __restrict__ order,
+                                                 int* __restrict__ work, int64_t N, int64_t n_chunks,
+                                                 int64_t n_supers, const GmFixExact* __restrict__ fixes,
+                                                 const GmFixCull* __restrict__ culls, int B, DepthView dv,
+                                                 double inv_sigma, double eps_abs, double eps_rel,
+                                                 double* __restrict__ values, const uint32_t* __restrict__ cbits,
+                                                 const long long* __restrict__ fail, long long b0) {
+    if (*fail <= b0) return;  // this batch overflowed the triangle store: the host redoes it
+    const int lane = threadIdx.x & 31;
+    const int ngroups = (B + 31) >> 5;  // <= 32 (B <= GM_MAX_BATCH)
+    const int W = dv.W, H = dv.H;
+    const double Wd = (double)W, Hd = (double)H;
+    const double lo = -1.0 - GM_NDC_SLACK, hi = 1.0 + GM_NDC_SLACK;
+    const int64_t n_items = n_supers * 8;
+    unsigned c_l1 = 0, c_l2 = 0, c_exact = 0, c_ndc = 0, c_cand = 0, c_vis = 0;
+    // persistent warps; items = chunks of the super-chunks in descending-work
+    // order (k_level1 + radix sort), claimed one at a time
+    for (;;) {
+        int item = 0;
+        if (lane == 0) item = atomicAdd(work, 1);
+        item = __shfl_sync(0xffffffffu, item, 0);
+        if (item >= n_items) break;
+        const int64_t sc = order[item >> 3];
+        const int64_t ch = sc * 8 + (item & 7);
+        if (ch >= n_chunks) continue;
+        const unsigned l1 = lane < ngroups ? lvl1[sc * ngroups + lane] : 0u;  // lane g: group g
+        if (STATS) c_l1 += 1;
+        if (!__any_sync(0xffffffffu, l1 != 0u)) continue;
+        {
+        const int64_t i = ch * 32 + lane;
+        const bool valid = i < N;
+        double wx = 0.0, wy = 0.0, wz = 0.0, v = 0.0;
+        if (valid) {
+            wx = px[i];
+            wy = py[i];
+            wz = pz[i];
+            v = values[i];
+        }
+        for (int gi = 0; gi < ngroups; gi++) {
+            const unsigned sm = __shfl_sync(0xffffffffu, l1, gi);
+            if (!sm) continue;
+            const int g = gi * 32;
+            // levels 2 + 3 (k_mark): the fixations of this group with a candidate in the chunk
+            if (STATS) c_l2 += (sm >> lane) & 1u;
+            unsigned mask = cbits[ch * 32 + gi];
+            while (mask) {
+                const int j = __ffs(mask) - 1;
+                mask &= mask - 1;
+                if (!valid) continue;
+                const int f = g + j;
+                const GmFixExact& F = fixes[f];
+                if (STATS) c_exact++;
+                // kernels.py:305-319
+                double x = F.rot[0] * wx + F.rot[1] * wy + F.rot[2] * wz + F.trans[0];
+                double y = F.rot[3] * wx + F.rot[4] * wy + F.rot[5] * wz + F.trans[1];
+                double z = F.rot[6] * wx + F.rot[7] * wy + F.rot[8] * wz + F.trans[2];
+                double w = -z;
+                if (w <= 0.0) continue;
+                double d = w;
+                if (d < F.near_lo || d > F.far_hi) continue;
+                double ndc_x = (F.p00 * x + F.p02 * z) / w;
+                double ndc_y = (F.p11 * y + F.p12 * z) / w;
+                if (ndc_x < lo || ndc_x > hi) continue;
+                if (ndc_y < lo || ndc_y > hi) continue;
+                if (STATS) c_ndc++;
+                // kernels.py:330-339 (moved before the depth test)
+                double d1 = x * F.gaze[0] + y * F.gaze[1] + z * F.gaze[2];
+                if (d1 <= 0.0) continue;
+                double d2sq = x * x + y * y + z * z - d1 * d1;
+                if (d2sq < 0.0) d2sq = 0.0;
+                double ratio_sq = d2sq * inv_sigma * inv_sigma / (d1 * d1);
+                if (ratio_sq > 16.0) continue;
+                if (STATS) c_cand++;
+                // texel coordinates (kernels.py:327, :231-232, :267-276)
+                double gx = (ndc_x + 1.0) * 0.5 * Wd - 0.5;
+                double gy = (1.0 - ndc_y) * 0.5 * Hd - 0.5;
+                long long cx = x86_i64(rint(gx));
+                if (cx < 0) cx = 0;
+                else if (cx > W - 1) cx = W - 1;
+                long long cy = x86_i64(rint(gy));
+                if (cy < 0) cy = 0;
+                else if (cy > H - 1) cy = H - 1;
+                int bx0 = (int)max(cx - 1, 0LL), bx1 = (int)min(cx + 1, (long long)W - 1);
+                int by0 = (int)max(cy - 1, 0LL), by1 = (int)min(cy + 1, (long long)H - 1);
+                // kernels.py:323-329
+                double eps = eps_abs;
+                if (eps_rel * d > eps) eps = eps_rel * d;
+                if (!depth_test(dv, f, gx, gy, bx0, bx1, by0, by1, d, eps)) continue;
+                if (STATS) c_vis++;
+                v += F.amp * exp(-0.5 * ratio_sq);  // kernels.py:340
+            }
+        }
+        if (valid) values[i] = v;
+        }
+    }
+    if (STATS) {
+        stat_add(dv.stats, GM_STAT_L1_TESTS, lane == 0 ? c_l1 * (unsigned long long)B : 0ull);
+        stat_add(dv.stats, GM_STAT_L2_TESTS, c_l2);
+        stat_add(dv.stats, GM_STAT_EXACT, c_exact);
+        stat_add(dv.stats, GM_STAT_NDC, c_ndc);
+        stat_add(dv.stats, GM_STAT_CANDIDATES, c_cand);
+        stat_add(dv.stats, GM_STAT_VISIBLE, c_vis);
+    }
+}
+

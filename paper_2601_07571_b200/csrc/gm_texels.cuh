@@ -1,0 +1,479 @@
+// gm_texels.cuh -- k_texels, the marked z-buffer texels (included once by
+// gm_kernels.cu): per (fixation, 32x16 tile) selection of the writing
+// triangle in float32 with rigorous bounds, exact float64 evaluation of the
+// survivors (kernels.py:67-137), and the sorted pass for crowded tiles.
+#pragma once
+
+#define TW_CAP 32
+#define TW_SEL 128  // overlapping triangles remembered per tile (more: rescanned per round)
+#ifndef TW_WARPS
+#define TW_WARPS 2  // warps (independent tile items) per k_texels CTA
+#endif
+struct __align__(16) TexelWarpSmem {
+    TriF32 t32[TW_CAP];  // staged, in ascending min-depth order
+    int sel[TW_SEL + 32];
+};
+#define TX_DYN_SMEM (TW_WARPS * (int)sizeof(TexelWarpSmem))
+#define TC_SEL 512   // crowded tiles: overlap list sorted per pass (longer lists: several passes)
+#define TC_RES 64    // crowded tiles: nearest triangles staged in shared memory
+struct __align__(16) CrowdedWarpSmem {
+    TriF32 t32[TC_RES];
+    int sel[TC_SEL];
+    float key[TC_SEL];
+};
+#ifndef TC_WARPS
+#define TC_WARPS 4  // warps per CTA of the crowded pass
+#endif
+#ifndef CROWD_DEPTH
+#define CROWD_DEPTH 10  // ... and whose triangle bboxes cover the tile more than this many times
+#endif
+#ifndef CROWD_MIN
+#define CROWD_MIN 128  // tiles overlapping more triangles than this go to the crowded pass
+#endif
+#define TC_DYN_SMEM (TC_WARPS * (int)sizeof(CrowdedWarpSmem))
+#define TX_MAX_THREADS (32 * (TW_WARPS > TC_WARPS ? TW_WARPS : TC_WARPS))
+
+// position of the k-th (0-based) set bit of w (k < popc(w))
+__device__ __forceinline__ int kth_set_bit(uint32_t w, int k) {
+    int base = 0;
+#pragma unroll
+    for (int half = 16; half >= 1; half >>= 1) {
+        const uint32_t low = w & ((1u << half) - 1u);
+        const int c = __popc(low);
+        if (k >= c) {
+            k -= c;
+            w >>= half;
+            base += half;
+        } else {
+            w = low;
+        }
+    }
+    return base;
+}
+
+// Fixation-major evaluation of the marked texels.  Every warp is an
+// independent work item (fixation, 32x16-pixel tile): no CTA barriers, no
+// atomics, per-texel state in registers.
+//   1. the tile's triangles are gathered from its coarse bin (bbox-filtered);
+//   2. their float32 forms (TriF32, built once per screen triangle by
+//      k_tri_setup: edge-function and inverse-depth planes with rigorous error
+//      bounds) are staged in the warp's shared slice TW_CAP at a time, in
+//      ascending min-depth order;
+//   3. lanes take the marked texels (compacted, 32 per round) and walk the
+//      sorted triangles with uniform float32 tests: "certainly written"
+//      (inside by more than the bound, inverse depth certainly within
+//      (1/far', 1/near')) or "maybe written".  V, the largest certain lower
+//      bound of the inverse depth, proves depth <= 1/V, so a maybe-triangle
+//      whose inverse-depth upper bound is < V can never be the minimum, and
+//      once a triangle's 1/minw bound is < V no later one can be (stop);
+//   4. the surviving candidates (normally one) are evaluated exactly with the
+//      reference's float64 pixel arithmetic (texel_depth, float64 record read
+//      from L1/L2) and the minimum is stored -- the value kernels.rasterize
+//      leaves in that pixel.
+// One (fixation, tile) work item of k_texels.  T32/SEL: the warp's staging and
+// selection slices; KEY (crowded mode only): sort keys of SEL.
+template <bool ATTRS, bool STATS, bool CROWDED>
+__device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __restrict__ SEL, float* __restrict__ KEY,
+                                           int64_t item, const TriStore& ts, const DepthView& dv,
+                                           const CoarseBins& cb, int tiles_x, int tiles_per_fix,
+                                           const GmFixExact* __restrict__ fixes) {
+    const int lane = threadIdx.x & 31;
+    const int f = (int)(item / tiles_per_fix);
+    const int tile = (int)(item - (int64_t)f * tiles_per_fix);
+    const int W = dv.W, H = dv.H;
+    const int xb = (tile % tiles_x) * TW, yb = (tile / tiles_x) * TH;
+    const unsigned FULL = 0xffffffffu;
+    // marked texels: lane r < TH holds the mask word of row yb + r
+    uint32_t wr = 0;
+    if (lane < TH && yb + lane < H) wr = dv.mask[((int64_t)f * H + yb + lane) * dv.wwords + (xb >> 5)];
+    const int cnt_r = __popc(wr);
+    int pref = cnt_r;  // inclusive prefix over rows
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(FULL, pref, o);
+        if (lane >= o) pref += v;
+    }
+    const int total = __shfl_sync(FULL, pref, 31);
+    if (total == 0) return;
+    const int pref_ex = pref - cnt_r;
+    const GmFixExact& F = fixes[f];
+    const double near_ = F.near_, far_ = F.far_;
+    // written iff near' <= 1/inv_w <= far' (kernels.py:123-127): certainly inside
+    // [inv_far_hi, inv_near_lo], certainly outside beyond [inv_far_lo, inv_near_hi]
+    const float inv_near = (float)(1.0 / near_), inv_far = (float)(1.0 / far_);
+    const float inv_near_lo = inv_near * (1.0f - 1e-5f), inv_near_hi = inv_near * (1.0f + 1e-5f);
+    const float inv_far_lo = inv_far * (1.0f - 1e-5f), inv_far_hi = inv_far * (1.0f + 1e-5f);
+    const GmScreenTri* seg = ts.tris + (int64_t)f * ts.cap_seg;
+    const uint2* segb = ts.bbox + (int64_t)f * ts.cap_seg;
+    const int* clist = nullptr;
+    int n = min(ts.count[f], (int)ts.cap_seg);
+    if (!cb.ovf[f]) {
+        const int* off = cb.off + (int64_t)f * (GM_MAX_CBINS + 1);
+        const int bb = (yb >> cb.shift) * cb.ncx + (xb >> cb.shift);
+        clist = cb.items + (int64_t)f * cb.cap_items + off[bb];
+        n = off[bb + 1] - off[bb];
+    }
+    const int xe = xb + TW - 1, ye = yb + TH - 1;
+    unsigned long long c_pairs = 0, c_cov = 0, c_iter = 0, c_edge = 0;
+
+    // 1. triangles overlapping the tile -> S.sel (scan cursor resumes if > TW_SEL)
+    int cover = 0;  // this lane's share of the selected bboxes' area inside the tile (depth complexity)
+    auto gather = [&](int& cursor) {
+        int cnt = 0;
+        while (cursor < n && cnt < TW_SEL) {
+            int i = cursor + lane;
+            bool sel = false;
+            if (i < n) {
+                if (clist) i = clist[i];
+                const uint2 bbx = segb[i];
+                const int x0 = bbx.x & 0xffff, x1 = bbx.x >> 16, y0 = bbx.y & 0xffff, y1 = bbx.y >> 16;
+                sel = !(x1 < xb || x0 > xe || y1 < yb || y0 > ye);
+                if (sel) cover += (min(x1, xe) - max(x0, xb) + 1) * (min(y1, ye) - max(y0, yb) + 1);
+            }
+            const unsigned bal = __ballot_sync(FULL, sel);
+            if (sel) SEL[cnt + __popc(bal & ((1u << lane) - 1u))] = i;
+            cnt += __popc(bal);
+            cursor += 32;
+        }
+        __syncwarp();
+        return cnt;  // may exceed TW_SEL by < 32 (S.sel has the room)
+    };
+
+    // 2. stage SEL[c0 .. c0 + kend) (float32 forms) in ascending min-depth order
+    const TriF32* segf = ts.t32 + (int64_t)f * ts.cap_seg;
+    auto stage = [&](int c0, int kend) {
+        __syncwarp();
+        const int gi = lane < kend ? SEL[c0 + lane] : 0;
+        float key = lane < kend ? -__ldg(&segf[gi].inv_minw) : CUDART_INF_F;  // ascending min depth
+        int slot = lane;
+#pragma unroll
+        for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+            for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                const float ok = __shfl_xor_sync(FULL, key, stride);
+                const int os = __shfl_xor_sync(FULL, slot, stride);
+                const bool keep_min = ((lane & stride) == 0) == ((lane & size) == 0);
+                const bool less = ok < key || (ok == key && os < slot);
+                if (keep_min ? less : !less && !(ok == key && os == slot)) {
+                    key = ok;
+                    slot = os;
+                }
+            }
+        }
+        // lane = rank; it copies the record of sorted position `lane`
+        const int src = __shfl_sync(FULL, gi, slot);
+        if (lane < kend) {
+            const uint4* from = reinterpret_cast<const uint4*>(segf + src);
+            uint4* to = reinterpret_cast<uint4*>(&T32[lane]);
+#pragma unroll
+            for (int part = 0; part < 6; part++) to[part] = from[part];
+        }
+        __syncwarp();
+    };
+
+    // texel of compact id q: (row, tile-local column)
+    auto texel_of = [&](int q, int& row, int& colo) {
+        row = 0;
+#pragma unroll
+        for (int step = TH / 2; step > 0; step >>= 1) {
+            const int cand = row + step;
+            const int pc = __shfl_sync(FULL, pref_ex, cand & 31);
+            if (cand < TH && pc <= q) row = cand;
+        }
+        const uint32_t w_row = __shfl_sync(FULL, wr, row);
+        const int k_in_row = q - __shfl_sync(FULL, pref_ex, row);
+        colo = q < total ? kth_set_bit(w_row, k_in_row) : 0;
+    };
+
+    // 3 + 4 for the staged chunk (kend triangles) and one texel: updates V, best
+    // kernels.py:128-129 writes iff d < depth[py, px]: among equal minima the
+    // first triangle in rasterization order (key 2 t + fan) owns the texel
+    auto take = [&](double d, int cs, double& best, int& bkey) {
+        if (!ATTRS) {
+            if (d < best) best = d;
+            return;
+        }
+        const int key = (int)(seg[cs].tl >> 3);
+        if (d < best || (d == best && d < CUDART_INF && key < bkey)) {
+            best = d;
+            bkey = key;
+        }
+    };
+    // triangle kk of the walk: staged in shared memory (kk < nst) or, crowded mode, from global
+    auto tri_at = [&](int kk, int nst) -> const TriF32& { return (!CROWDED || kk < nst) ? T32[kk] : segf[SEL[kk]]; };
+    auto walk = [&](int kend, int nst, bool valid, int row, int colo, float& V, double& best, int& bkey) {
+        const int px = xb + colo, py = yb + row;
+        int cs0 = -1, cs1 = -1;  // exact candidates (global record index) and their bounds
+        float ch0 = 0.0f, ch1 = 0.0f;
+        bool overflow = false;
+        for (int kk = 0; kk < kend; kk++) {
+            const TriF32& t = tri_at(kk, nst);
+            const float inv_minw = t.inv_minw;
+            if (__all_sync(FULL, !(inv_minw >= V))) break;  // nothing later can be nearer
+            if (STATS) c_iter++;
+            const uint32_t tbx = t.bx, tby = t.by;
+            if (!(inv_minw >= V) || px < (int)(tbx & 0xffff) || px > (int)(tbx >> 16) || py < (int)(tby & 0xffff) ||
+                py > (int)(tby >> 16))
+                continue;
+            if (STATS) c_edge++;
+            const float fx = (float)(px - t.ox) + 0.5f, fy = (float)(py - t.oy) + 0.5f;  // bbox-local centre
+            bool maybe = true, certain = true;
+#pragma unroll
+            for (int i = 0; i < 3; i++) {
+                const float e = __fmaf_rn(t.a[i], fx, __fmaf_rn(t.b[i], fy, t.c[i]));
+                maybe = maybe && (e >= -t.tol[i]);
+                certain = certain && (e > t.tol[i]);
+            }
+            if (!maybe) continue;
+            const float iwv = __fmaf_rn(t.A, fx, __fmaf_rn(t.B, fy, t.C));
+            const float lo = iwv - t.tolw, hi = iwv + t.tolw;
+            if (!(hi > 0.0f) || lo > inv_near_hi || hi < inv_far_lo) continue;  // certainly not written
+            if (certain && lo > 0.0f && hi <= inv_near_lo && lo >= inv_far_hi && lo * (1.0f - 1e-6f) > V)
+                V = lo * (1.0f - 1e-6f);
+            if (hi >= V) {
+                if (cs0 < 0) {
+                    cs0 = t.gidx;
+                    ch0 = hi;
+                } else if (cs1 < 0) {
+                    cs1 = t.gidx;
+                    ch1 = hi;
+                } else if (ch0 < V) {  // a stale candidate can be replaced
+                    cs0 = t.gidx;
+                    ch0 = hi;
+                } else if (ch1 < V) {
+                    cs1 = t.gidx;
+                    ch1 = hi;
+                } else {
+                    overflow = true;
+                }
+            }
+        }
+        if (!valid) return;
+        if (!overflow) {
+            if (cs0 >= 0 && ch0 >= V) {
+                const double d = texel_depth(seg[cs0], px, py, near_, far_);
+                if (STATS) c_pairs++;
+                if (STATS) c_cov += d < CUDART_INF;
+                take(d, cs0, best, bkey);
+            }
+            if (cs1 >= 0 && ch1 >= V) {
+                const double d = texel_depth(seg[cs1], px, py, near_, far_);
+                if (STATS) c_pairs++;
+                if (STATS) c_cov += d < CUDART_INF;
+                take(d, cs1, best, bkey);
+            }
+        } else {  // slow path: every staged triangle whose bbox covers the texel
+            for (int k = 0; k < kend; k++) {
+                const TriF32& t = tri_at(k, nst);
+                if (px < (int)(t.bx & 0xffff) || px > (int)(t.bx >> 16) || py < (int)(t.by & 0xffff) ||
+                    py > (int)(t.by >> 16))
+                    continue;
+                const double d = texel_depth(seg[t.gidx], px, py, near_, far_);
+                if (STATS) c_pairs++;
+                if (STATS) c_cov += d < CUDART_INF;
+                take(d, t.gidx, best, bkey);
+            }
+        }
+    };
+
+    double* dep = dv.depth + (int64_t)f * W * H;
+    int cursor = 0;
+    int nsel_total = 0;
+    auto store = [&](int row, int colo, double best, int bkey) {
+        dep[(int64_t)(yb + row) * W + xb + colo] = best;
+        if (ATTRS) dv.key[(int64_t)(yb + row) * W + xb + colo] = best < CUDART_INF ? bkey : -1;
+    };
+    if (!CROWDED) {
+        int nsel = gather(cursor);
+        if (STATS) nsel_total = nsel;
+        // deep tiles (overlapping surfaces: the selected bboxes cover the tile more than
+        // CROWD_DEPTH times) profit from the sorted crowded pass; wide ones (many
+        // side-by-side triangles) stay here
+        if ((cursor < n || nsel > CROWD_MIN) && dv.crowd &&
+            __reduce_add_sync(FULL, (unsigned)cover) > (unsigned)(CROWD_DEPTH * TW * TH)) {
+            // more than TW_CAP triangles: k_texels<CROWDED> sorts the whole list (deferred)
+            if (lane == 0) dv.crowd[atomicAdd(dv.crowd_count, 1)] = (int)item;
+            return;
+        }
+        if (cursor >= n && nsel <= TW_CAP) {
+            // common case: one staging serves every round, per-texel state in registers
+            if (nsel > 0) stage(0, nsel);
+            for (int r0 = 0; r0 < total; r0 += 32) {
+                const int q = r0 + lane;
+                const bool valid = q < total;
+                int row, colo;
+                texel_of(q, row, colo);
+                float V = valid ? 0.0f : CUDART_INF_F;
+                double best = CUDART_INF;
+                int bkey = INT_MAX;
+                if (nsel > 0) walk(nsel, nsel, valid, row, colo, V, best, bkey);
+                if (valid) store(row, colo, best, bkey);
+            }
+        } else {
+            // many triangles without a deferral list: chunk by chunk (each staged once),
+            // per-texel state kept in the depth array and the inverse-depth-bound buffer
+            float* vb = dv.vbuf + (int64_t)f * W * H;
+            bool first = true;
+            while (true) {
+                for (int c0 = 0; c0 < nsel; c0 += TW_CAP) {
+                    const int kend = min(TW_CAP, nsel - c0);
+                    stage(c0, kend);
+                    for (int r0 = 0; r0 < total; r0 += 32) {
+                        const int q = r0 + lane;
+                        const bool valid = q < total;
+                        int row, colo;
+                        texel_of(q, row, colo);
+                        const int64_t at = (int64_t)(yb + row) * W + xb + colo;
+                        float V = valid ? (first ? 0.0f : vb[at]) : CUDART_INF_F;
+                        double best = (valid && !first) ? dep[at] : CUDART_INF;
+                        int bkey = INT_MAX;
+                        if (ATTRS && valid && !first) bkey = dv.key[at];
+                        walk(kend, kend, valid, row, colo, V, best, bkey);
+                        if (valid) {
+                            dep[at] = best;
+                            vb[at] = V;
+                            if (ATTRS) dv.key[at] = best < CUDART_INF ? bkey : -1;
+                        }
+                    }
+                    first = false;
+                }
+                if (cursor >= n) break;
+                nsel = gather(cursor);
+                if (STATS) nsel_total += nsel;
+            }
+            if (first) {  // no triangle at all
+                for (int r0 = 0; r0 < total; r0 += 32) {
+                    const int q = r0 + lane;
+                    int row, colo;
+                    texel_of(q, row, colo);
+                    if (q < total) store(row, colo, CUDART_INF, -1);
+                }
+            }
+        }
+    } else {
+        // crowded tile: gather the whole overlap list (TC_SEL at a time), sort it by
+        // ascending min depth, stage the nearest TC_RES float32 forms; the walk reads
+        // any later one from global memory.  The nearest certain cover then proves
+        // (V) that every later triangle is behind it, so a texel's walk usually ends
+        // in the first chunk -- nested surfaces cost one sort, not one pass each.
+        float* vb = dv.vbuf + (int64_t)f * W * H;
+        bool first = true;
+        do {
+            int cnt = 0;
+            while (cursor < n && cnt < TC_SEL - 32) {
+                int i = cursor + lane;
+                bool sel = false;
+                if (i < n) {
+                    if (clist) i = clist[i];
+                    const uint2 bbx = segb[i];
+                    const int x0 = bbx.x & 0xffff, x1 = bbx.x >> 16, y0 = bbx.y & 0xffff, y1 = bbx.y >> 16;
+                    sel = !(x1 < xb || x0 > xe || y1 < yb || y0 > ye);
+                }
+                const unsigned bal = __ballot_sync(FULL, sel);
+                if (sel) {
+                    const int at = cnt + __popc(bal & ((1u << lane) - 1u));
+                    SEL[at] = i;
+                    KEY[at] = -__ldg(&segf[i].inv_minw);
+                }
+                cnt += __popc(bal);
+                cursor += 32;
+            }
+            if (STATS) nsel_total += cnt;
+            int P = 32;
+            while (P < cnt) P <<= 1;
+            for (int k = cnt + lane; k < P; k += 32) {
+                KEY[k] = CUDART_INF_F;
+                SEL[k] = -1;
+            }
+            __syncwarp();
+            // warp bitonic sort of (KEY, SEL) ascending, P <= TC_SEL
+            for (int size = 2; size <= P; size <<= 1) {
+                for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                    for (int a = lane; a < P; a += 32) {
+                        const int b = a ^ stride;
+                        if (b > a) {
+                            const float ka = KEY[a], kb = KEY[b];
+                            const int sa = SEL[a], sb = SEL[b];
+                            const bool up = (a & size) == 0;
+                            const bool gt = ka > kb || (ka == kb && sa > sb);
+                            if (gt == up) {
+                                KEY[a] = kb;
+                                KEY[b] = ka;
+                                SEL[a] = sb;
+                                SEL[b] = sa;
+                            }
+                        }
+                    }
+                    __syncwarp();
+                }
+            }
+            const int ns = min(cnt, TC_RES);
+            for (int k = lane; k < ns; k += 32) {
+                const uint4* from = reinterpret_cast<const uint4*>(segf + SEL[k]);
+                uint4* to = reinterpret_cast<uint4*>(&T32[k]);
+#pragma unroll
+                for (int part = 0; part < 6; part++) to[part] = from[part];
+            }
+            __syncwarp();
+            const bool last = cursor >= n;
+            for (int r0 = 0; r0 < total; r0 += 32) {
+                const int q = r0 + lane;
+                const bool valid = q < total;
+                int row, colo;
+                texel_of(q, row, colo);
+                const int64_t at = (int64_t)(yb + row) * W + xb + colo;
+                float V = valid ? (first ? 0.0f : vb[at]) : CUDART_INF_F;
+                double best = (valid && !first) ? dep[at] : CUDART_INF;
+                int bkey = INT_MAX;
+                if (ATTRS && valid && !first) bkey = dv.key[at];
+                if (cnt > 0) walk(cnt, ns, valid, row, colo, V, best, bkey);
+                if (valid) {
+                    dep[at] = best;
+                    if (!last) vb[at] = V;
+                    if (ATTRS) dv.key[at] = best < CUDART_INF ? bkey : -1;
+                }
+            }
+            first = false;
+            __syncwarp();
+        } while (cursor < n);
+    }
+    if (STATS) {
+        const bool l0 = lane == 0;
+        stat_add(dv.stats, GM_STAT_TEXELS, l0 ? (unsigned long long)total : 0ull);
+        stat_add(dv.stats, GM_STAT_TX_TILES, l0 ? 1ull : 0ull);
+        stat_add(dv.stats, GM_STAT_TX_STAGED, l0 ? (unsigned long long)nsel_total : 0ull);
+        stat_add(dv.stats, GM_STAT_TX_LIST, l0 ? (unsigned long long)n : 0ull);
+        stat_add(dv.stats, GM_STAT_TX_ITER, l0 ? c_iter : 0ull);
+        stat_add(dv.stats, GM_STAT_PAIRS, c_pairs);
+        stat_add(dv.stats, GM_STAT_COVERED, c_cov);
+        stat_add(dv.stats, GM_STAT_TX_EDGE, c_edge);
+    }
+}
+
+template <bool ATTRS, bool STATS, bool CROWDED>
+__global__ void TX_BOUNDS k_texels(TriStore ts, DepthView dv, CoarseBins cb, int tiles_x,
+                                   int tiles_per_fix, int64_t n_items,
+                                   const GmFixExact* __restrict__ fixes, long long b0) {
+    extern __shared__ __align__(16) unsigned char tx_dyn[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (*ts.fail <= b0) return;
+    if (!CROWDED) {
+        const int64_t item = (int64_t)blockIdx.x * TW_WARPS + warp;
+        if (item < n_items)
+            texel_item<ATTRS, STATS, false>(reinterpret_cast<TexelWarpSmem*>(tx_dyn)[warp].t32,
+                                            reinterpret_cast<TexelWarpSmem*>(tx_dyn)[warp].sel, nullptr, item, ts, dv,
+                                            cb, tiles_x, tiles_per_fix, fixes);
+        return;
+    }
+    // crowded tiles (deferred by the pass above): persistent warps over the list
+    CrowdedWarpSmem& C = reinterpret_cast<CrowdedWarpSmem*>(tx_dyn)[warp];
+    const int n_crowd = *dv.crowd_count;
+    for (;;) {
+        int w = 0;
+        if (lane == 0) w = atomicAdd(dv.crowd_count + 1, 1);
+        w = __shfl_sync(0xffffffffu, w, 0);
+        if (w >= n_crowd) break;
+        texel_item<ATTRS, STATS, true>(C.t32, C.sel, C.key, dv.crowd[w], ts, dv, cb, tiles_x, tiles_per_fix, fixes);
+    }
+}
+
