@@ -322,7 +322,10 @@ struct TriStore {
 // One warp per group of 32 triangle clusters (32 triangles each); blockIdx.y =
 // fixation slot.  Lane-parallel cluster test -> ballot -> per passing cluster
 // lane = triangle: sphere test, exact projection, warp-aggregated append.
-__global__ void __launch_bounds__(256) k_tri_setup(const double* __restrict__ tw, int64_t T,
+#ifndef TS_WARPS
+#define TS_WARPS 2  // warps (independent cluster groups) per k_tri_setup CTA
+#endif
+__global__ void __launch_bounds__(TS_WARPS * 32) k_tri_setup(const double* __restrict__ tw, int64_t T,
                                                    const float4* __restrict__ tsph, const float4* __restrict__ csph,
                                                    int64_t n_clu, const GmFixExact* __restrict__ fixes,
                                                    const GmFixCull* __restrict__ culls, int W, int H, TriStore ts,
@@ -1138,8 +1141,8 @@ static int enqueue_batch(gm_plan* p, const GmFixExact* d_fix, const GmFixCull* d
     if (ev) CK(cudaEventRecord(ev[0], s));
     CK(cudaMemsetAsync(p->d_count, 0, sizeof(int) * nb, s));
     if (p->n_clu > 0) {
-        dim3 grid(blocks_for((p->n_clu + 31) / 32, 8), nb);
-        k_tri_setup<<<grid, 256, 0, s>>>(p->d_tw, p->T, p->d_tsph, p->d_csph, p->n_clu, d_fix, d_cull, W, H, ts, b0);
+        dim3 grid(blocks_for((p->n_clu + 31) / 32, TS_WARPS), nb);
+        k_tri_setup<<<grid, TS_WARPS * 32, 0, s>>>(p->d_tw, p->T, p->d_tsph, p->d_csph, p->n_clu, d_fix, d_cull, W, H, ts, b0);
     }
     if (ev) CK(cudaEventRecord(ev[1], s));
     if (p->n_chunks > 0 && accumulate) {
@@ -1620,8 +1623,8 @@ static int raster_pass(gm_plan* p, int W, int H, bool attrs) {
         CK(cudaMemsetAsync(p->d_count, 0, sizeof(int), s));
         TriStore ts{p->d_tris, p->d_t32, p->d_bbox, p->d_count, p->cap_seg, p->d_fail, p->d_maxcount, p->d_ntris};
         if (p->n_clu > 0) {
-            dim3 grid(blocks_for((p->n_clu + 31) / 32, 8), 1);
-            k_tri_setup<<<grid, 256, 0, s>>>(p->d_tw, p->T, p->d_tsph, p->d_csph, p->n_clu, p->d_fix, p->d_cull, W,
+            dim3 grid(blocks_for((p->n_clu + 31) / 32, TS_WARPS), 1);
+            k_tri_setup<<<grid, TS_WARPS * 32, 0, s>>>(p->d_tw, p->T, p->d_tsph, p->d_csph, p->n_clu, p->d_fix, p->d_cull, W,
                                              H, ts, 0);
         }
         long long failed = LLONG_MAX;
