@@ -499,6 +499,7 @@ enum {
     GM_STAT_TX_LIST = 12,    // coarse-bin list entries scanned per item (sum)
     GM_STAT_TX_ITER = 13,    // warp iterations of the selection walk
     GM_STAT_TX_EDGE = 14,    // lane x triangle edge-function evaluations in the walk
+    GM_STAT_TX_CROWDED = 15, // tiles deferred to the sorted crowded pass
     GM_STAT_N = 16
 };
 #define GM_FLAG_STATS 1

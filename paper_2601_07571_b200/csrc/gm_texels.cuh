@@ -293,6 +293,7 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
             __reduce_add_sync(FULL, (unsigned)cover) > (unsigned)(CROWD_DEPTH * TW * TH)) {
             // more than TW_CAP triangles: k_texels<CROWDED> sorts the whole list (deferred)
             if (lane == 0) dv.crowd[atomicAdd(dv.crowd_count, 1)] = (int)item;
+            if (STATS) stat_add(dv.stats, GM_STAT_TX_CROWDED, lane == 0 ? 1ull : 0ull);
             return;
         }
         if (cursor >= n && nsel <= TW_CAP) {

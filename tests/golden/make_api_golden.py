@@ -103,6 +103,22 @@ def main():
     pts = tris[rng.integers(0, len(tris), 200)].mean(axis=1) + rng.normal(0, 0.01, (200, 3))
     d["r_pts"] = pts
     d["r_vis"] = np.array([raster.is_visible(buf, p) for p in pts])
+    # ---- raster with attributes on nested shells (deep tiles: the sorted crowded pass)
+    base = R.Mesh(W.icosphere(3, 1.0).vertices, W.icosphere(3, 1.0).faces)
+    shells = R.Scene(tuple(R.SceneObject(f"s{i}", R.Mesh(base.vertices * (0.5 + 0.08 * i), base.faces))
+                           for i in range(16)))
+    scam = np.array([0.4, 0.3, 3.0])
+    sq = W.look_at_quat(scam, [0.0, 0.0, 0.0])
+    sfx = R.Fixation(0.0, 1.0, scam, sq, (-0.1, 0.1, 0.1, -0.1, 0.1, 50.0), [0.0, 0.0, -1.0])
+    sview, sproj = sfx.view_matrix(), sfx.projection_matrix()
+    stris = raster.scene_world_triangles(shells)
+    sd = np.full((128, 160), np.inf)
+    sid = np.full((128, 160), -1, np.int32)
+    sb = np.zeros((128, 160, 3))
+    kernels.rasterize(np.ascontiguousarray(stris), np.ascontiguousarray(sview[:3, :3]),
+                      np.ascontiguousarray(sview[:3, 3]), sproj[0, 0], sproj[1, 1], sproj[0, 2], sproj[1, 2],
+                      160, 128, 0.1, 50.0, sd, sid, sb, True)
+    d["s_view"], d["s_proj"], d["s_depth"], d["s_tri"], d["s_bary"] = sview, sproj, sd, sid, sb
     # ---- render
     sm = R.build_sampled_meshes(scene, 3000.0)
     vals = {}

@@ -140,3 +140,20 @@ def test_host_depth_match_vs_oracle():
             eps = float(rng.choice([1e-3, 5e-3, 0.2]))
             got = bool(lib.gm_depth_match(_native.dptr(depth), H, W, fx, fy, d, eps))
             assert got == O.depth_match(depth, fx, fy, d, eps), (H, W, fx, fy, d, eps)
+
+
+@pytest.mark.gpu
+def test_rasterize_with_attributes_deep_tiles():
+    """16 nested shells seen whole: every tile is deep (bboxes cover it > 10x) and
+    goes through the sorted crowded pass; depth, winner and barycentrics must
+    still be the reference's bits."""
+    base = W.icosphere(3, 1.0)
+    shells = gm.Scene(tuple(gm.SceneObject(f"s{i}", gm.Mesh(base.vertices * (0.5 + 0.08 * i), base.faces))
+                            for i in range(16)))
+    view, proj = G["s_view"], G["s_proj"]
+    tris = raster.scene_world_triangles(shells)
+    depth, tri_id, bary = raster.rasterize_with_attributes(tris, view, proj[0, 0], proj[1, 1], proj[0, 2], proj[1, 2],
+                                                           (160, 128), 0.1, 50.0)
+    np.testing.assert_array_equal(_bits(depth), _bits(G["s_depth"]))
+    np.testing.assert_array_equal(tri_id, G["s_tri"])
+    np.testing.assert_array_equal(_bits(bary), _bits(G["s_bary"]))

@@ -139,3 +139,21 @@ def test_shells_occlusion_vs_oracle():
             np.testing.assert_allclose(dm.values[oid], vals[oid], rtol=1e-12, atol=0.0)
         inner = sum(int((vals[f"s{i}"] != 0).sum()) for i in range(5))
         assert inner == 0  # only the outermost shell is visible
+
+
+def test_deep_shells_crowded_pass_vs_oracle():
+    """16 nested icosphere(3) shells, full frustum: the texel tiles are deep
+    (triangle bboxes cover them > 10x), so the z-buffer texels come from the
+    sorted crowded pass of k_texels."""
+    base = W.icosphere(3, 1.0)
+    scene = gm.Scene(tuple(gm.SceneObject(f"s{i}", gm.Mesh(base.vertices * (0.5 + 0.08 * i), base.faces))
+                           for i in range(16)))
+    fx = W.orbit_fixations(6, 7, 2.6, 3.2, jitter=0.2)
+    cfg = gm.GenerationConfig(k=1500.0, filtering_enabled=False)
+    sampled = gm.build_sampled_meshes(scene, cfg.k)
+    dm = gm.generate(scene, sampled, fx, cfg)
+    vals, gmax = O.generate(scene, O.rows_as_fixations(fx), k=cfg.k, filtering_enabled=False, threads=8)
+    assert dm.global_max == pytest.approx(gmax, rel=1e-12)
+    for oid in vals:
+        np.testing.assert_array_equal(dm.values[oid] != 0, vals[oid] != 0)
+        np.testing.assert_allclose(dm.values[oid], vals[oid], rtol=1e-12, atol=0.0)
