@@ -385,6 +385,17 @@ def run_ours(args, rank, world):
             "algorithmic_flops_per_step": dom_flops,
             "peak_kind": "nominal FP64 FMA peak at max SM clock (MEASURED_PEAKS.json has no FP64 figure)",
             "work": st}
+    # SURVEY.md 8d's step roofline: algorithmic FLOPs of the reference's per-pair work -- 26 per nominal
+    # sample-fixation pair (camera transform + NDC projection, kernels.py:305-315) + 43 per NDC candidate
+    # (depth test + Gaussian, :323-340) -- over the whole step, against the FP32 SIMT peak (nominal:
+    # 148 SM x 128 lanes x 2 x max clock; the path computes in FP64 for parity, the FP32 peak is the
+    # survey's yardstick).  Culling means most nominal pairs are never evaluated, so this can exceed 1.
+    fp32_peak = 148 * 128 * 2 * clk_ghz / 1e3
+    step_flops = 26.0 * N * F + 43.0 * st.get("ndc_candidates", 0)
+    step_tf = step_flops / (step_ms / 1e3) / 1e12 if st.get("ndc_candidates") else None
+    roof_step = {"bound": "fp32", "achieved": step_tf, "peak": fp32_peak, "unit": "TFLOP/s",
+                 "frac": step_tf / fp32_peak if step_tf else None, "algorithmic_flops_per_step": step_flops,
+                 "definition": "SURVEY.md 8d: (26 N F + 43 sum C_ndc) / t / P_FP32 (per rank)"}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
@@ -406,7 +417,7 @@ def run_ours(args, rank, world):
                        "parallelism": f"fixation-sharded x{world}, NCCL sum all-reduce" if world > 1 else "single GPU",
                        "l2": "flushed (512 MiB write) before every timed step",
                        "timing": "CUDA events on the plan stream around each full generation (+ all-reduce)"},
-            "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "clocks": clk.summary(), "gpu_launches": launches,
+            "e2e": e2e, "roofline": roof, "roofline_step_fp32": roof_step, "cpu_baseline": cpu, "clocks": clk.summary(), "gpu_launches": launches,
             "library_launches": library_launches,
             "phases_ms": {"cull": tm.cull_ms, "mark": tm.mark_ms, "texels": tm.texel_ms,
                           "accumulate": tm.accumulate_ms, "batches": tm.batches, "retries": tm.retries,
