@@ -479,6 +479,8 @@ struct DepthView {
     unsigned long long* stats;  // optional work counters (GM_STAT_*), nullptr = off
     float* vbuf;      // [B][H][W]: k_texels' inverse-depth bounds for tiles with many triangles
     int* key;         // [H][W] (ATTRS only): order key 2 t + fan of the triangle that wrote the texel
+    int* win;         // [B][H][W] (generation batches): segment index of the texel's writer, -1 none
+    double* carry;    // [B][H][W] (generation batches): exact best depth between chunks of a tile
     int* crowd;       // work items deferred to k_texels<CROWDED> (nullptr: handle them in place)
     int* crowd_count; // [2]: deferred items, claimed items
 };
@@ -562,6 +564,116 @@ __device__ __forceinline__ bool depth_test(const DepthView& dv, int f, double gx
         }
     }
     return best <= eps;
+}
+
+// depth_match on a generation batch's texel store: every texel holds rigorous
+// float32 bounds [lo, hi] of the float64 depth kernels.rasterize leaves there
+// ((+inf, +inf) where nothing is written) and the segment index of its writer.
+// Each stage of kernels.py:219-285 is decided on the bounds when they decide it
+// (the comparisons use a slack that covers the reference's and this code's own
+// float64 rounding); otherwise the exact depths of the texels the test reads
+// are re-evaluated from their writers (texel_depth) and the reference test runs
+// on them.  Either way the result is the reference's.
+__device__ __forceinline__ bool depth_test_exact(const DepthView& dv, const GmScreenTri* __restrict__ seg, double near_,
+                                              double far_, int f, double gx, double gy, int bx0, int bx1, int by0,
+                                              int by1, double d, double eps) {
+    const int W = dv.W, H = dv.H;
+    const int* win = dv.win + (int64_t)f * W * H;
+    auto val = [&](int x, int y) -> double {
+        const int w = win[(int64_t)y * W + x];
+        return w < 0 ? CUDART_INF : texel_depth(seg[w], x, y, near_, far_);
+    };
+    if (W > 1 && H > 1) {
+        long long x0 = x86_i64(floor(gx));
+        if (x0 < 0) x0 = 0;
+        else if (x0 > W - 2) x0 = W - 2;
+        long long y0 = x86_i64(floor(gy));
+        if (y0 < 0) y0 = 0;
+        else if (y0 > H - 2) y0 = H - 2;
+        const double q00 = val((int)x0, (int)y0), q01 = val((int)x0 + 1, (int)y0);
+        const double q10 = val((int)x0, (int)y0 + 1), q11 = val((int)x0 + 1, (int)y0 + 1);
+        if (isfinite(q00) && isfinite(q01) && isfinite(q10) && isfinite(q11)) {
+            double tx = gx - (double)x0;
+            if (tx < 0.0) tx = 0.0;
+            else if (tx > 1.0) tx = 1.0;
+            double ty = gy - (double)y0;
+            if (ty < 0.0) ty = 0.0;
+            else if (ty > 1.0) ty = 1.0;
+            double top = q00 * (1.0 - tx) + q01 * tx;
+            double bot = q10 * (1.0 - tx) + q11 * tx;
+            if (fabs(d - (top * (1.0 - ty) + bot * ty)) <= eps) return true;
+            double hi = fmax(fmax(q00, q01), fmax(q10, q11));
+            double lo = fmin(fmin(q00, q01), fmin(q10, q11));
+            if (hi - lo <= eps) return false;
+        }
+    }
+    double best = CUDART_INF;
+    for (int yy = by0; yy <= by1; yy++)
+        for (int xx = bx0; xx <= bx1; xx++) {
+            const double t = val(xx, yy);
+            if (isfinite(t)) {
+                double diff = fabs(t - d);
+                if (diff < best) best = diff;
+            }
+        }
+    return best <= eps;
+}
+
+__device__ __forceinline__ bool depth_test_iv(const DepthView& dv, const GmScreenTri* __restrict__ seg, double near_,
+                                              double far_, int f, double gx, double gy, int bx0, int bx1, int by0,
+                                              int by1, double d, double eps) {
+    const int W = dv.W, H = dv.H;
+    const float2* q2 = reinterpret_cast<const float2*>(dv.depth) + (int64_t)f * W * H;
+    const double slack = 1e-13 * (fabs(d) + eps);
+    if (W > 1 && H > 1) {
+        long long x0 = x86_i64(floor(gx));
+        if (x0 < 0) x0 = 0;
+        else if (x0 > W - 2) x0 = W - 2;
+        long long y0 = x86_i64(floor(gy));
+        if (y0 < 0) y0 = 0;
+        else if (y0 > H - 2) y0 = H - 2;
+        const float2* r0 = q2 + (int64_t)y0 * W + x0;
+        const float2 a = r0[0], b = r0[1], c = r0[W], e = r0[W + 1];
+        if (a.x < CUDART_INF_F && b.x < CUDART_INF_F && c.x < CUDART_INF_F && e.x < CUDART_INF_F) {
+            double tx = gx - (double)x0;
+            if (tx < 0.0) tx = 0.0;
+            else if (tx > 1.0) tx = 1.0;
+            double ty = gy - (double)y0;
+            if (ty < 0.0) ty = 0.0;
+            else if (ty > 1.0) ty = 1.0;
+            // the weights are >= 0: the bilinear value is monotone in every texel
+            const double blo = ((double)a.x * (1.0 - tx) + (double)b.x * tx) * (1.0 - ty) +
+                               ((double)c.x * (1.0 - tx) + (double)e.x * tx) * ty;
+            const double bhi = ((double)a.y * (1.0 - tx) + (double)b.y * tx) * (1.0 - ty) +
+                               ((double)c.y * (1.0 - tx) + (double)e.y * tx) * ty;
+            const double sl = slack + 1e-13 * fabs(bhi);
+            if (fmax(fabs(d - blo), fabs(d - bhi)) + sl <= eps) return true;       // certain match
+            if (!(fmax(fmax(d - bhi, blo - d), 0.0) - sl > eps))                     // undecided
+                return depth_test_exact(dv, seg, near_, far_, f, gx, gy, bx0, bx1, by0, by1, d, eps);
+            const double smax = (double)fmaxf(fmaxf(a.y, b.y), fmaxf(c.y, e.y)) -
+                                (double)fminf(fminf(a.x, b.x), fminf(c.x, e.x));
+            const double smin = (double)fmaxf(fmaxf(a.x, b.x), fmaxf(c.x, e.x)) -
+                                (double)fminf(fminf(a.y, b.y), fminf(c.y, e.y));
+            if (smax + sl <= eps) return false;                                      // smooth quad
+            if (!(smin - sl > eps))                                                  // undecided
+                return depth_test_exact(dv, seg, near_, far_, f, gx, gy, bx0, bx1, by0, by1, d, eps);
+        }
+    }
+    bool all_far = true;
+    for (int yy = by0; yy <= by1; yy++) {
+        const float2* row = q2 + (int64_t)yy * W;
+        for (int xx = bx0; xx <= bx1; xx++) {
+            const float2 v = row[xx];
+            if (v.x < CUDART_INF_F) {
+                const double lo = v.x, hi = v.y;
+                const double sl = slack + 1e-13 * hi;
+                if (fmax(fabs(lo - d), fabs(hi - d)) + sl <= eps) return true;
+                if (!(fmax(fmax(lo - d, d - hi), 0.0) - sl > eps)) all_far = false;
+            }
+        }
+    }
+    if (all_far) return false;
+    return depth_test_exact(dv, seg, near_, far_, f, gx, gy, bx0, bx1, by0, by1, d, eps);
 }
 
 #include "gm_samples.cuh"
@@ -657,6 +769,7 @@ static int dev_alloc(T** p, size_t n) {
     X(GmFixExact*, d_fix) X(GmFixCull*, d_cull) X(GmFixF32*, d_fix32) X(GmScreenTri*, d_tris)          \
     X(TriF32*, d_t32) X(uint2*, d_bbox) X(int*, d_count) X(int64_t, cap_seg) X(int64_t, cap_seg_B)     \
     X(double*, d_depth) X(float*, d_vbuf) X(uint32_t*, d_mask) X(int64_t, cap_depth) X(int64_t, cap_mask) \
+    X(int*, d_win) X(double*, d_carry)                                                                 \
     X(int*, d_citems) X(int*, d_coff) X(int*, d_covf) X(int64_t, cap_citems) X(int64_t, cap_cB)         \
     X(int*, d_crowd) X(int*, d_crowd_count) X(int64_t, cap_crowd)
 
@@ -709,6 +822,8 @@ struct gm_plan {
     // marked z-buffer texels
     double* d_depth = nullptr;   // [B][H][W] marked texels only
     float* d_vbuf = nullptr;     // [B][H][W] k_texels state for crowded tiles
+    int* d_win = nullptr;        // [B][H][W] writer of each marked texel (generation batches)
+    double* d_carry = nullptr;   // [B][H][W] k_texels' exact best between chunks
     uint32_t* d_mask = nullptr;  // [B][H][wwords]
     int64_t cap_depth = 0, cap_mask = 0;
     int* d_citems = nullptr;  // coarse bins: [B][cap_citems]
@@ -794,12 +909,22 @@ extern "C" int gm_plan_create(int device, gm_plan** out) {
         return set_err(GM_ERR_CUDA, cudaGetErrorString(e));
     }
     cudaDeviceGetAttribute(&p->sms, cudaDevAttrMultiProcessorCount, device);
-    CK(cudaFuncSetAttribute(k_texels<false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
-    CK(cudaFuncSetAttribute(k_texels<false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
-    CK(cudaFuncSetAttribute(k_texels<true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
-    CK(cudaFuncSetAttribute(k_texels<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_DYN_SMEM));
-    CK(cudaFuncSetAttribute(k_texels<false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_DYN_SMEM));
-    CK(cudaFuncSetAttribute(k_texels<true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels<false, false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels<false, false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels<false, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels<false, false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels<false, true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels<false, true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels<false, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels<false, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels<true, false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels<true, false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels<true, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels<true, false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels<true, true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels<true, true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels<true, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels<true, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_DYN_SMEM));
     CK(cudaMalloc(&p->d_max, sizeof(unsigned long long)));
     CK(cudaMalloc(&p->d_stats, GM_STAT_STRIPES * GM_STAT_N * sizeof(unsigned long long)));
     CK(cudaMemset(p->d_stats, 0, GM_STAT_STRIPES * GM_STAT_N * sizeof(unsigned long long)));
@@ -821,7 +946,7 @@ static void free_batch_set(gm_plan* p) {
     free_scene_batch_bufs(p);
     cudaFree(p->d_fix); cudaFree(p->d_cull); cudaFree(p->d_fix32); cudaFree(p->d_work);
     cudaFree(p->d_tris); cudaFree(p->d_t32); cudaFree(p->d_bbox); cudaFree(p->d_count);
-    cudaFree(p->d_depth); cudaFree(p->d_mask); cudaFree(p->d_vbuf);
+    cudaFree(p->d_depth); cudaFree(p->d_mask); cudaFree(p->d_vbuf); cudaFree(p->d_win); cudaFree(p->d_carry);
     cudaFree(p->d_citems); cudaFree(p->d_coff); cudaFree(p->d_covf);
     cudaFree(p->d_crowd); cudaFree(p->d_crowd_count);
     if (p->stream) cudaStreamDestroy(p->stream);
@@ -1050,6 +1175,8 @@ static int ensure_batch_set(gm_plan* p, int B, int W, int H, int64_t seg) {
     if ((int64_t)B * W * H > p->cap_depth) {
         if ((rc = dev_alloc(&p->d_depth, (size_t)B * W * H))) return rc;
         if ((rc = dev_alloc(&p->d_vbuf, (size_t)B * W * H))) return rc;
+        if ((rc = dev_alloc(&p->d_win, (size_t)B * W * H))) return rc;
+        if ((rc = dev_alloc(&p->d_carry, (size_t)B * W * H))) return rc;
         p->cap_depth = (int64_t)B * W * H;
     }
     if (B > p->cap_cB || CB_ITEMS_PER_TRI * p->cap_seg > p->cap_citems) {
@@ -1109,15 +1236,15 @@ static CoarseBins coarse_bins(gm_plan* p, int W, int H) {
 
 // k_texels over `items` (fixation, tile) work items, then the crowded tiles the
 // first pass deferred (k_texels<CROWDED>, persistent, larger shared slices).
-template <bool ATTRS, bool STATS>
+template <bool ATTRS, bool STATS, bool EXACT>
 static int launch_texels(gm_plan* p, cudaStream_t s, const TriStore& ts, DepthView dv, const CoarseBins& cb,
                          int tiles_x, int tiles_per_fix, int64_t items, const GmFixExact* fix, long long b0) {
     dv.crowd = p->d_crowd;
     dv.crowd_count = p->d_crowd_count;
     CK(cudaMemsetAsync(p->d_crowd_count, 0, 2 * sizeof(int), s));
-    k_texels<ATTRS, STATS, false><<<(unsigned)((items + TW_WARPS - 1) / TW_WARPS), TW_WARPS * 32, TX_DYN_SMEM, s>>>(
+    k_texels<ATTRS, STATS, false, EXACT><<<(unsigned)((items + TW_WARPS - 1) / TW_WARPS), TW_WARPS * 32, TX_DYN_SMEM, s>>>(
         ts, dv, cb, tiles_x, tiles_per_fix, items, fix, b0);
-    k_texels<ATTRS, STATS, true><<<p->sms * (20 / TC_WARPS), TC_WARPS * 32, TC_DYN_SMEM, s>>>(ts, dv, cb, tiles_x, tiles_per_fix,
+    k_texels<ATTRS, STATS, true, EXACT><<<p->sms * (20 / TC_WARPS), TC_WARPS * 32, TC_DYN_SMEM, s>>>(ts, dv, cb, tiles_x, tiles_per_fix,
                                                                               items, fix, b0);
     CK(cudaGetLastError());
     return GM_OK;
@@ -1139,6 +1266,8 @@ static int enqueue_batch(gm_plan* p, const GmFixExact* d_fix, const GmFixCull* d
     TriStore ts{p->d_tris, p->d_t32, p->d_bbox, p->d_count, p->cap_seg, p->d_fail, p->d_maxcount, p->d_ntris};
     DepthView dv{p->d_depth, p->d_mask, W, H, wwords, (cfg->flags & GM_FLAG_STATS) ? p->d_stats : nullptr,
                  p->d_vbuf};
+    dv.win = p->d_win;
+    dv.carry = p->d_carry;
     if (ev) CK(cudaEventRecord(ev[0], s));
     CK(cudaMemsetAsync(p->d_count, 0, sizeof(int) * nb, s));
     if (p->n_clu > 0) {
@@ -1168,8 +1297,9 @@ static int enqueue_batch(gm_plan* p, const GmFixExact* d_fix, const GmFixCull* d
         const int64_t items = (int64_t)nb * tiles_x * tiles_y;
         CoarseBins cbins = coarse_bins(p, W, H);
         k_coarse<<<nb, 256, 0, s>>>(ts, cbins, p->d_fail, b0);
-        int trc = dv.stats ? launch_texels<false, true>(p, s, ts, dv, cbins, tiles_x, tiles_x * tiles_y, items, d_fix, b0)
-                           : launch_texels<false, false>(p, s, ts, dv, cbins, tiles_x, tiles_x * tiles_y, items, d_fix, b0);
+        int trc = dv.stats
+                      ? launch_texels<false, true, false>(p, s, ts, dv, cbins, tiles_x, tiles_x * tiles_y, items, d_fix, b0)
+                      : launch_texels<false, false, false>(p, s, ts, dv, cbins, tiles_x, tiles_x * tiles_y, items, d_fix, b0);
         if (trc) return trc;
         if (ev) CK(cudaEventRecord(ev[3], s));
         // accumulation passes run in batch order across the two streams (log order per sample)
@@ -1177,7 +1307,7 @@ static int enqueue_batch(gm_plan* p, const GmFixExact* d_fix, const GmFixCull* d
         auto ks = dv.stats ? k_samples<true> : k_samples<false>;
         ks<<<grid_s, 256, 0, s>>>(p->d_px, p->d_py, p->d_pz, p->d_chunk, p->d_lvl1, p->d_lorder2, p->d_work + 1, p->N,
                                 p->n_chunks, p->n_supers, d_fix, d_cull, nb, dv, inv_sigma, cfg->eps_abs,
-                                cfg->eps_rel, p->d_values, p->d_cbits, p->d_fail, b0);
+                                cfg->eps_rel, p->d_values, p->d_cbits, p->d_tris, p->cap_seg, p->d_fail, b0);
         CK(cudaEventRecord(p->ev_order, s));
     } else if (ev) {
         CK(cudaEventRecord(ev[2], s));
@@ -1646,8 +1776,8 @@ static int raster_pass(gm_plan* p, int W, int H, bool attrs) {
     CoarseBins cbins = coarse_bins(p, W, H);
     k_coarse<<<1, 256, 0, s>>>(ts, cbins, p->d_fail, 0);
     const int64_t items = (int64_t)tiles_x * tiles_y;
-    return attrs ? launch_texels<true, false>(p, s, ts, dv, cbins, tiles_x, tiles_x * tiles_y, items, p->d_fix, 0)
-                 : launch_texels<false, false>(p, s, ts, dv, cbins, tiles_x, tiles_x * tiles_y, items, p->d_fix, 0);
+    return attrs ? launch_texels<true, false, true>(p, s, ts, dv, cbins, tiles_x, tiles_x * tiles_y, items, p->d_fix, 0)
+                 : launch_texels<false, false, true>(p, s, ts, dv, cbins, tiles_x, tiles_x * tiles_y, items, p->d_fix, 0);
 }
 
 // kernels.rasterize for the plan's occluders under fixation `fx` (18 floats):

@@ -253,6 +253,7 @@ __global__ void KS_BOUNDS k_samples(const double* __restrict__ px, const double*
                                                  const GmFixCull* __restrict__ culls, int B, DepthView dv,
                                                  double inv_sigma, double eps_abs, double eps_rel,
                                                  double* __restrict__ values, const uint32_t* __restrict__ cbits,
+                                                 const GmScreenTri* __restrict__ tris, int64_t cap_seg,
                                                  const long long* __restrict__ fail, long long b0) {
     if (*fail <= b0) return;  // this batch overflowed the triangle store: the host redoes it
     const int lane = threadIdx.x & 31;
@@ -334,7 +335,9 @@ __global__ void KS_BOUNDS k_samples(const double* __restrict__ px, const double*
                 // kernels.py:323-329
                 double eps = eps_abs;
                 if (eps_rel * d > eps) eps = eps_rel * d;
-                if (!depth_test(dv, f, gx, gy, bx0, bx1, by0, by1, d, eps)) continue;
+                if (!depth_test_iv(dv, tris + (int64_t)f * cap_seg, F.near_, F.far_, f, gx, gy, bx0, bx1, by0, by1, d,
+                                   eps))
+                    continue;
                 if (STATS) c_vis++;
                 v += F.amp * exp(-0.5 * ratio_sq);  // kernels.py:340
             }

@@ -72,7 +72,7 @@ __device__ __forceinline__ int kth_set_bit(uint32_t w, int k) {
 //      leaves in that pixel.
 // One (fixation, tile) work item of k_texels.  T32/SEL: the warp's staging and
 // selection slices; KEY (crowded mode only): sort keys of SEL.
-template <bool ATTRS, bool STATS, bool CROWDED>
+template <bool ATTRS, bool STATS, bool CROWDED, bool EXACT>
 __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __restrict__ SEL, float* __restrict__ KEY,
                                            int64_t item, const TriStore& ts, const DepthView& dv,
                                            const CoarseBins& cb, int tiles_x, int tiles_per_fix,
@@ -188,23 +188,34 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
     // 3 + 4 for the staged chunk (kend triangles) and one texel: updates V, best
     // kernels.py:128-129 writes iff d < depth[py, px]: among equal minima the
     // first triangle in rasterization order (key 2 t + fan) owns the texel
-    auto take = [&](double d, int cs, double& best, int& bkey) {
+    auto take = [&](double d, int cs, double& best, int& bkey, int& bwin) {
         if (!ATTRS) {
-            if (d < best) best = d;
+            if (d < best) {
+                best = d;
+                bwin = cs;
+            }
             return;
         }
         const int key = (int)(seg[cs].tl >> 3);
         if (d < best || (d == best && d < CUDART_INF && key < bkey)) {
             best = d;
             bkey = key;
+            bwin = cs;
         }
     };
     // triangle kk of the walk: staged in shared memory (kk < nst) or, crowded mode, from global
     auto tri_at = [&](int kk, int nst) -> const TriF32& { return (!CROWDED || kk < nst) ? T32[kk] : segf[SEL[kk]]; };
-    auto walk = [&](int kend, int nst, bool valid, int row, int colo, float& V, double& best, int& bkey) {
+    // Returns true when (allow_fast) one certainly-written candidate provably wins:
+    // then its segment index is in bwin and fastb holds rigorous float32 bounds of
+    // its inverse depth at the texel -- no float64 evaluation (the accumulation pass
+    // decides its depth tests on these bounds and evaluates only undecided ones).
+    auto walk = [&](int kend, int nst, bool valid, int row, int colo, float& V, double& best, int& bkey, int& bwin,
+                    bool allow_fast, float2& fastb) -> bool {
         const int px = xb + colo, py = yb + row;
         int cs0 = -1, cs1 = -1;  // exact candidates (global record index) and their bounds
         float ch0 = 0.0f, ch1 = 0.0f;
+        float cl0 = 0.0f, cl1 = 0.0f;   // their lower inverse-depth bounds
+        bool ce0 = false, ce1 = false;  // certainly covering and written
         bool overflow = false;
         for (int kk = 0; kk < kend; kk++) {
             const TriF32& t = tri_at(kk, nst);
@@ -228,39 +239,55 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
             const float iwv = __fmaf_rn(t.A, fx, __fmaf_rn(t.B, fy, t.C));
             const float lo = iwv - t.tolw, hi = iwv + t.tolw;
             if (!(hi > 0.0f) || lo > inv_near_hi || hi < inv_far_lo) continue;  // certainly not written
-            if (certain && lo > 0.0f && hi <= inv_near_lo && lo >= inv_far_hi && lo * (1.0f - 1e-6f) > V)
-                V = lo * (1.0f - 1e-6f);
+            const bool cw = certain && lo > 0.0f && hi <= inv_near_lo && lo >= inv_far_hi;
+            if (cw && lo * (1.0f - 1e-6f) > V) V = lo * (1.0f - 1e-6f);
             if (hi >= V) {
                 if (cs0 < 0) {
                     cs0 = t.gidx;
                     ch0 = hi;
+                    cl0 = lo;
+                    ce0 = cw;
                 } else if (cs1 < 0) {
                     cs1 = t.gidx;
                     ch1 = hi;
+                    cl1 = lo;
+                    ce1 = cw;
                 } else if (ch0 < V) {  // a stale candidate can be replaced
                     cs0 = t.gidx;
                     ch0 = hi;
+                    cl0 = lo;
+                    ce0 = cw;
                 } else if (ch1 < V) {
                     cs1 = t.gidx;
                     ch1 = hi;
+                    cl1 = lo;
+                    ce1 = cw;
                 } else {
                     overflow = true;
                 }
             }
         }
-        if (!valid) return;
+        if (!valid) return false;
+        const bool live0 = cs0 >= 0 && ch0 >= V, live1 = cs1 >= 0 && ch1 >= V;
+        if (allow_fast && !overflow && live0 != live1 && (live0 ? ce0 : ce1)) {
+            // the only candidate left is certainly written and every other triangle is
+            // provably farther (inverse depth < V <= its own lower bound)
+            bwin = live0 ? cs0 : cs1;
+            fastb = make_float2((live0 ? cl0 : cl1) * (1.0f - 1e-6f), (live0 ? ch0 : ch1) * (1.0f + 1e-6f));
+            return true;
+        }
         if (!overflow) {
-            if (cs0 >= 0 && ch0 >= V) {
+            if (live0) {
                 const double d = texel_depth(seg[cs0], px, py, near_, far_);
                 if (STATS) c_pairs++;
                 if (STATS) c_cov += d < CUDART_INF;
-                take(d, cs0, best, bkey);
+                take(d, cs0, best, bkey, bwin);
             }
-            if (cs1 >= 0 && ch1 >= V) {
+            if (live1) {
                 const double d = texel_depth(seg[cs1], px, py, near_, far_);
                 if (STATS) c_pairs++;
                 if (STATS) c_cov += d < CUDART_INF;
-                take(d, cs1, best, bkey);
+                take(d, cs1, best, bkey, bwin);
             }
         } else {  // slow path: every staged triangle whose bbox covers the texel
             for (int k = 0; k < kend; k++) {
@@ -271,17 +298,43 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
                 const double d = texel_depth(seg[t.gidx], px, py, near_, far_);
                 if (STATS) c_pairs++;
                 if (STATS) c_cov += d < CUDART_INF;
-                take(d, t.gidx, best, bkey);
+                take(d, t.gidx, best, bkey, bwin);
             }
         }
+        return false;
     };
 
     double* dep = dv.depth + (int64_t)f * W * H;
+    float2* dep2 = reinterpret_cast<float2*>(dv.depth) + (int64_t)f * W * H;  // !EXACT: depth bounds
+    int* win = dv.win + (int64_t)f * W * H;                                    // !EXACT: the writer
+    double* carry = EXACT ? dep : dv.carry + (int64_t)f * W * H;               // best between chunks
     int cursor = 0;
     int nsel_total = 0;
-    auto store = [&](int row, int colo, double best, int bkey) {
-        dep[(int64_t)(yb + row) * W + xb + colo] = best;
-        if (ATTRS) dv.key[(int64_t)(yb + row) * W + xb + colo] = best < CUDART_INF ? bkey : -1;
+    // final value of texel `at`.  EXACT: the float64 depth kernels.rasterize leaves
+    // there (+ the writer's order key with attributes).  Otherwise: rigorous float32
+    // bounds [lo, hi] of that depth and the writing triangle's segment index, from
+    // which k_samples re-evaluates the exact depth when a test is undecided.
+    auto store_at = [&](int64_t at, bool fast, float2 fb, double best, int bkey, int bwin) {
+        if (EXACT) {
+            dep[at] = best;
+            if (ATTRS) dv.key[at] = best < CUDART_INF ? bkey : -1;
+            return;
+        }
+        float2 o;
+        int w = bwin;
+        if (fast) {
+            o = make_float2(__frcp_rd(fb.y), __frcp_ru(fb.x));
+        } else if (best < CUDART_INF) {
+            o = make_float2(__double2float_rd(best), __double2float_ru(best));
+        } else {
+            o = make_float2(CUDART_INF_F, CUDART_INF_F);
+            w = -1;
+        }
+        dep2[at] = o;
+        win[at] = w;
+    };
+    auto store = [&](int row, int colo, bool fast, float2 fb, double best, int bkey, int bwin) {
+        store_at((int64_t)(yb + row) * W + xb + colo, fast, fb, best, bkey, bwin);
     };
     if (!CROWDED) {
         int nsel = gather(cursor);
@@ -306,9 +359,11 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
                 texel_of(q, row, colo);
                 float V = valid ? 0.0f : CUDART_INF_F;
                 double best = CUDART_INF;
-                int bkey = INT_MAX;
-                if (nsel > 0) walk(nsel, nsel, valid, row, colo, V, best, bkey);
-                if (valid) store(row, colo, best, bkey);
+                int bkey = INT_MAX, bwin = -1;
+                float2 fb = make_float2(0.0f, 0.0f);
+                bool fast = false;
+                if (nsel > 0) fast = walk(nsel, nsel, valid, row, colo, V, best, bkey, bwin, !EXACT, fb);
+                if (valid) store(row, colo, fast, fb, best, bkey, bwin);
             }
         } else {
             // many triangles without a deferral list: chunk by chunk (each staged once),
@@ -318,6 +373,7 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
             while (true) {
                 for (int c0 = 0; c0 < nsel; c0 += TW_CAP) {
                     const int kend = min(TW_CAP, nsel - c0);
+                    const bool last = c0 + TW_CAP >= nsel && cursor >= n;
                     stage(c0, kend);
                     for (int r0 = 0; r0 < total; r0 += 32) {
                         const int q = r0 + lane;
@@ -326,14 +382,21 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
                         texel_of(q, row, colo);
                         const int64_t at = (int64_t)(yb + row) * W + xb + colo;
                         float V = valid ? (first ? 0.0f : vb[at]) : CUDART_INF_F;
-                        double best = (valid && !first) ? dep[at] : CUDART_INF;
-                        int bkey = INT_MAX;
+                        double best = (valid && !first) ? carry[at] : CUDART_INF;
+                        int bkey = INT_MAX, bwin = -1;
                         if (ATTRS && valid && !first) bkey = dv.key[at];
-                        walk(kend, kend, valid, row, colo, V, best, bkey);
+                        if (!EXACT && valid && !first) bwin = win[at];
+                        float2 fb;
+                        walk(kend, kend, valid, row, colo, V, best, bkey, bwin, false, fb);
                         if (valid) {
-                            dep[at] = best;
                             vb[at] = V;
-                            if (ATTRS) dv.key[at] = best < CUDART_INF ? bkey : -1;
+                            if (last) {
+                                store_at(at, false, fb, best, bkey, bwin);
+                            } else {
+                                carry[at] = best;
+                                if (ATTRS) dv.key[at] = best < CUDART_INF ? bkey : -1;
+                                if (!EXACT) win[at] = bwin;
+                            }
                         }
                     }
                     first = false;
@@ -347,7 +410,7 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
                     const int q = r0 + lane;
                     int row, colo;
                     texel_of(q, row, colo);
-                    if (q < total) store(row, colo, CUDART_INF, -1);
+                    if (q < total) store(row, colo, false, make_float2(0.0f, 0.0f), CUDART_INF, -1, -1);
                 }
             }
         }
@@ -424,14 +487,23 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
                 texel_of(q, row, colo);
                 const int64_t at = (int64_t)(yb + row) * W + xb + colo;
                 float V = valid ? (first ? 0.0f : vb[at]) : CUDART_INF_F;
-                double best = (valid && !first) ? dep[at] : CUDART_INF;
-                int bkey = INT_MAX;
+                double best = (valid && !first) ? carry[at] : CUDART_INF;
+                int bkey = INT_MAX, bwin = -1;
                 if (ATTRS && valid && !first) bkey = dv.key[at];
-                if (cnt > 0) walk(cnt, ns, valid, row, colo, V, best, bkey);
+                if (!EXACT && valid && !first) bwin = win[at];
+                float2 fb = make_float2(0.0f, 0.0f);
+                bool fast = false;
+                // a single pass (the usual case) may take the float32 fast path
+                if (cnt > 0) fast = walk(cnt, ns, valid, row, colo, V, best, bkey, bwin, !EXACT && first && last, fb);
                 if (valid) {
-                    dep[at] = best;
-                    if (!last) vb[at] = V;
-                    if (ATTRS) dv.key[at] = best < CUDART_INF ? bkey : -1;
+                    if (last) {
+                        store_at(at, fast, fb, best, bkey, bwin);
+                    } else {
+                        vb[at] = V;
+                        carry[at] = best;
+                        if (ATTRS) dv.key[at] = best < CUDART_INF ? bkey : -1;
+                        if (!EXACT) win[at] = bwin;
+                    }
                 }
             }
             first = false;
@@ -451,7 +523,7 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
     }
 }
 
-template <bool ATTRS, bool STATS, bool CROWDED>
+template <bool ATTRS, bool STATS, bool CROWDED, bool EXACT>
 __global__ void TX_BOUNDS k_texels(TriStore ts, DepthView dv, CoarseBins cb, int tiles_x,
                                    int tiles_per_fix, int64_t n_items,
                                    const GmFixExact* __restrict__ fixes, long long b0) {
@@ -461,7 +533,7 @@ __global__ void TX_BOUNDS k_texels(TriStore ts, DepthView dv, CoarseBins cb, int
     if (!CROWDED) {
         const int64_t item = (int64_t)blockIdx.x * TW_WARPS + warp;
         if (item < n_items)
-            texel_item<ATTRS, STATS, false>(reinterpret_cast<TexelWarpSmem*>(tx_dyn)[warp].t32,
+            texel_item<ATTRS, STATS, false, EXACT>(reinterpret_cast<TexelWarpSmem*>(tx_dyn)[warp].t32,
                                             reinterpret_cast<TexelWarpSmem*>(tx_dyn)[warp].sel, nullptr, item, ts, dv,
                                             cb, tiles_x, tiles_per_fix, fixes);
         return;
@@ -474,7 +546,7 @@ __global__ void TX_BOUNDS k_texels(TriStore ts, DepthView dv, CoarseBins cb, int
         if (lane == 0) w = atomicAdd(dv.crowd_count + 1, 1);
         w = __shfl_sync(0xffffffffu, w, 0);
         if (w >= n_crowd) break;
-        texel_item<ATTRS, STATS, true>(C.t32, C.sel, C.key, dv.crowd[w], ts, dv, cb, tiles_x, tiles_per_fix, fixes);
+        texel_item<ATTRS, STATS, true, EXACT>(C.t32, C.sel, C.key, dv.crowd[w], ts, dv, cb, tiles_x, tiles_per_fix, fixes);
     }
 }
 
