@@ -323,7 +323,24 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
         float2 o;
         int w = bwin;
         if (fast) {
+#ifndef GM_RCP_EXACT
+            // depth in [1/fb.y, 1/fb.x] (fb >= 1/far' > 0): rcp.approx is within 1 ulp
+            // (PTX ISA), the 1e-6 widening covers it with room to spare
+            float rl, rh;
+            asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rl) : "f"(fb.y));
+            asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rh) : "f"(fb.x));
+            o = make_float2(rl * (1.0f - 1e-6f), rh * (1.0f + 1e-6f));
+#else
             o = make_float2(__frcp_rd(fb.y), __frcp_ru(fb.x));
+#endif
+#ifdef GM_CHECK_BOUNDS  // debug build: verify the bounds against the exact depth
+            {
+                const double ex = texel_depth(seg[w], (int)(at % W), (int)(at / W), near_, far_);
+                if (!(ex >= (double)o.x && ex <= (double)o.y))
+                    printf("BOUND VIOLATION f=%d at=%lld exact=%.17g lo=%.9g hi=%.9g fb=(%.9g,%.9g)\n", f,
+                           (long long)at, ex, o.x, o.y, fb.x, fb.y);
+            }
+#endif
         } else if (best < CUDART_INF) {
             o = make_float2(__double2float_rd(best), __double2float_ru(best));
         } else {
@@ -404,6 +421,22 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
                 if (cursor >= n) break;
                 nsel = gather(cursor);
                 if (STATS) nsel_total += nsel;
+                if (nsel == 0 && cursor >= n && !first) {
+                    // the final rescan found nothing more: the last staged chunk was not
+                    // flagged `last`, so publish the carried state now
+                    for (int r0 = 0; r0 < total; r0 += 32) {
+                        const int q = r0 + lane;
+                        int row, colo;
+                        texel_of(q, row, colo);
+                        if (q < total) {
+                            const int64_t at = (int64_t)(yb + row) * W + xb + colo;
+                            const double best = carry[at];
+                            store_at(at, false, make_float2(0.0f, 0.0f), best, ATTRS ? dv.key[at] : -1,
+                                     EXACT ? -1 : win[at]);
+                        }
+                    }
+                    break;
+                }
             }
             if (first) {  // no triangle at all
                 for (int r0 = 0; r0 < total; r0 += 32) {
