@@ -351,9 +351,10 @@ def run_ours(args, rank, world):
     # algorithmic FP64 flops per unit, counted from the reference source (kernels.py):
     #   exact sample evaluation (camera transform :305-307 + NDC projection :314-315) 26
     #   cone test (:330-337) 14, depth test (:323-327 + bilinear :231-261) 24
-    #   texel pair (3 edge functions :107-109, 23) + covered texel (l, inv_w, 1/inv_w :119-125, 9)
+    #   marked texel: the writer's exact pixel test -- 3 edge functions (:107-109, 23) + l, inv_w,
+    #   1/inv_w (:119-125, 9) -- whether k_texels evaluates it in float64 or proves it with float32 bounds
     fl = {"k_samples<mark>": 26 * st["exact_evals"] + 14 * st["ndc_candidates"],
-          "k_texels": 23 * st["texel_pairs"] + 9 * st["covered_pairs"],
+          "k_texels": 32 * st["texels"],
           "k_samples<accumulate>": 26 * st["exact_evals"] + 14 * st["ndc_candidates"] + 24 * st["cone_candidates"]}
     times = {"k_samples<mark>": tm.mark_ms, "k_texels": tm.texel_ms, "k_samples<accumulate>": tm.accumulate_ms,
              "k_tri_setup": tm.cull_ms}
