@@ -756,10 +756,13 @@ static int dev_alloc(T** p, size_t n) {
 }
 
 #define GM_RING 3  // pinned host setup slots in flight
+#ifndef GM_NSETS
+#define GM_NSETS 3  // batch-buffer sets / streams in the overlapped batch pipeline
+#endif
 
-// Everything one batch of fixations owns on the device.  A plan holds two sets
-// (the plan's own fields and `alt`); consecutive batches alternate between them
-// and between two streams, so batch i + 1's occluder setup, marking and texel
+// Everything one batch of fixations owns on the device.  A plan holds GM_NSETS
+// sets (the plan's own fields and `alt[]`); consecutive batches rotate over them
+// and over as many streams, so batch i + 1's occluder setup, marking and texel
 // kernels overlap batch i's tail.  Only the accumulation pass (k_samples) is
 // chained across batches (event), which keeps the per-sample log order.
 #define GM_BATCH_FIELDS(X)                                                                            \
@@ -857,15 +860,15 @@ struct gm_plan {
     int* d_crowd_count = nullptr;  // [2]
     int64_t cap_crowd = 0;
     int64_t cap_key = 0;
-    int64_t cap_cbits = 0, cap_sort = 0;  // (per batch-buffer set, swapped with alt)
+    int64_t cap_cbits = 0, cap_sort = 0;  // (per batch-buffer set, swapped with alt[])
     int cap_ring = 0;
-    BatchBufs alt;                   // the second batch-buffer set (and stream)
+    BatchBufs alt[GM_NSETS - 1];     // the other batch-buffer sets (and streams)
     cudaEvent_t ev_order = nullptr;  // last accumulation pass enqueued (chains k_samples across streams)
 };
 
 // Exchange the plan's batch buffers (and stream) with the alternate set.
-static void swap_batch_bufs(gm_plan* p) {
-#define GM_X(T, n) std::swap(p->n, p->alt.n);
+static void swap_batch_bufs(gm_plan* p, int k = 1) {
+#define GM_X(T, n) std::swap(p->n, p->alt[k - 1].n);
     GM_BATCH_FIELDS(GM_X)
 #undef GM_X
 }
@@ -885,9 +888,11 @@ static void plan_free_scene(gm_plan* p) {
     p->d_pxf = p->d_pyf = p->d_pzf = nullptr;
     cudaFree(p->d_chunk); cudaFree(p->d_values); cudaFree(p->d_super);
     free_scene_batch_bufs(p);
-    swap_batch_bufs(p);
-    free_scene_batch_bufs(p);
-    swap_batch_bufs(p);
+    for (int k = 1; k < GM_NSETS; k++) {
+        swap_batch_bufs(p, k);
+        free_scene_batch_bufs(p);
+        swap_batch_bufs(p, k);
+    }
     p->d_tw = nullptr; p->d_tsph = p->d_csph = p->d_chunk = p->d_super = nullptr;
     p->d_px = p->d_py = p->d_pz = p->d_values = nullptr;
     p->T = p->n_clu = p->N = p->n_chunks = p->n_supers = 0;
@@ -957,7 +962,8 @@ extern "C" void gm_plan_destroy(gm_plan* p) {
     if (!p) return;
     cudaSetDevice(p->device);
     cudaStreamSynchronize(p->stream);
-    if (p->alt.stream) cudaStreamSynchronize(p->alt.stream);
+    for (int k = 0; k < GM_NSETS - 1; k++)
+        if (p->alt[k].stream) cudaStreamSynchronize(p->alt[k].stream);
     plan_free_scene(p);
     for (int r = 0; r < GM_RING; r++) {
         cudaFreeHost(p->h_fix[r]); cudaFreeHost(p->h_cull[r]); cudaEventDestroy(p->h_ev[r]);
@@ -968,8 +974,10 @@ extern "C" void gm_plan_destroy(gm_plan* p) {
     cudaFree(p->d_key);
     if (p->ev_order) cudaEventDestroy(p->ev_order);
     free_batch_set(p);
-    swap_batch_bufs(p);
-    free_batch_set(p);
+    for (int k = 1; k < GM_NSETS; k++) {
+        swap_batch_bufs(p, k);
+        free_batch_set(p);
+    }
     delete p;
 }
 
@@ -1216,9 +1224,11 @@ static int ensure_batch(gm_plan* p, int B, int W, int H, int64_t seg, bool both 
     }
     if ((rc = ensure_batch_set(p, B, W, H, seg))) return rc;
     if (!both) return GM_OK;
-    swap_batch_bufs(p);
-    rc = ensure_batch_set(p, B, W, H, std::max(seg, p->alt.cap_seg));
-    swap_batch_bufs(p);
+    for (int k = 1; k < GM_NSETS && !rc; k++) {
+        swap_batch_bufs(p, k);
+        rc = ensure_batch_set(p, B, W, H, std::max(seg, p->cap_seg));
+        swap_batch_bufs(p, k);
+    }
     return rc;
 }
 
@@ -1351,19 +1361,21 @@ static int run_batches(gm_plan* p, const double* fx, int64_t F, const GmConfig* 
     int rc = ensure_batch(p, B, W, H, std::max<int64_t>(p->cap_seg, 16384), two);
     if (rc) return rc;
     cudaStream_t s = p->stream;          // primary stream (even batches)
-    cudaStream_t s2 = p->alt.stream;     // odd batches
+
     cudaEvent_t ev_fork = nullptr;
     CK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
-    auto fork = [&]() -> int {  // everything enqueued on s so far precedes what s2 runs next
+    auto fork = [&]() -> int {  // everything enqueued on s so far precedes what the other streams run next
         if (!two) return GM_OK;
         CK(cudaEventRecord(ev_fork, s));
-        CK(cudaStreamWaitEvent(s2, ev_fork, 0));
+        for (int k = 0; k < GM_NSETS - 1; k++) CK(cudaStreamWaitEvent(p->alt[k].stream, ev_fork, 0));
         return GM_OK;
     };
-    auto join = [&]() -> int {  // s waits for everything enqueued on s2
+    auto join = [&]() -> int {  // s waits for everything enqueued on the other streams
         if (!two) return GM_OK;
-        CK(cudaEventRecord(ev_fork, s2));
-        CK(cudaStreamWaitEvent(s, ev_fork, 0));
+        for (int k = 0; k < GM_NSETS - 1; k++) {
+            CK(cudaEventRecord(ev_fork, p->alt[k].stream));
+            CK(cudaStreamWaitEvent(s, ev_fork, 0));
+        }
         return GM_OK;
     };
     cudaEvent_t ev_start = nullptr, ev_end = nullptr;
@@ -1397,17 +1409,17 @@ static int run_batches(gm_plan* p, const double* fx, int64_t F, const GmConfig* 
         if ((rc = fork())) return rc;
         int slot = 0;
         int parity = 0;
-        for (int64_t b0 = start; b0 < F; b0 += B, parity ^= (two ? 1 : 0)) {
+        for (int64_t b0 = start; b0 < F; b0 += B, parity = two ? (parity + 1) % GM_NSETS : 0) {
             int nb = (int)std::min<int64_t>(B, F - b0);
             // odd batches run on the alternate buffer set and stream
             struct SwapGuard {
                 gm_plan* p;
-                bool on;
+                int k;
                 ~SwapGuard() {
-                    if (on) swap_batch_bufs(p);
+                    if (k) swap_batch_bufs(p, k);
                 }
-            } guard{p, parity == 1};
-            if (parity) swap_batch_bufs(p);
+            } guard{p, parity};
+            if (parity) swap_batch_bufs(p, parity);
             cudaStream_t s = p->stream;
             const GmFixExact* d_fix = p->d_fix;
             const GmFixCull* d_cull = p->d_cull;
@@ -1466,7 +1478,7 @@ static int run_batches(gm_plan* p, const double* fx, int64_t F, const GmConfig* 
         // grow the per-fixation segments and resume at the first failed batch
         int64_t want = std::max<int64_t>(2 * p->cap_seg, (int64_t)maxcount + maxcount / 4 + 64);
         p->cap_seg = 0;
-        p->alt.cap_seg = 0;
+        for (int k = 0; k < GM_NSETS - 1; k++) p->alt[k].cap_seg = 0;
         rc = ensure_batch(p, B, W, H, want, two);
         if (rc) {
             cleanup();
