@@ -168,11 +168,14 @@ __global__ void KM_BOUNDS k_mark(const float* __restrict__ pxf, const float* __r
                 if (!exact) {
                     // NDC (kernels.py:314-319) with bound dq on |q32 - q_exact|
                     const float nx = __fmaf_rn(Q.p00, x, Q.p02 * z), ny = __fmaf_rn(Q.p11, y, Q.p12 * z);
-                    const float qx = nx / w, qy = ny / w;
+                    // fast divisions (<= 2 ulp): covered by the 1e-6 relative slack of dq below
+                    const float rw = __fdividef(1.0f, w);
+                    const float qx = nx * rw, qy = ny * rw;
                     const float en_x = (fabsf(Q.p00) + fabsf(Q.p02)) * E + 4e-7f * (fabsf(Q.p00 * x) + fabsf(Q.p02 * z));
                     const float en_y = (fabsf(Q.p11) + fabsf(Q.p12)) * E + 4e-7f * (fabsf(Q.p11 * y) + fabsf(Q.p12 * z));
-                    const float dqx = (en_x + fabsf(qx) * E) / wl + 1e-6f * fabsf(qx) + 1e-7f;
-                    const float dqy = (en_y + fabsf(qy) * E) / wl + 1e-6f * fabsf(qy) + 1e-7f;
+                    const float rwl = __fdividef(1.0f, wl) * (1.0f + 1e-6f);
+                    const float dqx = (en_x + fabsf(qx) * E) * rwl + 1e-6f * fabsf(qx) + 1e-7f;
+                    const float dqy = (en_y + fabsf(qy) * E) * rwl + 1e-6f * fabsf(qy) + 1e-7f;
                     if (qx + dqx < lo || qx - dqx > hi || qy + dqy < lo || qy - dqy > hi) continue;
                     // cone (kernels.py:330-339): d1 > 0 and ratio^2 <= 16
                     const float d1 = __fmaf_rn(x, Q.gaze[0], __fmaf_rn(y, Q.gaze[1], z * Q.gaze[2]));
