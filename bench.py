@@ -375,7 +375,7 @@ def run_ours(args, rank, world):
     traffic, hbm, issue = None, None, None
     tpath = ROOT / "profiles" / "r1_ncu_traffic.json"
     kname = {"k_samples<mark>": "k_mark", "k_samples<accumulate>": "k_samples<0>",
-             "k_texels": "k_texels<0, 0, 0>"}.get(dom, dom)
+             "k_texels": "k_texels<0, 0, 0, 0>"}.get(dom, dom)
     if tpath.exists():
         tk = json.loads(tpath.read_text())["kernels"].get(kname)
         if tk and int(tm.batches):
