@@ -10,9 +10,6 @@
 
 #include "gm_types.h"
 
-#define GM_BIN_SHIFT 4  // 16 x 16 pixel screen bins
-#define GM_BIN 16
-
 namespace gm {
 
 // numba int(np.ceil(x)) / int(np.floor(x)) on x86-64: cvttsd2si returns

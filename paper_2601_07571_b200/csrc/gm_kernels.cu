@@ -522,50 +522,6 @@ __device__ __forceinline__ void stat_add(unsigned long long* stats, int idx, uns
                   (unsigned long long)lo + ((unsigned long long)hi << 32));
 }
 
-// kernels.py:219-285 depth_match, reading the texels k_texels evaluated
-// (the 3x3 block around rint(g), which contains the bilinear quad).
-__device__ __forceinline__ bool depth_test(const DepthView& dv, int f, double gx, double gy, int bx0, int bx1,
-                                           int by0, int by1, double d, double eps) {
-    const int W = dv.W, H = dv.H;
-    const double* dep = dv.depth + (int64_t)f * W * H;
-    if (W > 1 && H > 1) {
-        long long x0 = x86_i64(floor(gx));
-        if (x0 < 0) x0 = 0;
-        else if (x0 > W - 2) x0 = W - 2;
-        long long y0 = x86_i64(floor(gy));
-        if (y0 < 0) y0 = 0;
-        else if (y0 > H - 2) y0 = H - 2;
-        const double* r0 = dep + (int64_t)y0 * W + x0;
-        double q00 = r0[0], q01 = r0[1], q10 = r0[W], q11 = r0[W + 1];
-        if (isfinite(q00) && isfinite(q01) && isfinite(q10) && isfinite(q11)) {
-            double tx = gx - (double)x0;
-            if (tx < 0.0) tx = 0.0;
-            else if (tx > 1.0) tx = 1.0;
-            double ty = gy - (double)y0;
-            if (ty < 0.0) ty = 0.0;
-            else if (ty > 1.0) ty = 1.0;
-            double top = q00 * (1.0 - tx) + q01 * tx;
-            double bot = q10 * (1.0 - tx) + q11 * tx;
-            if (fabs(d - (top * (1.0 - ty) + bot * ty)) <= eps) return true;
-            double hi = fmax(fmax(q00, q01), fmax(q10, q11));
-            double lo = fmin(fmin(q00, q01), fmin(q10, q11));
-            if (hi - lo <= eps) return false;
-        }
-    }
-    double best = CUDART_INF;
-    for (int yy = by0; yy <= by1; yy++) {
-        const double* row = dep + (int64_t)yy * W;
-        for (int xx = bx0; xx <= bx1; xx++) {
-            const double t = row[xx];
-            if (isfinite(t)) {
-                double diff = fabs(t - d);
-                if (diff < best) best = diff;
-            }
-        }
-    }
-    return best <= eps;
-}
-
 // depth_match on a generation batch's texel store: every texel holds rigorous
 // float32 bounds [lo, hi] of the float64 depth kernels.rasterize leaves there
 // ((+inf, +inf) where nothing is written) and the segment index of its writer.
