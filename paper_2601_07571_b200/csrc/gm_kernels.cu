@@ -400,7 +400,7 @@ __global__ void __launch_bounds__(TS_WARPS * 32) k_tri_setup(const double* __res
 #define CB_ITEMS_PER_TRI 4  // coarse-bin list capacity per screen triangle (more: scan the whole list)
 #endif
 struct CoarseBins {
-    int* items;   // [B][cap_items]
+    int4* items;  // [B][cap_items]: (segment index, bbox x0|x1<<16, bbox y0|y1<<16, float bits of inv_minw)
     int* off;     // [B][GM_MAX_CBINS + 1]
     int* ovf;     // [B]
     int64_t cap_items;
@@ -454,15 +454,18 @@ __global__ void __launch_bounds__(256) k_coarse(TriStore ts, CoarseBins cb, cons
     if (threadIdx.x == 0) cb.ovf[f] = 0;
     for (int b = threadIdx.x; b < nbins; b += blockDim.x) s_cnt[b] = 0;
     __syncthreads();
-    int* items = cb.items + (int64_t)f * cb.cap_items;
+    int4* items = cb.items + (int64_t)f * cb.cap_items;
+    const TriF32* segf = ts.t32 + (int64_t)f * ts.cap_seg;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
         const uint2 bb = segb[i];
+        // the entry carries what k_texels' gather and sort read, so neither chases the index
+        const int4 e = make_int4(i, (int)bb.x, (int)bb.y, __float_as_int(segf[i].inv_minw));
         const int bx0 = (bb.x & 0xffff) >> cb.shift, bx1 = (bb.x >> 16) >> cb.shift;
         const int by0 = (bb.y & 0xffff) >> cb.shift, by1 = (bb.y >> 16) >> cb.shift;
         for (int by = by0; by <= by1; by++)
             for (int bx = bx0; bx <= bx1; bx++) {
                 const int b = by * cb.ncx + bx;
-                items[s_off[b] + atomicAdd(&s_cnt[b], 1)] = i;
+                items[s_off[b] + atomicAdd(&s_cnt[b], 1)] = e;
             }
     }
 }
@@ -729,7 +732,7 @@ static int dev_alloc(T** p, size_t n) {
     X(TriF32*, d_t32) X(uint2*, d_bbox) X(int*, d_count) X(int64_t, cap_seg) X(int64_t, cap_seg_B)     \
     X(double*, d_depth) X(float*, d_vbuf) X(uint32_t*, d_mask) X(int64_t, cap_depth) X(int64_t, cap_mask) \
     X(int*, d_win) X(double*, d_carry)                                                                 \
-    X(int*, d_citems) X(int*, d_coff) X(int*, d_covf) X(int64_t, cap_citems) X(int64_t, cap_cB)         \
+    X(int4*, d_citems) X(int*, d_coff) X(int*, d_covf) X(int64_t, cap_citems) X(int64_t, cap_cB)         \
     X(int*, d_crowd) X(int*, d_crowd_count) X(int64_t, cap_crowd)
 
 struct BatchBufs {
@@ -785,7 +788,7 @@ struct gm_plan {
     double* d_carry = nullptr;   // [B][H][W] k_texels' exact best between chunks
     uint32_t* d_mask = nullptr;  // [B][H][wwords]
     int64_t cap_depth = 0, cap_mask = 0;
-    int* d_citems = nullptr;  // coarse bins: [B][cap_citems]
+    int4* d_citems = nullptr;  // coarse bins: [B][cap_citems]
     int* d_coff = nullptr;    // [B][GM_MAX_CBINS + 1]
     int* d_covf = nullptr;    // [B]
     int64_t cap_citems = 0, cap_cB = 0;

@@ -12,6 +12,7 @@
 struct __align__(16) TexelWarpSmem {
     TriF32 t32[TW_CAP];  // staged, in ascending min-depth order
     int sel[TW_SEL + 32];
+    float key[TW_SEL + 32];  // -inv_minw of sel[] (sort key: ascending min depth)
 };
 #define TX_DYN_SMEM (TW_WARPS * (int)sizeof(TexelWarpSmem))
 #define TC_SEL 512   // crowded tiles: overlap list sorted per pass (longer lists: several passes)
@@ -105,7 +106,8 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
     const float inv_far_lo = inv_far * (1.0f - 1e-5f), inv_far_hi = inv_far * (1.0f + 1e-5f);
     const GmScreenTri* seg = ts.tris + (int64_t)f * ts.cap_seg;
     const uint2* segb = ts.bbox + (int64_t)f * ts.cap_seg;
-    const int* clist = nullptr;
+    const int4* clist = nullptr;
+    const TriF32* segf = ts.t32 + (int64_t)f * ts.cap_seg;
     int n = min(ts.count[f], (int)ts.cap_seg);
     if (!cb.ovf[f]) {
         const int* off = cb.off + (int64_t)f * (GM_MAX_CBINS + 1);
@@ -123,15 +125,28 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
         while (cursor < n && cnt < TW_SEL) {
             int i = cursor + lane;
             bool sel = false;
+            float key = 0.0f;
             if (i < n) {
-                if (clist) i = clist[i];
-                const uint2 bbx = segb[i];
+                uint2 bbx;
+                if (clist) {
+                    const int4 e = clist[i];
+                    i = e.x;
+                    bbx = make_uint2((uint32_t)e.y, (uint32_t)e.z);
+                    key = -__int_as_float(e.w);
+                } else {
+                    bbx = segb[i];
+                    key = -__ldg(&segf[i].inv_minw);
+                }
                 const int x0 = bbx.x & 0xffff, x1 = bbx.x >> 16, y0 = bbx.y & 0xffff, y1 = bbx.y >> 16;
                 sel = !(x1 < xb || x0 > xe || y1 < yb || y0 > ye);
                 if (sel) cover += (min(x1, xe) - max(x0, xb) + 1) * (min(y1, ye) - max(y0, yb) + 1);
             }
             const unsigned bal = __ballot_sync(FULL, sel);
-            if (sel) SEL[cnt + __popc(bal & ((1u << lane) - 1u))] = i;
+            if (sel) {
+                const int at = cnt + __popc(bal & ((1u << lane) - 1u));
+                SEL[at] = i;
+                KEY[at] = key;
+            }
             cnt += __popc(bal);
             cursor += 32;
         }
@@ -140,11 +155,10 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
     };
 
     // 2. stage SEL[c0 .. c0 + kend) (float32 forms) in ascending min-depth order
-    const TriF32* segf = ts.t32 + (int64_t)f * ts.cap_seg;
     auto stage = [&](int c0, int kend) {
         __syncwarp();
         const int gi = lane < kend ? SEL[c0 + lane] : 0;
-        float key = lane < kend ? -__ldg(&segf[gi].inv_minw) : CUDART_INF_F;  // ascending min depth
+        float key = lane < kend ? KEY[c0 + lane] : CUDART_INF_F;  // ascending min depth
         int slot = lane;
 #pragma unroll
         for (int size = 2; size <= 32; size <<= 1) {
@@ -460,9 +474,18 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
             while (cursor < n && cnt < TC_SEL - 32) {
                 int i = cursor + lane;
                 bool sel = false;
+                float key = 0.0f;
                 if (i < n) {
-                    if (clist) i = clist[i];
-                    const uint2 bbx = segb[i];
+                    uint2 bbx;
+                    if (clist) {
+                        const int4 e = clist[i];
+                        i = e.x;
+                        bbx = make_uint2((uint32_t)e.y, (uint32_t)e.z);
+                        key = -__int_as_float(e.w);
+                    } else {
+                        bbx = segb[i];
+                        key = -__ldg(&segf[i].inv_minw);
+                    }
                     const int x0 = bbx.x & 0xffff, x1 = bbx.x >> 16, y0 = bbx.y & 0xffff, y1 = bbx.y >> 16;
                     sel = !(x1 < xb || x0 > xe || y1 < yb || y0 > ye);
                 }
@@ -470,7 +493,7 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
                 if (sel) {
                     const int at = cnt + __popc(bal & ((1u << lane) - 1u));
                     SEL[at] = i;
-                    KEY[at] = -__ldg(&segf[i].inv_minw);
+                    KEY[at] = key;
                 }
                 cnt += __popc(bal);
                 cursor += 32;
@@ -567,7 +590,8 @@ __global__ void TX_BOUNDS k_texels(TriStore ts, DepthView dv, CoarseBins cb, int
         const int64_t item = (int64_t)blockIdx.x * TW_WARPS + warp;
         if (item < n_items)
             texel_item<ATTRS, STATS, false, EXACT>(reinterpret_cast<TexelWarpSmem*>(tx_dyn)[warp].t32,
-                                            reinterpret_cast<TexelWarpSmem*>(tx_dyn)[warp].sel, nullptr, item, ts, dv,
+                                            reinterpret_cast<TexelWarpSmem*>(tx_dyn)[warp].sel,
+                                            reinterpret_cast<TexelWarpSmem*>(tx_dyn)[warp].key, item, ts, dv,
                                             cb, tiles_x, tiles_per_fix, fixes);
         return;
     }
