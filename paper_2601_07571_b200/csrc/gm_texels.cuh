@@ -87,6 +87,11 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
     // marked texels: lane r < TH holds the mask word of row yb + r
     uint32_t wr = 0;
     if (lane < TH && yb + lane < H) wr = dv.mask[((int64_t)f * H + yb + lane) * dv.wwords + (xb >> 5)];
+    // per-fixation values every non-empty tile needs, loaded alongside the mask (independent of it)
+    const int bb = (yb >> cb.shift) * cb.ncx + (xb >> cb.shift);
+    const int* off = cb.off + (int64_t)f * (GM_MAX_CBINS + 1);
+    const int ovf = cb.ovf[f], off0 = off[bb], off1 = off[bb + 1], count_f = ts.count[f];
+    const double near_ = fixes[f].near_, far_ = fixes[f].far_;
     const int cnt_r = __popc(wr);
     int pref = cnt_r;  // inclusive prefix over rows
 #pragma unroll
@@ -97,8 +102,6 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
     const int total = __shfl_sync(FULL, pref, 31);
     if (total == 0) return;
     const int pref_ex = pref - cnt_r;
-    const GmFixExact& F = fixes[f];
-    const double near_ = F.near_, far_ = F.far_;
     // written iff near' <= 1/inv_w <= far' (kernels.py:123-127): certainly inside
     // [inv_far_hi, inv_near_lo], certainly outside beyond [inv_far_lo, inv_near_hi]
     const float inv_near = (float)(1.0 / near_), inv_far = (float)(1.0 / far_);
@@ -108,12 +111,10 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
     const uint2* segb = ts.bbox + (int64_t)f * ts.cap_seg;
     const int4* clist = nullptr;
     const TriF32* segf = ts.t32 + (int64_t)f * ts.cap_seg;
-    int n = min(ts.count[f], (int)ts.cap_seg);
-    if (!cb.ovf[f]) {
-        const int* off = cb.off + (int64_t)f * (GM_MAX_CBINS + 1);
-        const int bb = (yb >> cb.shift) * cb.ncx + (xb >> cb.shift);
-        clist = cb.items + (int64_t)f * cb.cap_items + off[bb];
-        n = off[bb + 1] - off[bb];
+    int n = min(count_f, (int)ts.cap_seg);
+    if (!ovf) {
+        clist = cb.items + (int64_t)f * cb.cap_items + off0;
+        n = off1 - off0;
     }
     const int xe = xb + TW - 1, ye = yb + TH - 1;
     unsigned long long c_pairs = 0, c_cov = 0, c_iter = 0, c_edge = 0;
