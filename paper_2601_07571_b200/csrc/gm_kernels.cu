@@ -394,10 +394,10 @@ __global__ void __launch_bounds__(TS_WARPS * 32) k_tri_setup(const double* __res
 // not fit, covf[f] = 1 and k_texels scans the fixation's whole list instead.
 #define GM_MAX_CBINS 1024
 #ifndef CB_SHIFT
-#define CB_SHIFT 6  // coarse bins of 64 x 64 pixels (k_texels tiles are 32 x 16)
+#define CB_SHIFT 5  // coarse bins of 32 x 32 pixels (k_texels tiles are 32 x 16)
 #endif
 #ifndef CB_ITEMS_PER_TRI
-#define CB_ITEMS_PER_TRI 4  // coarse-bin list capacity per screen triangle (more: scan the whole list)
+#define CB_ITEMS_PER_TRI 8  // coarse-bin list capacity per screen triangle (more: scan the whole list)
 #endif
 struct CoarseBins {
     int4* items;  // [B][cap_items]: (segment index, bbox x0|x1<<16, bbox y0|y1<<16, float bits of inv_minw)
@@ -1193,7 +1193,7 @@ static int ensure_batch(gm_plan* p, int B, int W, int H, int64_t seg, bool both 
 
 typedef void (*gm_progress_fn)(int64_t done, int64_t total, void* user);
 
-// Coarse-bin geometry for a W x H buffer: cb = 64 px, doubled until <= GM_MAX_CBINS bins.
+// Coarse-bin geometry for a W x H buffer: cb = 2^CB_SHIFT px, doubled until <= GM_MAX_CBINS bins.
 static CoarseBins coarse_bins(gm_plan* p, int W, int H) {
     int shift = CB_SHIFT;
     while ((int64_t)((W + (1 << shift) - 1) >> shift) * ((H + (1 << shift) - 1) >> shift) > GM_MAX_CBINS) shift++;
