@@ -166,7 +166,8 @@ def test_generate_vs_golden(golden, case):
         _assert_values(dm.values[obj.object_id], golden[f"{p}val{i}"])
 
 
-@pytest.mark.parametrize("filtering,res,batch", [(True, 512, 0), (False, 512, 7), (True, 77, 3), (False, 1, 0)])
+@pytest.mark.parametrize("filtering,res,batch", [(True, 512, 0), (False, 512, 7), (True, 77, 3), (False, 1, 0),
+                                                 (True, 1000, 0), (False, 2048, 0)])
 def test_generate_vs_oracle(filtering, res, batch):
     import workloads as W
 
