@@ -12,6 +12,7 @@ fixation log order, so results are deterministic run to run.
 from __future__ import annotations
 
 import ctypes
+import os
 import math
 import time
 from dataclasses import dataclass, field
@@ -111,6 +112,12 @@ class ScenePlan:
         _native.check(lib.gm_plan_create(device, ctypes.byref(h)), "gm_plan_create")
         self._h = h
         self._lib = lib
+        # one process per GPU (torchrun): split the host cores between the local ranks so
+        # their fixation-setup thread pools do not oversubscribe the node
+        local = int(os.environ.get("LOCAL_WORLD_SIZE", "1") or 1)
+        if local > 1:
+            cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+            _native.check(lib.gm_plan_set_host_threads(h, max(1, cores // local)), "gm_plan_set_host_threads")
         objs = list(scene.objects)
         inc = set(included)
         tri_counts, tris, xforms, res, flags = [], [], [], [], []
