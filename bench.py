@@ -336,7 +336,7 @@ def run_ours(args, rank, world):
                "timing": "host wall clock around the API call"}
 
     # ---- algorithmic work of this step (one instrumented, untimed pass) ----
-    stats = (ctypes.c_uint64 * 16)()
+    stats = (ctypes.c_uint64 * len(_native.STAT_NAMES))()
     tm_s = _native.GmTimings()
     ms_s = ctypes.c_float(0.0)
     if not args.no_stats:

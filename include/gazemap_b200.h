@@ -154,7 +154,8 @@ int gm_plan_flush_l2(gm_plan* plan, int64_t bytes);
 /* Work counters of the last pass run with GmConfig.flags & 1: 16 x uint64 =
  * super-chunk tests, chunk tests, exact sample evaluations, NDC-filtered
  * samples, in-cone candidates, visible contributions, marked texels, exact
- * (texel, triangle) evaluations, covered pairs, reserved. */
+ * (texel, triangle) evaluations, covered pairs, depth tests decided by the
+ * tile-max occlusion test, 6 k_texels counters (names: _native.STAT_NAMES). */
 int gm_plan_stats(gm_plan* plan, unsigned long long* out);
 
 /* Running global max (density.py:192) of the plan's values. */

@@ -43,7 +43,10 @@
 #endif
 // launch bounds of the hot kernels; -DTX_MINB=n etc. (build variants) cap
 // their registers for n CTAs per SM
-#ifdef TX_MINB
+#ifndef TX_MINB
+#define TX_MINB 7  // 72 registers (the tile-max reduction would otherwise push k_texels to 80)
+#endif
+#if TX_MINB > 0
 #define TX_BOUNDS __launch_bounds__(TX_MAX_THREADS, TX_MINB)
 #else
 #define TX_BOUNDS __launch_bounds__(TX_MAX_THREADS)
@@ -486,6 +489,10 @@ struct DepthView {
     double* carry;    // [B][H][W] (generation batches): exact best depth between chunks of a tile
     int* crowd;       // work items deferred to k_texels<CROWDED> (nullptr: handle them in place)
     int* crowd_count; // [2]: deferred items, claimed items
+    float* tmax;      // [B][tiles] (generation batches): largest finite depth upper bound of the
+                      // tile's marked texels, -inf if none (k_texels; tiles without marked
+                      // texels are not written); nullptr = off
+    int tiles_x, tiles_per_fix;
 };
 
 // Work counters filled when GmConfig.flags & GM_FLAG_STATS (bench roofline).
@@ -499,6 +506,7 @@ enum {
     GM_STAT_TEXELS = 6,      // marked texels evaluated
     GM_STAT_PAIRS = 7,       // (texel, screen triangle) exact evaluations
     GM_STAT_COVERED = 8,     // pairs where the triangle covers the texel
+    GM_STAT_TILE_OCCLUDED = 9,  // depth tests decided by the tile-max occlusion pre-test (float64 depth)
     GM_STAT_TX_TILES = 10,   // k_texels work items with marked texels
     GM_STAT_TX_STAGED = 11,  // triangles staged per item (sum)
     GM_STAT_TX_LIST = 12,    // coarse-bin list entries scanned per item (sum)
@@ -635,6 +643,27 @@ __device__ __forceinline__ bool depth_test_iv(const DepthView& dv, const GmScree
     return depth_test_exact(dv, seg, near_, far_, f, gx, gy, bx0, bx1, by0, by1, d, eps);
 }
 
+// Occlusion pre-test of depth_match (kernels.py:219-285): every texel the test
+// can read lies in the 3x3 block (the bilinear quad is inside it), and the test
+// can only succeed on a finite texel t with |t - d| <= eps.  If d - eps exceeds
+// the largest finite depth bound of every k_texels tile the block touches,
+// no such texel exists and the reference returns False (the relative slack
+// covers its float64 rounding of the bilinear blend and of |t - d|).
+__device__ __forceinline__ bool occluded_by_tiles(const DepthView& dv, int f, int bx0, int bx1, int by0, int by1,
+                                                  double d, double eps) {
+    const float* tm = dv.tmax + (int64_t)f * dv.tiles_per_fix;
+    const int tx0 = bx0 / TW, tx1 = bx1 / TW, ty0 = by0 / TH, ty1 = by1 / TH;
+    float m = tm[ty0 * dv.tiles_x + tx0];
+    if (tx1 != tx0) m = fmaxf(m, tm[ty0 * dv.tiles_x + tx1]);
+    if (ty1 != ty0) {
+        m = fmaxf(m, tm[ty1 * dv.tiles_x + tx0]);
+        if (tx1 != tx0) m = fmaxf(m, tm[ty1 * dv.tiles_x + tx1]);
+    }
+    if (!(m > -CUDART_INF_F)) return true;  // no finite texel at all: best stays +inf
+    const double mm = (double)m;
+    return (d - mm) - eps > 1e-12 * (fabs(d) + eps + mm);
+}
+
 #include "gm_samples.cuh"
 
 #include "gm_texels.cuh"
@@ -733,7 +762,7 @@ static int dev_alloc(T** p, size_t n) {
     X(double*, d_depth) X(float*, d_vbuf) X(uint32_t*, d_mask) X(int64_t, cap_depth) X(int64_t, cap_mask) \
     X(int*, d_win) X(double*, d_carry)                                                                 \
     X(int4*, d_citems) X(int*, d_coff) X(int*, d_covf) X(int64_t, cap_citems) X(int64_t, cap_cB)         \
-    X(int*, d_crowd) X(int*, d_crowd_count) X(int64_t, cap_crowd)
+    X(int*, d_crowd) X(int*, d_crowd_count) X(int64_t, cap_crowd) X(float*, d_tmax)
 
 struct BatchBufs {
 #define GM_X(T, n) T n{};
@@ -818,6 +847,7 @@ struct gm_plan {
     int* d_crowd = nullptr;        // [B * tiles] k_texels items deferred to the crowded pass
     int* d_crowd_count = nullptr;  // [2]
     int64_t cap_crowd = 0;
+    float* d_tmax = nullptr;       // [B * tiles] largest finite texel depth bound of each k_texels tile
     int64_t cap_key = 0;
     int64_t cap_cbits = 0, cap_sort = 0;  // (per batch-buffer set, swapped with alt[])
     int cap_ring = 0;
@@ -912,7 +942,7 @@ static void free_batch_set(gm_plan* p) {
     cudaFree(p->d_tris); cudaFree(p->d_t32); cudaFree(p->d_bbox); cudaFree(p->d_count);
     cudaFree(p->d_depth); cudaFree(p->d_mask); cudaFree(p->d_vbuf); cudaFree(p->d_win); cudaFree(p->d_carry);
     cudaFree(p->d_citems); cudaFree(p->d_coff); cudaFree(p->d_covf);
-    cudaFree(p->d_crowd); cudaFree(p->d_crowd_count);
+    cudaFree(p->d_crowd); cudaFree(p->d_crowd_count); cudaFree(p->d_tmax);
     if (p->stream) cudaStreamDestroy(p->stream);
     p->stream = nullptr;
 }
@@ -1157,6 +1187,7 @@ static int ensure_batch_set(gm_plan* p, int B, int W, int H, int64_t seg) {
     const int64_t n_tiles = (int64_t)B * ((W + TW - 1) / TW) * ((H + TH - 1) / TH);
     if (n_tiles > p->cap_crowd) {
         if ((rc = dev_alloc(&p->d_crowd, (size_t)n_tiles))) return rc;
+        if ((rc = dev_alloc(&p->d_tmax, (size_t)n_tiles))) return rc;
         if (!p->d_crowd_count && (rc = dev_alloc(&p->d_crowd_count, 2))) return rc;
         p->cap_crowd = n_tiles;
     }
@@ -1237,6 +1268,9 @@ static int enqueue_batch(gm_plan* p, const GmFixExact* d_fix, const GmFixCull* d
                  p->d_vbuf};
     dv.win = p->d_win;
     dv.carry = p->d_carry;
+    dv.tmax = p->d_tmax;
+    dv.tiles_x = (W + TW - 1) / TW;
+    dv.tiles_per_fix = dv.tiles_x * ((H + TH - 1) / TH);
     if (ev) CK(cudaEventRecord(ev[0], s));
     CK(cudaMemsetAsync(p->d_count, 0, sizeof(int) * nb, s));
     if (p->n_clu > 0) {

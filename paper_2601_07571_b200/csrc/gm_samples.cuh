@@ -99,6 +99,61 @@ __global__ void k_fix32(const GmFixExact* __restrict__ ex, int nb, double pmax, 
     out[f] = o;
 }
 
+// The float32 candidate test of one (sample, fixation) pair with rigorous
+// error bounds (kernels.py:305-339: camera transform, depth slab, NDC crop
+// filter, 4-sigma cone): GM_F32_REJECT only when the exact float64 test fails
+// too; GM_F32_BLOCK with the range [cxlo, cxhi] x [cylo, cyhi] of the exact
+// rint'ed texel coordinates; GM_F32_EXACT when the bounds are too loose to
+// decide (samples within ~E of the camera plane).  dlo: lower bound of the
+// exact depth w (GM_F32_BLOCK; up to float64 rounding).
+enum { GM_F32_REJECT = 0, GM_F32_BLOCK = 1, GM_F32_EXACT = 2 };
+__device__ __forceinline__ int mark_f32(const GmFixF32& Q, float wx, float wy, float wz, int W, int H, int& cxlo,
+                                        int& cxhi, int& cylo, int& cyhi, double& dlo) {
+    const float Wf = (float)W, Hf = (float)H;
+    const float lo = -1.0f - (float)GM_NDC_SLACK, hi = 1.0f + (float)GM_NDC_SLACK;
+    const float E = Q.E;
+    const float x = __fmaf_rn(Q.rot[2], wz, __fmaf_rn(Q.rot[1], wy, __fmaf_rn(Q.rot[0], wx, Q.trans[0])));
+    const float y = __fmaf_rn(Q.rot[5], wz, __fmaf_rn(Q.rot[4], wy, __fmaf_rn(Q.rot[3], wx, Q.trans[1])));
+    const float z = __fmaf_rn(Q.rot[8], wz, __fmaf_rn(Q.rot[7], wy, __fmaf_rn(Q.rot[6], wx, Q.trans[2])));
+    const float w = -z;
+    if (w + E <= 0.0f) return GM_F32_REJECT;                           // exact w <= 0
+    if (w + E < Q.near_lo || w - E > Q.far_hi) return GM_F32_REJECT;  // exact depth outside the slab
+    const float wl = w - E;
+    if (!(wl > 1e-3f * fabsf(w) + 1e-12f)) return GM_F32_EXACT;
+    dlo = (double)w - (double)E;
+    // NDC (kernels.py:314-319) with bound dq on |q32 - q_exact|
+    const float nx = __fmaf_rn(Q.p00, x, Q.p02 * z), ny = __fmaf_rn(Q.p11, y, Q.p12 * z);
+    // fast divisions (<= 2 ulp): covered by the 1e-6 relative slack of dq below
+    const float rw = __fdividef(1.0f, w);
+    const float qx = nx * rw, qy = ny * rw;
+    const float en_x = (fabsf(Q.p00) + fabsf(Q.p02)) * E + 4e-7f * (fabsf(Q.p00 * x) + fabsf(Q.p02 * z));
+    const float en_y = (fabsf(Q.p11) + fabsf(Q.p12)) * E + 4e-7f * (fabsf(Q.p11 * y) + fabsf(Q.p12 * z));
+    const float rwl = __fdividef(1.0f, wl) * (1.0f + 1e-6f);
+    const float dqx = (en_x + fabsf(qx) * E) * rwl + 1e-6f * fabsf(qx) + 1e-7f;
+    const float dqy = (en_y + fabsf(qy) * E) * rwl + 1e-6f * fabsf(qy) + 1e-7f;
+    if (qx + dqx < lo || qx - dqx > hi || qy + dqy < lo || qy - dqy > hi) return GM_F32_REJECT;
+    // cone (kernels.py:330-339): d1 > 0 and ratio^2 <= 16
+    const float d1 = __fmaf_rn(x, Q.gaze[0], __fmaf_rn(y, Q.gaze[1], z * Q.gaze[2]));
+    const float ed1 = 2.0f * E + 4e-7f * (fabsf(x) + fabsf(y) + fabsf(z));
+    if (d1 + ed1 <= 0.0f) return GM_F32_REJECT;
+    const float cx3 = y * Q.gaze[2] - z * Q.gaze[1], cy3 = z * Q.gaze[0] - x * Q.gaze[2];
+    const float cz3 = x * Q.gaze[1] - y * Q.gaze[0];
+    const float cr = sqrtf(__fmaf_rn(cx3, cx3, __fmaf_rn(cy3, cy3, cz3 * cz3)));
+    const float ecr = 3.0f * E + 1e-6f * (fabsf(x) + fabsf(y) + fabsf(z));
+    const float crl = cr - ecr, d1h = d1 + ed1;
+    if (crl > 0.0f && crl * crl > Q.sig16 * (1.0f + 1e-4f) * d1h * d1h) return GM_F32_REJECT;
+    // range of the exact g (texel coordinates); rint is monotone
+    const float gx = (qx + 1.0f) * 0.5f * Wf - 0.5f, gy = (1.0f - qy) * 0.5f * Hf - 0.5f;
+    const float dgx = dqx * 0.5f * Wf + 1e-4f + 1e-6f * fabsf(gx);
+    const float dgy = dqy * 0.5f * Hf + 1e-4f + 1e-6f * fabsf(gy);
+    if (dgx > 2.0f || dgy > 2.0f) return GM_F32_EXACT;
+    cxlo = (int)fminf(fmaxf(rintf(gx - dgx), 0.0f), (float)(W - 1));
+    cxhi = (int)fminf(fmaxf(rintf(gx + dgx), 0.0f), (float)(W - 1));
+    cylo = (int)fminf(fmaxf(rintf(gy - dgy), 0.0f), (float)(H - 1));
+    cyhi = (int)fminf(fmaxf(rintf(gy + dgy), 0.0f), (float)(H - 1));
+    return GM_F32_BLOCK;
+}
+
 // The marking pass: for every (sample, fixation) that can be a depth-test
 // candidate (kernels.py:305-339: NDC crop filter and 4-sigma cone), set the
 // mask bits of the texels depth_match may read.  Float32 with rigorous error
@@ -120,8 +175,6 @@ __global__ void KM_BOUNDS k_mark(const float* __restrict__ pxf, const float* __r
     const int lane = threadIdx.x & 31;
     const int ngroups = (B + 31) >> 5;
     const int W = dv.W, H = dv.H;
-    const float Wf = (float)W, Hf = (float)H;
-    const float lo = -1.0f - (float)GM_NDC_SLACK, hi = 1.0f + (float)GM_NDC_SLACK;
     const int64_t n_items = n_supers * 8;
     for (;;) {
         int item = 0;
@@ -154,53 +207,11 @@ __global__ void KM_BOUNDS k_mark(const float* __restrict__ pxf, const float* __r
                 mask &= mask - 1;
                 if (!valid) continue;
                 const int f = g + j;
-                const GmFixF32& Q = fix32[f];
-                const float E = Q.E;
-                const float x = __fmaf_rn(Q.rot[2], wz, __fmaf_rn(Q.rot[1], wy, __fmaf_rn(Q.rot[0], wx, Q.trans[0])));
-                const float y = __fmaf_rn(Q.rot[5], wz, __fmaf_rn(Q.rot[4], wy, __fmaf_rn(Q.rot[3], wx, Q.trans[1])));
-                const float z = __fmaf_rn(Q.rot[8], wz, __fmaf_rn(Q.rot[7], wy, __fmaf_rn(Q.rot[6], wx, Q.trans[2])));
-                const float w = -z;
-                if (w + E <= 0.0f) continue;                               // exact w <= 0
-                if (w + E < Q.near_lo || w - E > Q.far_hi) continue;      // exact depth outside the slab
-                const float wl = w - E;
-                float bxlo, bxhi, bylo, byhi;  // range of the exact g (texel coordinates)
-                bool exact = !(wl > 1e-3f * fabsf(w) + 1e-12f);
-                if (!exact) {
-                    // NDC (kernels.py:314-319) with bound dq on |q32 - q_exact|
-                    const float nx = __fmaf_rn(Q.p00, x, Q.p02 * z), ny = __fmaf_rn(Q.p11, y, Q.p12 * z);
-                    // fast divisions (<= 2 ulp): covered by the 1e-6 relative slack of dq below
-                    const float rw = __fdividef(1.0f, w);
-                    const float qx = nx * rw, qy = ny * rw;
-                    const float en_x = (fabsf(Q.p00) + fabsf(Q.p02)) * E + 4e-7f * (fabsf(Q.p00 * x) + fabsf(Q.p02 * z));
-                    const float en_y = (fabsf(Q.p11) + fabsf(Q.p12)) * E + 4e-7f * (fabsf(Q.p11 * y) + fabsf(Q.p12 * z));
-                    const float rwl = __fdividef(1.0f, wl) * (1.0f + 1e-6f);
-                    const float dqx = (en_x + fabsf(qx) * E) * rwl + 1e-6f * fabsf(qx) + 1e-7f;
-                    const float dqy = (en_y + fabsf(qy) * E) * rwl + 1e-6f * fabsf(qy) + 1e-7f;
-                    if (qx + dqx < lo || qx - dqx > hi || qy + dqy < lo || qy - dqy > hi) continue;
-                    // cone (kernels.py:330-339): d1 > 0 and ratio^2 <= 16
-                    const float d1 = __fmaf_rn(x, Q.gaze[0], __fmaf_rn(y, Q.gaze[1], z * Q.gaze[2]));
-                    const float ed1 = 2.0f * E + 4e-7f * (fabsf(x) + fabsf(y) + fabsf(z));
-                    if (d1 + ed1 <= 0.0f) continue;
-                    const float cx3 = y * Q.gaze[2] - z * Q.gaze[1], cy3 = z * Q.gaze[0] - x * Q.gaze[2];
-                    const float cz3 = x * Q.gaze[1] - y * Q.gaze[0];
-                    const float cr = sqrtf(__fmaf_rn(cx3, cx3, __fmaf_rn(cy3, cy3, cz3 * cz3)));
-                    const float ecr = 3.0f * E + 1e-6f * (fabsf(x) + fabsf(y) + fabsf(z));
-                    const float crl = cr - ecr, d1h = d1 + ed1;
-                    if (crl > 0.0f && crl * crl > Q.sig16 * (1.0f + 1e-4f) * d1h * d1h) continue;
-                    const float gx = (qx + 1.0f) * 0.5f * Wf - 0.5f, gy = (1.0f - qy) * 0.5f * Hf - 0.5f;
-                    const float dgx = dqx * 0.5f * Wf + 1e-4f + 1e-6f * fabsf(gx);
-                    const float dgy = dqy * 0.5f * Hf + 1e-4f + 1e-6f * fabsf(gy);
-                    if (dgx > 2.0f || dgy > 2.0f) {
-                        exact = true;
-                    } else {
-                        bxlo = gx - dgx;
-                        bxhi = gx + dgx;
-                        bylo = gy - dgy;
-                        byhi = gy + dgy;
-                    }
-                }
                 int cxlo, cxhi, cylo, cyhi;
-                if (exact) {
+                double dlo;
+                const int st = mark_f32(fix32[f], wx, wy, wz, W, H, cxlo, cxhi, cylo, cyhi, dlo);
+                if (st == GM_F32_REJECT) continue;
+                if (st == GM_F32_EXACT) {
                     // the exact float64 test of k_samples, for this lane only
                     const GmFixExact& F = fixes[f];
                     const double X = px[i], Y = py[i], Z = pz[i];
@@ -221,11 +232,6 @@ __global__ void KM_BOUNDS k_mark(const float* __restrict__ pxf, const float* __r
                     long long rx = x86_i64(rint(gxe)), ry = x86_i64(rint(gye));
                     cxlo = cxhi = (int)max(min(rx, (long long)W - 1), 0LL);
                     cylo = cyhi = (int)max(min(ry, (long long)H - 1), 0LL);
-                } else {
-                    cxlo = (int)fminf(fmaxf(rintf(bxlo), 0.0f), (float)(W - 1));
-                    cxhi = (int)fminf(fmaxf(rintf(bxhi), 0.0f), (float)(W - 1));
-                    cylo = (int)fminf(fmaxf(rintf(bylo), 0.0f), (float)(H - 1));
-                    cyhi = (int)fminf(fmaxf(rintf(byhi), 0.0f), (float)(H - 1));
                 }
                 const int bx0 = max(cxlo - 1, 0), bx1 = min(cxhi + 1, W - 1);
                 const int by0 = max(cylo - 1, 0), by1 = min(cyhi + 1, H - 1);
@@ -265,7 +271,7 @@ __global__ void KS_BOUNDS k_samples(const double* __restrict__ px, const double*
     const double Wd = (double)W, Hd = (double)H;
     const double lo = -1.0 - GM_NDC_SLACK, hi = 1.0 + GM_NDC_SLACK;
     const int64_t n_items = n_supers * 8;
-    unsigned c_l1 = 0, c_l2 = 0, c_exact = 0, c_ndc = 0, c_cand = 0, c_vis = 0;
+    unsigned c_l1 = 0, c_l2 = 0, c_exact = 0, c_ndc = 0, c_cand = 0, c_vis = 0, c_tocc = 0;
     // persistent warps; items = chunks of the super-chunks in descending-work
     // order (k_level1 + radix sort), claimed one at a time
     for (;;) {
@@ -338,6 +344,10 @@ __global__ void KS_BOUNDS k_samples(const double* __restrict__ px, const double*
                 // kernels.py:323-329
                 double eps = eps_abs;
                 if (eps_rel * d > eps) eps = eps_rel * d;
+                if (dv.tmax && occluded_by_tiles(dv, f, bx0, bx1, by0, by1, d, eps)) {
+                    if (STATS) c_tocc++;
+                    continue;
+                }
                 if (!depth_test_iv(dv, tris + (int64_t)f * cap_seg, F.near_, F.far_, f, gx, gy, bx0, bx1, by0, by1, d,
                                    eps))
                     continue;
@@ -355,6 +365,7 @@ __global__ void KS_BOUNDS k_samples(const double* __restrict__ px, const double*
         stat_add(dv.stats, GM_STAT_NDC, c_ndc);
         stat_add(dv.stats, GM_STAT_CANDIDATES, c_cand);
         stat_add(dv.stats, GM_STAT_VISIBLE, c_vis);
+        stat_add(dv.stats, GM_STAT_TILE_OCCLUDED, c_tocc);
     }
 }
 

@@ -100,7 +100,7 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
         if (lane >= o) pref += v;
     }
     const int total = __shfl_sync(FULL, pref, 31);
-    if (total == 0) return;
+    if (total == 0) return;  // (its tmax stays stale: no depth test reads this tile)
     const int pref_ex = pref - cnt_r;
     // written iff near' <= 1/inv_w <= far' (kernels.py:123-127): certainly inside
     // [inv_far_hi, inv_near_lo], certainly outside beyond [inv_far_lo, inv_near_hi]
@@ -325,6 +325,7 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
     double* carry = EXACT ? dep : dv.carry + (int64_t)f * W * H;               // best between chunks
     int cursor = 0;
     int nsel_total = 0;
+    float tmax = -CUDART_INF_F;  // largest finite upper depth bound this lane stored
     // final value of texel `at`.  EXACT: the float64 depth kernels.rasterize leaves
     // there (+ the writer's order key with attributes).  Otherwise: rigorous float32
     // bounds [lo, hi] of that depth and the writing triangle's segment index, from
@@ -364,6 +365,7 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
         }
         dep2[at] = o;
         win[at] = w;
+        if (o.y < CUDART_INF_F) tmax = fmaxf(tmax, o.y);
     };
     auto store = [&](int row, int colo, bool fast, float2 fb, double best, int bkey, int bwin) {
         store_at((int64_t)(yb + row) * W + xb + colo, fast, fb, best, bkey, bwin);
@@ -566,6 +568,11 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
             first = false;
             __syncwarp();
         } while (cursor < n);
+    }
+    if (!EXACT && dv.tmax) {
+        // depths are > 0: the float bit patterns order like ints (-inf < every depth)
+        const int m = __reduce_max_sync(FULL, __float_as_int(tmax));
+        if (lane == 0) dv.tmax[item] = __int_as_float(m);
     }
     if (STATS) {
         const bool l0 = lane == 0;

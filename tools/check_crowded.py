@@ -19,7 +19,7 @@ for filt in (False, True):
     sm = gm.build_sampled_meshes(scene, cfg.k)
     plan = gm.density.get_plan(scene, sm, cfg)
     plan.accumulate(fx, cfg, flags=_native.GM_FLAG_STATS)
-    st = (ctypes.c_uint64 * 16)()
+    st = (ctypes.c_uint64 * len(_native.STAT_NAMES))()
     plan._lib.gm_plan_stats(plan._h, st)
     d = dict(zip(_native.STAT_NAMES, [int(x) for x in st]))
     print("filtering", filt, "tiles", d["tx_tiles"], "crowded", d["tx_crowded"])
