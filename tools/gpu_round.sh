@@ -18,5 +18,5 @@ timeout 900 python bench.py --config c4 --steps 1 --warmup 3 --no-cpu > gpurun_o
 grep '^{' gpurun_out/bench_c4.log >> gpurun_out/configs.jsonl
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 4000 --csv --log-file gpurun_out/launches.csv python bench.py --fixations 10240 --steps 1 --warmup 2 --no-cpu --no-e2e --no-stats > gpurun_out/ncu_launches.log 2>&1
 echo "rc=$?" >> gpurun_out/ncu_launches.log
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_tri_setup|k_samples|k_texels|k_coarse|k_level1|k_mark' -s 80 -c 8 -o gpurun_out/prof_r1 -f python bench.py --fixations 4096 --steps 1 --warmup 3 --no-cpu --no-e2e --no-stats > gpurun_out/ncu_full.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_tri_setup|k_samples|k_texels|k_coarse|k_level1|k_mark' -s 80 -c 8 -o gpurun_out/prof_r1b -f python bench.py --fixations 4096 --steps 1 --warmup 3 --no-cpu --no-e2e --no-stats > gpurun_out/ncu_full.log 2>&1
 echo "rc=$?" >> gpurun_out/ncu_full.log
