@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-fixations", type=int, default=0)
     ap.add_argument("--no-stats", action="store_true", help="skip the instrumented roofline pass (profiling runs)")
+    ap.add_argument("--collective", choices=["auto", "p2p", "nccl"], default="auto",
+                    help="N > 1: fused peer reduce kernel (p2p; auto falls back to NCCL if peers cannot be mapped)")
     return ap.parse_args()
 
 
@@ -211,11 +213,6 @@ def run_reference(args, rank, world):
     }), flush=True)
 
 
-class _CudaArray:
-    def __init__(self, ptr, n):
-        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (ptr, False), "version": 3}
-
-
 def run_ours(args, rank, world):
     import paper_2601_07571_b200 as gm
     from paper_2601_07571_b200 import _native
@@ -246,11 +243,9 @@ def run_ours(args, rank, world):
     bad = np.zeros(1, np.int64)
     _native.check(lib.gm_plan_prepare(plan._h, _native.dptr(fx), F, ctypes.byref(ccfg), _native.iptr(bad)))
 
-    reduce_t = None
+    coll_used = None
     if world > 1:
-        import torch
-
-        vals_t = torch.as_tensor(_CudaArray(plan.values_device_ptr(), N), device=f"cuda:{device}")
+        from paper_2601_07571_b200.sharding import reduce_peers
 
     def one_step(timed_stats=None):
         tm = _native.GmTimings()
@@ -258,16 +253,12 @@ def run_ours(args, rank, world):
         _native.check(lib.gm_plan_run(plan._h, 1, 0, ctypes.byref(tm), ctypes.byref(ms)), "gm_plan_run")
         extra = 0.0
         if world > 1:
-            import torch
-
-            ev0 = torch.cuda.Event(enable_timing=True)
-            ev1 = torch.cuda.Event(enable_timing=True)
-            ev0.record()
-            dist.all_reduce(vals_t)
-            ev1.record()
-            torch.cuda.synchronize()
-            extra = ev0.elapsed_time(ev1)
-        gmax = plan.global_max()
+            # the ranks' partial maps -> the sum on every rank + global max (device ms of
+            # this rank's fused peer-reduce kernel, or of NCCL's all-reduce)
+            nonlocal coll_used
+            gmax, coll_used, extra = reduce_peers(plan, None, args.collective)
+        else:
+            gmax = plan.global_max()
         return ms.value + extra, tm, gmax
 
     for _ in range(args.warmup):
@@ -310,7 +301,7 @@ def run_ours(args, rank, world):
                 [workload(args.config, args.fixations, r)[2] for r in range(world)])
 
             def e2e_call():
-                return generate_sharded(scene, sampled, full, cfg, device=device)
+                return generate_sharded(scene, sampled, full, cfg, device=device, collective=args.collective)
         else:
             def e2e_call():
                 return gm.generate(scene, sampled, fx, cfg, device=device)
@@ -332,7 +323,7 @@ def run_ours(args, rank, world):
         e2e = {"value": N * total_F / e_t, "unit": UNIT, "h2d_bytes_per_step": int(F * (208 + 80)),
                "d2h_bytes_per_step": int(N * 8), "ms_per_step": e_t * 1e3,
                "path": "paper_2601_07571_b200.generate (fixation table in host memory -> values dict)"
-               if world == 1 else "paper_2601_07571_b200.sharding.generate_sharded (NCCL all-reduce)",
+               if world == 1 else "paper_2601_07571_b200.sharding.generate_sharded (partial maps + peer reduce)",
                "timing": "host wall clock around the API call"}
 
     # ---- algorithmic work of this step (one instrumented, untimed pass) ----
@@ -425,7 +416,8 @@ def run_ours(args, rank, world):
             "config": {"workload": desc, "samples": int(N), "triangles": int(plan._lib.gm_plan_num_triangles(plan._h)),
                        "fixations_per_gpu": int(F), "fixations_total": int(total_F),
                        "zbuffer": cfg.zbuffer_resolution, "filtering": filtering,
-                       "parallelism": f"fixation-sharded x{world}, NCCL sum all-reduce" if world > 1 else "single GPU",
+                       "parallelism": (f"fixation-sharded x{world}, " + ("fused peer reduce (CUDA IPC over NVLink)"
+                                       if coll_used == "p2p" else "NCCL sum all-reduce")) if world > 1 else "single GPU",
                        "l2": "flushed (512 MiB write) before every timed step",
                        "timing": "CUDA events on the plan stream around each full generation (+ all-reduce)"},
             "e2e": e2e, "roofline": roof, "roofline_step_fp32": roof_step, "cpu_baseline": cpu, "clocks": clk.summary(), "gpu_launches": launches,

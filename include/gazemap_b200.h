@@ -165,6 +165,20 @@ int gm_plan_read(gm_plan* plan, double* raw, double* normalized, double gmax);
 int gm_plan_write(gm_plan* plan, const double* raw);
 int gm_plan_sync(gm_plan* plan);
 
+/* ---- multi-GPU: fixation-sharded partial maps, fused peer reduce (§8e) ---
+ * Replaces the all-reduce + global max of the sharded generate
+ * (density.py:223-226 is a sum over fixations; the max of density.py:192 is
+ * taken on the sum).  One process per GPU: every rank exports the IPC handle
+ * of its accumulator (64 bytes), the host exchanges them (torch.distributed),
+ * each rank opens its peers' maps; after a host barrier (all partial maps
+ * complete) gm_plan_reduce_peers sums slice `rank` over the ranks in rank
+ * order through NVLink peer loads, stores the sum into every rank's map and
+ * returns the slice max; after a second barrier every rank holds the full sum
+ * and the global max is the max of the slice maxima. */
+int gm_plan_ipc_handle(gm_plan* plan, void* handle64);
+int gm_plan_open_peers(gm_plan* plan, int rank, int world, const void* handles64);
+int gm_plan_reduce_peers(gm_plan* plan, double* slice_max, float* device_ms);
+
 /* ---- kernel-seam ports (parity instruments) ----------------------------- */
 
 /* kernels.rasterize (kernels.py:140-192) via raster.rasterize_triangles

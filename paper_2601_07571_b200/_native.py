@@ -85,6 +85,9 @@ SIGNATURES = {
     "gm_plan_read": (ctypes.c_int, [_VP, _D, _D, ctypes.c_double]),
     "gm_plan_write": (ctypes.c_int, [_VP, _D]),
     "gm_plan_sync": (ctypes.c_int, [_VP]),
+    "gm_plan_ipc_handle": (ctypes.c_int, [_VP, ctypes.c_char_p]),
+    "gm_plan_open_peers": (ctypes.c_int, [_VP, ctypes.c_int, ctypes.c_int, ctypes.c_char_p]),
+    "gm_plan_reduce_peers": (ctypes.c_int, [_VP, _D, ctypes.POINTER(ctypes.c_float)]),
     "gm_plan_depth_buffer": (ctypes.c_int, [_VP, _D, ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                             _D]),
     "gm_plan_candidates": (ctypes.c_int, [_VP, _D, ctypes.c_int64, ctypes.c_double, ctypes.c_int, ctypes.c_int,

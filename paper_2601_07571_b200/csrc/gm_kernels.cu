@@ -823,6 +823,11 @@ struct gm_plan {
     int64_t cap_citems = 0, cap_cB = 0;
     unsigned long long* d_max = nullptr;
     unsigned long long* d_stats = nullptr;  // GM_STAT_N counters
+    // peer accumulators of the other ranks (CUDA IPC over NVLink), gm_plan_open_peers
+    int peer_rank = 0, peer_world = 0;
+    std::vector<cudaIpcMemHandle_t> peer_handle;
+    std::vector<double*> peer_ptr;  // [world]; own entry = d_values, others IPC-mapped
+    double** d_peer_ptr = nullptr;
     int host_threads = 8;
     // device-resident setup table (gm_plan_prepare)
     GmFixExact* d_fix_all = nullptr;
@@ -958,6 +963,9 @@ extern "C" void gm_plan_destroy(gm_plan* p) {
         cudaFreeHost(p->h_fix[r]); cudaFreeHost(p->h_cull[r]); cudaEventDestroy(p->h_ev[r]);
     }
     cudaFree(p->d_fail); cudaFree(p->d_maxcount); cudaFree(p->d_ntris);
+    for (int r = 0; r < p->peer_world; r++)
+        if (r != p->peer_rank && p->peer_ptr[r]) cudaIpcCloseMemHandle(p->peer_ptr[r]);
+    cudaFree(p->d_peer_ptr);
     cudaFree(p->d_scan_tmp); cudaFree(p->d_max); cudaFree(p->d_stats);
     cudaFree(p->d_fix_all); cudaFree(p->d_cull_all); cudaFree(p->d_flush);
     cudaFree(p->d_key);
@@ -1593,6 +1601,96 @@ extern "C" int gm_plan_max(gm_plan* p, double* gmax) {
     CK(cudaMemcpyAsync(&bits, p->d_max, sizeof(bits), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     memcpy(gmax, &bits, sizeof(double));
+    return GM_OK;
+}
+
+// ---------------------------------------------- multi-GPU: fused peer reduce
+// Rank r owns slice r of the N accumulators: it reads that slice from every
+// rank's partial map through NVLink peer loads, sums in rank order (the same
+// bits on every rank, run to run), stores the sum into every rank's map
+// through peer stores and takes the slice's max -- reduce-scatter, all-gather
+// and the first half of the global max in one pass, no staging buffer.
+// Slices are disjoint, so ranks never touch the same addresses.
+__global__ void k_reduce_peers(double* const* __restrict__ bufs, int world, int64_t a, int64_t b,
+                               unsigned long long* __restrict__ out) {
+    double m = 0.0;
+    for (int64_t i = a + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < b; i += (int64_t)gridDim.x * blockDim.x) {
+        double s = bufs[0][i];
+        for (int r = 1; r < world; r++) s += bufs[r][i];
+        for (int r = 0; r < world; r++) bufs[r][i] = s;
+        m = fmax(m, s);
+    }
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0 && m > 0.0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+}
+
+extern "C" int gm_plan_ipc_handle(gm_plan* p, void* out) {
+    if (!p || !out) return set_err(GM_ERR_ARG, "null argument");
+    if (!p->d_values) return set_err(GM_ERR_ARG, "plan has no scene");
+    CK(cudaSetDevice(p->device));
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, p->d_values));
+    memcpy(out, &h, sizeof(h));
+    return GM_OK;
+}
+
+extern "C" int gm_plan_open_peers(gm_plan* p, int rank, int world, const void* handles) {
+    if (!p || !handles || world < 1 || rank < 0 || rank >= world) return set_err(GM_ERR_ARG, "bad peer arguments");
+    CK(cudaSetDevice(p->device));
+    const cudaIpcMemHandle_t* hs = reinterpret_cast<const cudaIpcMemHandle_t*>(handles);
+    if (world != p->peer_world || rank != p->peer_rank) {  // new group: close every mapping
+        for (int r = 0; r < p->peer_world; r++)
+            if (r != p->peer_rank && p->peer_ptr[r]) CK(cudaIpcCloseMemHandle(p->peer_ptr[r]));
+        p->peer_handle.assign(world, cudaIpcMemHandle_t{});
+        p->peer_ptr.assign(world, nullptr);
+        p->peer_world = world;
+        p->peer_rank = rank;
+        int rc;
+        if ((rc = dev_alloc(&p->d_peer_ptr, (size_t)world))) return rc;
+    }
+    for (int r = 0; r < world; r++) {
+        if (r == rank) {
+            p->peer_ptr[r] = p->d_values;
+            continue;
+        }
+        if (p->peer_ptr[r] && !memcmp(&p->peer_handle[r], &hs[r], sizeof(cudaIpcMemHandle_t))) continue;
+        if (p->peer_ptr[r]) CK(cudaIpcCloseMemHandle(p->peer_ptr[r]));
+        p->peer_ptr[r] = nullptr;
+        void* ptr = nullptr;
+        CK(cudaIpcOpenMemHandle(&ptr, hs[r], cudaIpcMemLazyEnablePeerAccess));
+        p->peer_ptr[r] = static_cast<double*>(ptr);
+        p->peer_handle[r] = hs[r];
+    }
+    CK(cudaMemcpy(p->d_peer_ptr, p->peer_ptr.data(), sizeof(double*) * world, cudaMemcpyHostToDevice));
+    return GM_OK;
+}
+
+extern "C" int gm_plan_reduce_peers(gm_plan* p, double* slice_max, float* device_ms) {
+    if (!p || !slice_max) return set_err(GM_ERR_ARG, "null argument");
+    if (p->peer_world < 1 || !p->d_peer_ptr) return set_err(GM_ERR_ARG, "gm_plan_open_peers first");
+    CK(cudaSetDevice(p->device));
+    cudaStream_t s = p->stream;
+    const int64_t base = p->N / p->peer_world, extra = p->N % p->peer_world, r = p->peer_rank;
+    const int64_t a = r * base + std::min<int64_t>(r, extra), b = a + base + (r < extra ? 1 : 0);
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaMemsetAsync(p->d_max, 0, sizeof(unsigned long long), s));
+    CK(cudaEventRecord(e0, s));
+    if (b > a)
+        k_reduce_peers<<<std::min<int64_t>(blocks_for(b - a, 256), (int64_t)p->sms * 8), 256, 0, s>>>(
+            p->d_peer_ptr, p->peer_world, a, b, p->d_max);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(e1, s));
+    unsigned long long bits = 0;
+    CK(cudaMemcpyAsync(&bits, p->d_max, sizeof(bits), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    float ms = 0.0f;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (device_ms) *device_ms = ms;
+    memcpy(slice_max, &bits, sizeof(double));
     return GM_OK;
 }
 

@@ -274,6 +274,26 @@ class ScenePlan:
     def sync(self) -> None:
         _native.check(self._lib.gm_plan_sync(self._h), "gm_plan_sync")
 
+    # multi-GPU: fused peer reduce of the ranks' partial maps (sharding.reduce_peers)
+    def ipc_handle(self) -> bytes:
+        buf = ctypes.create_string_buffer(64)
+        _native.check(self._lib.gm_plan_ipc_handle(self._h, buf), "gm_plan_ipc_handle")
+        return buf.raw
+
+    def open_peers(self, rank: int, world: int, handles: bytes) -> None:
+        if len(handles) != 64 * world:
+            raise ValueError("one 64-byte IPC handle per rank expected")
+        _native.check(self._lib.gm_plan_open_peers(self._h, int(rank), int(world), handles), "gm_plan_open_peers")
+
+    def reduce_peers(self) -> tuple:
+        """Sum this rank's slice over the peers (rank order), store it into every
+        peer's map; returns (slice max, device ms)."""
+        mx = np.zeros(1)
+        ms = ctypes.c_float(0.0)
+        _native.check(self._lib.gm_plan_reduce_peers(self._h, _native.dptr(mx), ctypes.byref(ms)),
+                      "gm_plan_reduce_peers")
+        return float(mx[0]), float(ms.value)
+
     def split(self, flat: np.ndarray, sampled_meshes: dict) -> dict:
         """Per-object values: disjoint views of `flat` (a fresh buffer per call), no copy."""
         out = {}

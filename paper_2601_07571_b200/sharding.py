@@ -6,9 +6,15 @@ shard of the fixation log into a partial map on its own GPU, one sum
 all-reduce combines the partial maps, and the global max is taken on the
 reduced buffer (the max of per-rank maxima is not the max of the sum).
 
-Plumbing is torch.distributed: NCCL over NVLink/NVSwitch for CUDA ranks,
-gloo for the CPU tests.  The partial map stays in HBM: the plan's device
-accumulator is wrapped zero-copy as a torch tensor and reduced in place.
+The reduce of the GPU path is this package's own kernel (reduce_peers):
+every rank maps its peers' accumulators (CUDA IPC over NVLink/NVSwitch), sums
+its slice over the ranks in rank order (the same bits on every rank and every
+run), stores the sum into every peer's map and takes the slice max, so the
+reduce-scatter, all-gather and global max are one pass over HBM with no
+staging copy.  torch.distributed is the plumbing (handle exchange, barriers,
+a scalar max); NCCL's all-reduce on the zero-copy tensor view of the
+accumulator is the fallback when peer mapping fails on some rank
+(collective="nccl" forces it), gloo carries the CPU tests.
 """
 
 from __future__ import annotations
@@ -18,7 +24,7 @@ import numpy as np
 from .density import DensityMap, GenerationConfig, get_plan
 from .gaze import fixation_table
 
-__all__ = ["shard_range", "generate_sharded"]
+__all__ = ["shard_range", "generate_sharded", "reduce_peers"]
 
 
 def shard_range(n: int, rank: int, world: int) -> tuple:
@@ -36,26 +42,59 @@ class _CudaArray:
         self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (ptr, False), "version": 3}
 
 
-def _gpu_partial(scene, sampled_meshes, shard, config, device):
-    """Accumulate on this rank's GPU (pose overrides honoured); return (torch
-    tensor aliasing the plan's device values, plan)."""
+def reduce_peers(plan, group=None, collective: str = "auto") -> tuple:
+    """Sum the ranks' partial maps in place on every rank; returns (global max,
+    collective used, device ms of this rank's reduce).  Collective over `group`:
+    every rank must call it after its partial map is complete."""
     import torch
+    import torch.distributed as dist
 
-    plan = get_plan(scene, sampled_meshes, config, device)
-    plan.accumulate_log(shard, config, reset=True)
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    if collective not in ("auto", "p2p", "nccl"):
+        raise ValueError(f"unknown collective {collective!r}")
+    use_p2p = collective != "nccl"
+    if use_p2p:
+        handles = [None] * world
+        dist.all_gather_object(handles, plan.ipc_handle(), group=group)
+        ok = True
+        try:
+            plan.open_peers(rank, world, b"".join(handles))
+        except Exception:
+            if collective == "p2p":
+                raise
+            ok = False
+        flags = [None] * world
+        dist.all_gather_object(flags, ok, group=group)
+        use_p2p = all(flags)
+    if use_p2p:
+        plan.sync()
+        dist.barrier(group=group)  # every partial map is complete
+        smax, ms = plan.reduce_peers()
+        dist.barrier(group=group)  # every slice is stored in every map
+        maxima = [None] * world
+        dist.all_gather_object(maxima, smax, group=group)
+        return max(maxima), "p2p", ms
+    dev = torch.cuda.current_device()
+    vals = torch.as_tensor(_CudaArray(plan.values_device_ptr(), plan.n_samples), device=f"cuda:{dev}")
     plan.sync()
-    t = torch.as_tensor(_CudaArray(plan.values_device_ptr(), plan.n_samples), device=f"cuda:{device}")
-    return t, plan
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    dist.all_reduce(vals, op=dist.ReduceOp.SUM, group=group)
+    ev1.record()
+    torch.cuda.synchronize(dev)
+    return plan.global_max(), "nccl", ev0.elapsed_time(ev1)
 
 
 def generate_sharded(scene, sampled_meshes: dict, fixations, config: GenerationConfig, group=None,
-                     device: int | None = None, local_compute=None) -> DensityMap:
+                     device: int | None = None, local_compute=None, collective: str = "auto") -> DensityMap:
     """generate() over all ranks of `group` (torch.distributed); every rank
     returns the full reduced, un-normalized map.
 
     `local_compute(scene, sampled_meshes, table, config) -> flat values` may be
     injected (tests run the CPU oracle here under gloo); by default the shard
-    runs on this rank's GPU and the reduce happens in HBM.
+    runs on this rank's GPU and the reduce happens in HBM (reduce_peers;
+    `collective` "auto" = peer kernel, NCCL if a rank cannot map its peers).
     """
     import torch
     import torch.distributed as dist
@@ -69,11 +108,14 @@ def generate_sharded(scene, sampled_meshes: dict, fixations, config: GenerationC
     if local_compute is None:
         dev = torch.cuda.current_device() if device is None else device
         objs = shard if isinstance(fixations, np.ndarray) else list(fixations)[a:b]
-        vals, plan = _gpu_partial(scene, sampled_meshes, objs, config, dev)
+        plan = get_plan(scene, sampled_meshes, config, dev)
+        plan.accumulate_log(objs, config, reset=True)
+        plan.sync()
         if world > 1:
-            dist.all_reduce(vals, op=dist.ReduceOp.SUM, group=group)
-        torch.cuda.synchronize(dev)
-        gmax = plan.global_max() if len(table) else 0.0
+            gmax, _, _ = reduce_peers(plan, group, collective)
+        else:
+            gmax = plan.global_max()
+        gmax = gmax if len(table) else 0.0
         values = plan.split(plan.read(), sampled_meshes)
         return DensityMap(values, global_max=gmax)
     flat = np.ascontiguousarray(local_compute(scene, sampled_meshes, shard, config), dtype=np.float64)
