@@ -151,11 +151,11 @@ int gm_plan_run(gm_plan* plan, int reset, int flags, GmTimings* timings, float* 
 /* Write `bytes` of scratch on the plan's stream to evict L2 between repetitions. */
 int gm_plan_flush_l2(gm_plan* plan, int64_t bytes);
 
-/* Work counters of the last pass run with GmConfig.flags & 1: 16 x uint64 =
+/* Work counters of the last pass run with GmConfig.flags & 1: 19 x uint64 =
  * super-chunk tests, chunk tests, exact sample evaluations, NDC-filtered
  * samples, in-cone candidates, visible contributions, marked texels, exact
  * (texel, triangle) evaluations, covered pairs, depth tests decided by the
- * tile-max occlusion test, 6 k_texels counters (names: _native.STAT_NAMES). */
+ * tile-max occlusion test, 9 k_texels counters (names: _native.STAT_NAMES). */
 int gm_plan_stats(gm_plan* plan, unsigned long long* out);
 
 /* Running global max (density.py:192) of the plan's values. */

@@ -52,7 +52,8 @@ GM_FLAG_ONE_STREAM = 2
 GM_FLAG_TWO_STREAMS = 4
 STAT_NAMES = ["l1_tests", "l2_tests", "exact_evals", "ndc_candidates", "cone_candidates", "visible",
               "texels", "texel_pairs", "covered_pairs", "tile_occluded", "tx_tiles", "tx_staged", "tx_list", "tx_iter",
-              "tx_edge", "tx_crowded"]
+              "tx_edge", "tx_crowded",
+              "tx_chunked", "tx_chunked_pairs", "tx_chunked_texels"]
 
 PROGRESS_FN = ctypes.CFUNCTYPE(None, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p)
 

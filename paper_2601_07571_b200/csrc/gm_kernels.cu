@@ -513,7 +513,10 @@ enum {
     GM_STAT_TX_ITER = 13,    // warp iterations of the selection walk
     GM_STAT_TX_EDGE = 14,    // lane x triangle edge-function evaluations in the walk
     GM_STAT_TX_CROWDED = 15, // tiles deferred to the sorted crowded pass
-    GM_STAT_N = 16
+    GM_STAT_TX_CHUNKED = 16, // tiles walked chunk by chunk (> TW_CAP staged triangles, no fast path)
+    GM_STAT_TX_CHUNKED_PAIRS = 17,   // exact evaluations in those tiles
+    GM_STAT_TX_CHUNKED_TEXELS = 18,  // marked texels in those tiles
+    GM_STAT_N = 19
 };
 #define GM_FLAG_STATS 1
 #define GM_FLAG_ONE_STREAM 2   // force batches onto one stream/buffer set

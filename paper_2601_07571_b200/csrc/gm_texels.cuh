@@ -118,6 +118,7 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
     }
     const int xe = xb + TW - 1, ye = yb + TH - 1;
     unsigned long long c_pairs = 0, c_cov = 0, c_iter = 0, c_edge = 0;
+    bool chunked = false;  // STATS: the tile took the multi-chunk path
 
     // 1. triangles overlapping the tile -> S.sel (scan cursor resumes if > TW_SEL)
     int cover = 0;  // this lane's share of the selected bboxes' area inside the tile (depth complexity)
@@ -400,6 +401,7 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
                 if (valid) store(row, colo, fast, fb, best, bkey, bwin);
             }
         } else {
+            if (STATS) chunked = true;
             // many triangles without a deferral list: chunk by chunk (each staged once),
             // per-texel state kept in the depth array and the inverse-depth-bound buffer
             float* vb = dv.vbuf + (int64_t)f * W * H;
@@ -582,6 +584,9 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
         stat_add(dv.stats, GM_STAT_TX_LIST, l0 ? (unsigned long long)n : 0ull);
         stat_add(dv.stats, GM_STAT_TX_ITER, l0 ? c_iter : 0ull);
         stat_add(dv.stats, GM_STAT_PAIRS, c_pairs);
+        stat_add(dv.stats, GM_STAT_TX_CHUNKED, (l0 && chunked) ? 1ull : 0ull);
+        stat_add(dv.stats, GM_STAT_TX_CHUNKED_PAIRS, chunked ? c_pairs : 0ull);
+        stat_add(dv.stats, GM_STAT_TX_CHUNKED_TEXELS, (l0 && chunked) ? (unsigned long long)total : 0ull);
         stat_add(dv.stats, GM_STAT_COVERED, c_cov);
         stat_add(dv.stats, GM_STAT_TX_EDGE, c_edge);
     }
