@@ -493,6 +493,7 @@ struct DepthView {
                       // tile's marked texels, -inf if none (k_texels; tiles without marked
                       // texels are not written); nullptr = off
     int tiles_x, tiles_per_fix;
+    int crowd_mid;    // k_texels: lists of TW_CAP < n <= crowd_mid triangles also go to the crowded pass
 };
 
 // Work counters filled when GmConfig.flags & GM_FLAG_STATS (bench roofline).
@@ -1280,6 +1281,11 @@ static int enqueue_batch(gm_plan* p, const GmFixExact* d_fix, const GmFixCull* d
     dv.win = p->d_win;
     dv.carry = p->d_carry;
     dv.tmax = p->d_tmax;
+    // crop-frustum z-buffers (filtering): a tile overlapping more than TW_CAP triangles is
+    // a small distant object, walked faster whole (crowded pass, float32 fast path) than
+    // chunk by chunk (C2 -3%); full-frustum tiles with such lists are far more common and
+    // the persistent crowded pass is slower for them (unfiltered C2 +6%)
+    dv.crowd_mid = cfg->filtering ? CROWD_MID : 0;
     dv.tiles_x = (W + TW - 1) / TW;
     dv.tiles_per_fix = dv.tiles_x * ((H + TH - 1) / TH);
     if (ev) CK(cudaEventRecord(ev[0], s));
