@@ -15,8 +15,12 @@ struct __align__(16) TexelWarpSmem {
     float key[TW_SEL + 32];  // -inv_minw of sel[] (sort key: ascending min depth)
 };
 #define TX_DYN_SMEM (TW_WARPS * (int)sizeof(TexelWarpSmem))
+#ifndef TC_SEL
 #define TC_SEL 512   // crowded tiles: overlap list sorted per pass (longer lists: several passes)
+#endif
+#ifndef TC_RES
 #define TC_RES 64    // crowded tiles: nearest triangles staged in shared memory
+#endif
 struct __align__(16) CrowdedWarpSmem {
     TriF32 t32[TC_RES];
     int sel[TC_SEL];
