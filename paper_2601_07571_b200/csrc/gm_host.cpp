@@ -3,6 +3,7 @@
 // FMA-free kernels).
 #include <math.h>
 #include <stdint.h>
+#include <string.h>
 
 namespace {
 
@@ -64,3 +65,17 @@ int gm_depth_match(const double* depth, int64_t height, int64_t width, double fx
 }
 
 }  // extern "C"
+
+// Parallel host memcpy for gm_plan_read's staged read-back (1 MiB pieces over
+// the plan's host threads; internal to the library, not part of the ABI).
+extern "C" __attribute__((visibility("hidden"))) void gm_host_copy(void* dst, const void* src, size_t bytes,
+                                                                   int threads) {
+    const size_t grain = (size_t)1 << 20;
+    const int64_t n = (int64_t)((bytes + grain - 1) / grain);
+#pragma omp parallel for num_threads(threads > 0 ? threads : 1) schedule(static)
+    for (int64_t i = 0; i < n; i++) {
+        const size_t o = (size_t)i * grain;
+        memcpy((char*)dst + o, (const char*)src + o, bytes - o < grain ? bytes - o : grain);
+    }
+}
+

@@ -862,6 +862,8 @@ struct gm_plan {
     int cap_ring = 0;
     BatchBufs alt[GM_NSETS - 1];     // the other batch-buffer sets (and streams)
     cudaEvent_t ev_order = nullptr;  // last accumulation pass enqueued (chains k_samples across streams)
+    char* h_stage = nullptr;             // pinned read-back staging, 2 x GM_STAGE bytes (gm_plan_read)
+    cudaEvent_t stage_ev[2] = {nullptr, nullptr};
 };
 
 // Exchange the plan's batch buffers (and stream) with the alternate set.
@@ -966,6 +968,9 @@ extern "C" void gm_plan_destroy(gm_plan* p) {
     for (int r = 0; r < GM_RING; r++) {
         cudaFreeHost(p->h_fix[r]); cudaFreeHost(p->h_cull[r]); cudaEventDestroy(p->h_ev[r]);
     }
+    cudaFreeHost(p->h_stage);
+    for (int k = 0; k < 2; k++)
+        if (p->stage_ev[k]) cudaEventDestroy(p->stage_ev[k]);
     cudaFree(p->d_fail); cudaFree(p->d_maxcount); cudaFree(p->d_ntris);
     for (int r = 0; r < p->peer_world; r++)
         if (r != p->peer_rank && p->peer_ptr[r]) cudaIpcCloseMemHandle(p->peer_ptr[r]);
@@ -1704,18 +1709,56 @@ extern "C" int gm_plan_reduce_peers(gm_plan* p, double* slice_max, float* device
 }
 
 // Copy the plan's values to host (raw) and optionally values / gmax.
+// Device -> caller's (pageable) host buffer.  Large maps stream through two
+// pinned 8 MiB stages: chunk c+1 is in flight over PCIe while the host threads
+// copy chunk c into the destination (and take its first-touch page faults), so
+// the read-back runs at pinned-DMA speed instead of the driver's pageable path.
+extern "C" void gm_host_copy(void* dst, const void* src, size_t bytes, int threads);  // gm_host.cpp
+#define GM_STAGE ((size_t)8 << 20)
+static int copy_out(gm_plan* p, const double* d_src, double* dst, cudaStream_t s) {
+    const size_t bytes = sizeof(double) * (size_t)p->N;
+    if (bytes <= GM_STAGE) {
+        CK(cudaMemcpyAsync(dst, d_src, bytes, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        return GM_OK;
+    }
+    if (!p->h_stage) {
+        CK(cudaMallocHost(&p->h_stage, 2 * GM_STAGE));
+        for (int k = 0; k < 2; k++) CK(cudaEventCreateWithFlags(&p->stage_ev[k], cudaEventDisableTiming));
+    }
+    const int64_t nch = (int64_t)((bytes + GM_STAGE - 1) / GM_STAGE);
+    auto len = [&](int64_t c) { return std::min(GM_STAGE, bytes - (size_t)c * GM_STAGE); };
+    for (int64_t c = 0; c < std::min<int64_t>(nch, 2); c++) {
+        CK(cudaMemcpyAsync(p->h_stage + (c & 1) * GM_STAGE, (const char*)d_src + c * GM_STAGE, len(c),
+                           cudaMemcpyDeviceToHost, s));
+        CK(cudaEventRecord(p->stage_ev[c & 1], s));
+    }
+    for (int64_t c = 0; c < nch; c++) {
+        CK(cudaEventSynchronize(p->stage_ev[c & 1]));
+        gm_host_copy((char*)dst + c * GM_STAGE, p->h_stage + (c & 1) * GM_STAGE, len(c), p->host_threads);
+        if (c + 2 < nch) {
+            CK(cudaMemcpyAsync(p->h_stage + (c & 1) * GM_STAGE, (const char*)d_src + (c + 2) * GM_STAGE, len(c + 2),
+                               cudaMemcpyDeviceToHost, s));
+            CK(cudaEventRecord(p->stage_ev[c & 1], s));
+        }
+    }
+    return GM_OK;
+}
+
 extern "C" int gm_plan_read(gm_plan* p, double* raw, double* normalized, double gmax) {
     if (!p) return set_err(GM_ERR_ARG, "null plan");
     CK(cudaSetDevice(p->device));
     cudaStream_t s = p->stream;
     if (p->N == 0) return GM_OK;
-    if (raw) CK(cudaMemcpyAsync(raw, p->d_values, sizeof(double) * p->N, cudaMemcpyDeviceToHost, s));
+    int rc;
+    if (raw && (rc = copy_out(p, p->d_values, raw, s))) return rc;
     if (normalized) {
         double* tmp = nullptr;
         CK(cudaMallocAsync(&tmp, sizeof(double) * p->N, s));
         k_normalize<<<std::min<int64_t>(blocks_for(p->N, 256), (int64_t)p->sms * 8), 256, 0, s>>>(p->d_values, p->N, gmax, tmp);
-        CK(cudaMemcpyAsync(normalized, tmp, sizeof(double) * p->N, cudaMemcpyDeviceToHost, s));
+        rc = copy_out(p, tmp, normalized, s);
         CK(cudaFreeAsync(tmp, s));
+        if (rc) return rc;
     }
     CK(cudaStreamSynchronize(s));
     return GM_OK;
