@@ -157,3 +157,19 @@ def test_deep_shells_crowded_pass_vs_oracle():
     for oid in vals:
         np.testing.assert_array_equal(dm.values[oid] != 0, vals[oid] != 0)
         np.testing.assert_allclose(dm.values[oid], vals[oid], rtol=1e-12, atol=0.0)
+
+
+def test_room_staged_readback_roundtrip(room):
+    """gm_plan_read streams maps > 8 MiB through two pinned stages (17.5 MB
+    here: three chunks, ragged tail): a write -> read round trip returns the
+    same bits, and the normalized read equals raw / max bit-for-bit (k_normalize
+    divides, like the reference's values / global_max)."""
+    scene, k, fx, sampled, cfg, plan = room
+    assert plan.n_samples * 8 > 2 * (8 << 20)
+    rng = np.random.default_rng(7)
+    vals = rng.random(plan.n_samples) * 1e3
+    plan.write(vals)
+    back = plan.read()
+    np.testing.assert_array_equal(back.view(np.uint64), vals.view(np.uint64))
+    gmax = float(vals.max())
+    np.testing.assert_array_equal(plan.read(normalized_by=gmax).view(np.uint64), (vals / gmax).view(np.uint64))
