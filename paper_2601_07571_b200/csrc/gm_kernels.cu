@@ -494,6 +494,7 @@ struct DepthView {
                       // texels are not written); nullptr = off
     int tiles_x, tiles_per_fix;
     int crowd_mid;    // k_texels: lists of TW_CAP < n <= crowd_mid triangles also go to the crowded pass
+    int crowd_depth;  // k_texels: bbox cover (x tile area) above which a long list goes to the crowded pass
 };
 
 // Work counters filled when GmConfig.flags & GM_FLAG_STATS (bench roofline).
@@ -1257,6 +1258,7 @@ template <bool ATTRS, bool STATS, bool EXACT>
 static int launch_texels(gm_plan* p, cudaStream_t s, const TriStore& ts, DepthView dv, const CoarseBins& cb,
                          int tiles_x, int tiles_per_fix, int64_t items, const GmFixExact* fix, long long b0) {
     dv.crowd = p->d_crowd;
+    if (dv.crowd_depth <= 0) dv.crowd_depth = CROWD_DEPTH;  // raster API / renderer views
     dv.crowd_count = p->d_crowd_count;
     CK(cudaMemsetAsync(p->d_crowd_count, 0, 2 * sizeof(int), s));
     k_texels<ATTRS, STATS, false, EXACT><<<(unsigned)((items + TW_WARPS - 1) / TW_WARPS), TW_WARPS * 32, TX_DYN_SMEM, s>>>(
@@ -1291,6 +1293,7 @@ static int enqueue_batch(gm_plan* p, const GmFixExact* d_fix, const GmFixCull* d
     // chunk by chunk (C2 -3%); full-frustum tiles with such lists are far more common and
     // the persistent crowded pass is slower for them (unfiltered C2 +6%)
     dv.crowd_mid = cfg->filtering ? CROWD_MID : 0;
+    dv.crowd_depth = cfg->filtering ? CROWD_DEPTH_CROP : CROWD_DEPTH;
     dv.tiles_x = (W + TW - 1) / TW;
     dv.tiles_per_fix = dv.tiles_x * ((H + TH - 1) / TH);
     if (ev) CK(cudaEventRecord(ev[0], s));

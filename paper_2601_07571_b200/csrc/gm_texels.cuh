@@ -32,6 +32,9 @@ struct __align__(16) CrowdedWarpSmem {
 #ifndef CROWD_DEPTH
 #define CROWD_DEPTH 10  // ... and whose triangle bboxes cover the tile more than this many times
 #endif
+#ifndef CROWD_DEPTH_CROP
+#define CROWD_DEPTH_CROP 2  // the same in crop-frustum batches (C5 -1.7%; full-frustum C2 +55% at 2)
+#endif
 #ifndef CROWD_MID
 #define CROWD_MID 128  // ... and, in crop-frustum batches, tiles overlapping TW_CAP < n <= this many triangles
 #endif
@@ -382,14 +385,14 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
         int nsel = gather(cursor);
         if (STATS) nsel_total = nsel;
         // deep tiles (overlapping surfaces: the selected bboxes cover the tile more than
-        // CROWD_DEPTH times) profit from the sorted crowded pass; wide ones (many
+        // dv.crowd_depth times) profit from the sorted crowded pass; wide ones (many
         // side-by-side triangles) stay here
         // mid-size lists (TW_CAP < nsel <= CROWD_MID) go there too: the crowded pass stages
         // them whole (TC_RES) and walks them in one pass with the float32 fast path, where
         // the multi-chunk walk here must resolve every chunk's candidates exactly
         const bool mid = cursor >= n && nsel > TW_CAP && nsel <= dv.crowd_mid;
         if (dv.crowd && (mid || ((cursor < n || nsel > CROWD_MIN) &&
-                                 __reduce_add_sync(FULL, (unsigned)cover) > (unsigned)(CROWD_DEPTH * TW * TH)))) {
+                                 __reduce_add_sync(FULL, (unsigned)cover) > (unsigned)(dv.crowd_depth * TW * TH)))) {
             // more than TW_CAP triangles: k_texels<CROWDED> sorts the whole list (deferred)
             if (lane == 0) dv.crowd[atomicAdd(dv.crowd_count, 1)] = (int)item;
             if (STATS) stat_add(dv.stats, GM_STAT_TX_CROWDED, lane == 0 ? 1ull : 0ull);
