@@ -75,6 +75,9 @@ typedef void (*gm_progress_fn)(int64_t done, int64_t total, void* user);
 const char* gm_last_error(void);
 int gm_abi_version(void);
 int gm_device_count(void);
+/* Measured FMA throughput of `device` in TFLOP/s (fp64 != 0: float64, else
+ * float32): the SIMT roofline denominators bench.py reports against. */
+int gm_peak_flops(int device, int fp64, double* tflops);
 
 /* ---- stage 1: sampling -------------------------------------------------- */
 
@@ -151,12 +154,23 @@ int gm_plan_run(gm_plan* plan, int reset, int flags, GmTimings* timings, float* 
 /* Write `bytes` of scratch on the plan's stream to evict L2 between repetitions. */
 int gm_plan_flush_l2(gm_plan* plan, int64_t bytes);
 
-/* Work counters of the last pass run with GmConfig.flags & 1: 19 x uint64 =
+/* Work counters of the last pass run with GmConfig.flags & 1: 20 x uint64 =
  * super-chunk tests, chunk tests, exact sample evaluations, NDC-filtered
  * samples, in-cone candidates, visible contributions, marked texels, exact
  * (texel, triangle) evaluations, covered pairs, depth tests decided by the
- * tile-max occlusion test, 9 k_texels counters (names: _native.STAT_NAMES). */
+ * tile-max occlusion test, 9 k_texels counters, and the screen triangles'
+ * summed pixel bboxes = the pixel tests of the reference's rasterizer
+ * (kernels.py:103-137) for the same batch (names: _native.STAT_NAMES). */
 int gm_plan_stats(gm_plan* plan, unsigned long long* out);
+
+/* Self-check counters (16 x uint64, names: _native.CHECK_NAMES) accumulated by
+ * a GM_CHECK build (bound / cull / depth-test decisions re-done in exact
+ * float64 and compared); zeros in production builds.  reset != 0 zeroes them.
+ * *is_check_build = 1 for a GM_CHECK build. */
+int gm_plan_check(gm_plan* plan, unsigned long long* out, int reset, int* is_check_build);
+/* Testing hook: restart the per-fixation screen-triangle segments at `cap`
+ * entries, so the next run exercises the overflow -> grow -> resume path. */
+int gm_plan_set_segment_capacity(gm_plan* plan, int64_t cap);
 
 /* Running global max (density.py:192) of the plan's values. */
 int gm_plan_max(gm_plan* plan, double* gmax);

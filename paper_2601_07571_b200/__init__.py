@@ -11,13 +11,12 @@ from .errors import (ConfigError, GazemapError, GazeOutsideFrustumError, Invalid
                      ParseError)
 from .estimator import FixationDensityMapper
 from .fixlog import FixationLog, parse_fixation_log, parse_fixation_table
-from .io_export import (EXPORT_HEADER, ExportRecord, load_config, load_map, save_map, scene_layout_hash,
-                        write_export)
+from .io_export import EXPORT_HEADER, ExportRecord, load_map, save_map, write_export
 from .gaze import (DEFAULT_THETA, SQRT_TWO_PI, CropFrustum, EllipseParams, Fixation, GazeCone, build_crop_frustum,
                    crop_bounds, crop_projection_matrix, ellipse_intersection, fixation_setup, fixation_table,
                    frustum_from_matrix, gaussian_weight, perspective_matrix)
 from .raster import DepthBuffer, cull_triangles, depth_to_image, is_visible, rasterize_depth
-from .render import ColorMap, default_colormap, load_colormap, render_heatmap
+from .render import ColorMap, camera_view_matrix, default_colormap, render_heatmap
 from .geometry import (Mesh, SampledMesh, Scene, SceneObject, Transform, TriangleSampling, adaptive_resolution,
                        build_sampled_mesh, build_sampled_meshes, quat_to_matrix, rowcol_to_barycentric,
                        sample_count, sample_index_to_rowcol, sample_positions_local, sample_world_position,

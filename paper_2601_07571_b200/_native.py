@@ -53,7 +53,10 @@ GM_FLAG_TWO_STREAMS = 4
 STAT_NAMES = ["l1_tests", "l2_tests", "exact_evals", "ndc_candidates", "cone_candidates", "visible",
               "texels", "texel_pairs", "covered_pairs", "tile_occluded", "tx_tiles", "tx_staged", "tx_list", "tx_iter",
               "tx_edge", "tx_crowded",
-              "tx_chunked", "tx_chunked_pairs", "tx_chunked_texels"]
+              "tx_chunked", "tx_chunked_pairs", "tx_chunked_texels", "bbox_px"]
+
+CHECK_NAMES = ["tx_texels", "tx_bound_wrong", "tx_winner_wrong", "cand_pairs", "cand_l1_wrong", "cand_l3_wrong",
+               "mask_wrong", "depth_tests", "depth_wrong", "tileocc_wrong"] + [f"reserved{i}" for i in range(6)]
 
 PROGRESS_FN = ctypes.CFUNCTYPE(None, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p)
 
@@ -62,6 +65,7 @@ SIGNATURES = {
     "gm_last_error": (ctypes.c_char_p, []),
     "gm_abi_version": (ctypes.c_int, []),
     "gm_device_count": (ctypes.c_int, []),
+    "gm_peak_flops": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _D]),
     "gm_layout": (ctypes.c_int, [ctypes.c_int, _D, ctypes.c_int64, ctypes.c_double, _I64, _I64, _I64, _I64]),
     "gm_sample_positions": (ctypes.c_int, [ctypes.c_int, _D, ctypes.c_int64, _I64, _I64, ctypes.c_int64, _D, _D]),
     "gm_normalize": (ctypes.c_int, [ctypes.c_int, _D, ctypes.c_int64, ctypes.c_double, _D]),
@@ -82,6 +86,9 @@ SIGNATURES = {
                                    ctypes.POINTER(ctypes.c_float)]),
     "gm_plan_flush_l2": (ctypes.c_int, [_VP, ctypes.c_int64]),
     "gm_plan_stats": (ctypes.c_int, [_VP, ctypes.POINTER(ctypes.c_uint64)]),
+    "gm_plan_check": (ctypes.c_int, [_VP, ctypes.POINTER(ctypes.c_uint64), ctypes.c_int,
+                                     ctypes.POINTER(ctypes.c_int)]),
+    "gm_plan_set_segment_capacity": (ctypes.c_int, [_VP, ctypes.c_int64]),
     "gm_plan_max": (ctypes.c_int, [_VP, _D]),
     "gm_plan_read": (ctypes.c_int, [_VP, _D, _D, ctypes.c_double]),
     "gm_plan_write": (ctypes.c_int, [_VP, _D]),

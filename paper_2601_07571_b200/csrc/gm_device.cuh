@@ -108,10 +108,30 @@ __device__ __forceinline__ int project_triangle(const double* tw, const GmFixExa
         for (int i = 0; i < 3; i++)
             vin[v][i] = F.rot[3 * i] * wx + F.rot[3 * i + 1] * wy + F.rot[3 * i + 2] * wz + F.trans[i];
     }
+    const double nn = F.near_;
+    const double half_w = 0.5 * (double)W, half_h = 0.5 * (double)H;
+    if (vin[0][2] <= -nn && vin[1][2] <= -nn && vin[2][2] <= -nn) {
+        // no vertex behind the near plane (the common case): _clip_near returns the
+        // triangle unchanged and the fan has one triangle -- the general path below
+        // computes exactly this, without the dynamically indexed polygon in local memory
+        double sx[3], sy[3], iw[3];
+#pragma unroll
+        for (int m = 0; m < 3; m++) {
+            const double x = vin[m][0], y = vin[m][1], z = vin[m][2];
+            const double w = -z;  // >= near' > 0
+            const double ndc_x = (F.p00 * x + F.p02 * z) / w;
+            const double ndc_y = (F.p11 * y + F.p12 * z) / w;
+            sx[m] = (ndc_x + 1.0) * half_w;
+            sy[m] = (1.0 - ndc_y) * half_h;
+            iw[m] = 1.0 / w;
+        }
+        if (!make_screen_tri(sx, sy, iw, W, H, &out[0])) return 0;
+        out[0].minw = __double2float_rd(fmin(-vin[0][2], fmin(-vin[1][2], -vin[2][2])));
+        return 1;
+    }
     // _clip_near (kernels.py:35-59) against z = -near'
     double vout[4][3];
     int nv = 0;
-    const double nn = F.near_;
 #pragma unroll
     for (int i = 0; i < 3; i++) {
         int j = (i + 1) % 3;
@@ -130,7 +150,6 @@ __device__ __forceinline__ int project_triangle(const double* tw, const GmFixExa
         }
     }
     if (nv < 3) return 0;
-    const double half_w = 0.5 * (double)W, half_h = 0.5 * (double)H;
     int n_out = 0;
     for (int k = 0; k < nv - 2; k++) {
         double sx[3], sy[3], iw[3];

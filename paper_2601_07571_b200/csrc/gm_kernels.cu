@@ -85,6 +85,22 @@ static int set_err(int code, const std::string& msg) {
                            std::string(#x) + ": " + cudaGetErrorString(e_));                             \
     } while (0)
 
+// Frees the device temporaries of an entry point on every return path
+// (CK() returns early on the first failing call).
+struct DevScratch {
+    std::vector<void*> ptrs;
+    template <typename T>
+    cudaError_t alloc(T** p, size_t bytes) {
+        *p = nullptr;
+        cudaError_t e = cudaMalloc((void**)p, bytes);
+        if (e == cudaSuccess) ptrs.push_back((void*)*p);
+        return e;
+    }
+    ~DevScratch() {
+        for (void* q : ptrs) cudaFree(q);
+    }
+};
+
 extern "C" const char* gm_last_error(void) { return g_err.c_str(); }
 extern "C" int gm_abi_version(void) { return 1; }
 
@@ -265,10 +281,11 @@ struct __align__(16) TriF32 {
     float a[3], b[3], c[3], tol[3];  // e_i = a x + b y + c
     float A, B, C, tolw;             // inverse depth
     float inv_minw;                  // >= every inverse depth the triangle writes
-    int ox, oy;                      // frame origin = bbox corner (pixels)
-    uint32_t bx, by;                 // bbox x0 | x1 << 16, y0 | y1 << 16
+    float ox, oy;                    // frame origin = bbox corner (x0, y0), pixels
+    float wx, wy;                    // bbox extent x1 - x0 + 1, y1 - y0 + 1: pixel centre c = (px + 0.5,
+                                     // py + 0.5) is in the bbox iff 0 < c - o < w (exact in float32)
     int gidx;                        // index of the float64 record in the fixation's segment
-    int pad[2];
+    int pad;
 };  // 96 B
 
 __device__ __forceinline__ void make_tri_f32(const GmScreenTri& T, int gidx, TriF32& o) {
@@ -303,12 +320,12 @@ __device__ __forceinline__ void make_tri_f32(const GmScreenTri& T, int gidx, Tri
     o.C = (float)C;
     o.tolw = (float)(4.8e-7 * (Aab * xmax + Bab * ymax + Cab) + 1e-30);
     o.inv_minw = __double2float_ru(1.0 / (double)T.minw) * (1.0f + 1e-6f);
-    o.ox = T.x0;
-    o.oy = T.y0;
-    o.bx = (uint32_t)T.x0 | ((uint32_t)T.x1 << 16);
-    o.by = (uint32_t)T.y0 | ((uint32_t)T.y1 << 16);
+    o.ox = (float)T.x0;
+    o.oy = (float)T.y0;
+    o.wx = (float)(T.x1 - T.x0 + 1);
+    o.wy = (float)(T.y1 - T.y0 + 1);
     o.gidx = gidx;
-    o.pad[0] = o.pad[1] = 0;
+    o.pad = 0;
 }
 
 struct TriStore {
@@ -386,6 +403,39 @@ __global__ void __launch_bounds__(TS_WARPS * 32) k_tri_setup(const double* __res
     }
 }
 
+// Work counters filled when GmConfig.flags & GM_FLAG_STATS (bench roofline).
+enum {
+    GM_STAT_L1_TESTS = 0,    // super-chunk x fixation sphere tests (warp ballots x 32)
+    GM_STAT_L2_TESTS = 1,    // chunk x fixation sphere tests
+    GM_STAT_EXACT = 2,       // exact per-sample camera transform + NDC filter evaluations
+    GM_STAT_NDC = 3,         // samples passing the NDC filter (the reference's filtered set)
+    GM_STAT_CANDIDATES = 4,  // NDC and in the 4-sigma cone (depth test performed)
+    GM_STAT_VISIBLE = 5,     // depth test passed (contributions added)
+    GM_STAT_TEXELS = 6,      // marked texels evaluated
+    GM_STAT_PAIRS = 7,       // (texel, screen triangle) exact evaluations
+    GM_STAT_COVERED = 8,     // pairs where the triangle covers the texel
+    GM_STAT_TILE_OCCLUDED = 9,  // depth tests decided by the tile-max occlusion pre-test (float64 depth)
+    GM_STAT_TX_TILES = 10,   // k_texels work items with marked texels
+    GM_STAT_TX_STAGED = 11,  // triangles staged per item (sum)
+    GM_STAT_TX_LIST = 12,    // coarse-bin list entries scanned per item (sum)
+    GM_STAT_TX_ITER = 13,    // warp iterations of the selection walk
+    GM_STAT_TX_EDGE = 14,    // lane x triangle edge-function evaluations in the walk
+    GM_STAT_TX_CROWDED = 15, // tiles deferred to the sorted crowded pass
+    GM_STAT_TX_CHUNKED = 16, // tiles walked chunk by chunk (> TW_CAP staged triangles, no fast path)
+    GM_STAT_TX_CHUNKED_PAIRS = 17,   // exact evaluations in those tiles
+    GM_STAT_TX_CHUNKED_TEXELS = 18,  // marked texels in those tiles
+    GM_STAT_BBOX_PX = 19,    // sum of the screen triangles' clamped pixel bboxes: the pixel tests the
+                             // reference's _raster_tri loop performs (kernels.py:103-137)
+    GM_STAT_N = 20
+};
+#define GM_FLAG_STATS 1
+#define GM_FLAG_ONE_STREAM 2   // force batches onto one stream/buffer set
+#define GM_FLAG_TWO_STREAMS 4  // force the two-stream batch pipeline
+#ifndef GM_OVERLAP_MAX_TRIS
+#define GM_OVERLAP_MAX_TRIS 400000  // default: overlap batches for scenes up to this many occluders
+#endif
+#define GM_STAT_STRIPES 128  // counter copies (summed by gm_plan_stats): keeps the stats pass free of atomic hot spots
+
 // ------------------------------------------------------ the hot kernels
 
 // Per-batch z-buffer store: only the texels some candidate's depth_match will
@@ -411,7 +461,7 @@ struct CoarseBins {
 };
 
 __global__ void __launch_bounds__(256) k_coarse(TriStore ts, CoarseBins cb, const long long* __restrict__ fail,
-                                                long long b0) {
+                                                long long b0, unsigned long long* __restrict__ bbox_px) {
     __shared__ int s_cnt[GM_MAX_CBINS];
     __shared__ int s_off[GM_MAX_CBINS + 1];
     if (*fail <= b0) return;
@@ -421,12 +471,19 @@ __global__ void __launch_bounds__(256) k_coarse(TriStore ts, CoarseBins cb, cons
     const uint2* segb = ts.bbox + (int64_t)f * ts.cap_seg;
     for (int b = threadIdx.x; b < nbins; b += blockDim.x) s_cnt[b] = 0;
     __syncthreads();
+    unsigned long long px_sum = 0;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
         const uint2 bb = segb[i];
         const int bx0 = (bb.x & 0xffff) >> cb.shift, bx1 = (bb.x >> 16) >> cb.shift;
         const int by0 = (bb.y & 0xffff) >> cb.shift, by1 = (bb.y >> 16) >> cb.shift;
         for (int by = by0; by <= by1; by++)
             for (int bx = bx0; bx <= bx1; bx++) atomicAdd(&s_cnt[by * cb.ncx + bx], 1);
+        if (bbox_px)
+            px_sum += (unsigned long long)((bb.x >> 16) - (bb.x & 0xffff) + 1) * ((bb.y >> 16) - (bb.y & 0xffff) + 1);
+    }
+    if (bbox_px) {  // statistics pass only
+        for (int o = 16; o; o >>= 1) px_sum += __shfl_xor_sync(0xffffffffu, px_sum, o);
+        if ((threadIdx.x & 31) == 0 && px_sum) atomicAdd(bbox_px + (size_t)(blockIdx.x % GM_STAT_STRIPES) * GM_STAT_N + GM_STAT_BBOX_PX, px_sum);
     }
     __syncthreads();
     if (threadIdx.x < 32) {  // warp scan over <= 1024 bins
@@ -495,38 +552,30 @@ struct DepthView {
     int tiles_x, tiles_per_fix;
     int crowd_mid;    // k_texels: lists of TW_CAP < n <= crowd_mid triangles also go to the crowded pass
     int crowd_depth;  // k_texels: bbox cover (x tile area) above which a long list goes to the crowded pass
+    unsigned long long* check;  // GM_CHECK builds: violation counters (GM_CHK_*), nullptr = off
 };
 
-// Work counters filled when GmConfig.flags & GM_FLAG_STATS (bench roofline).
+// Self-check counters of a GM_CHECK build (gm_plan_check).  Each "wrong"
+// counter is a decision the production kernels took on float32 bounds or
+// conservative culls that the exact float64 reference arithmetic contradicts;
+// the others count how many decisions were checked.
 enum {
-    GM_STAT_L1_TESTS = 0,    // super-chunk x fixation sphere tests (warp ballots x 32)
-    GM_STAT_L2_TESTS = 1,    // chunk x fixation sphere tests
-    GM_STAT_EXACT = 2,       // exact per-sample camera transform + NDC filter evaluations
-    GM_STAT_NDC = 3,         // samples passing the NDC filter (the reference's filtered set)
-    GM_STAT_CANDIDATES = 4,  // NDC and in the 4-sigma cone (depth test performed)
-    GM_STAT_VISIBLE = 5,     // depth test passed (contributions added)
-    GM_STAT_TEXELS = 6,      // marked texels evaluated
-    GM_STAT_PAIRS = 7,       // (texel, screen triangle) exact evaluations
-    GM_STAT_COVERED = 8,     // pairs where the triangle covers the texel
-    GM_STAT_TILE_OCCLUDED = 9,  // depth tests decided by the tile-max occlusion pre-test (float64 depth)
-    GM_STAT_TX_TILES = 10,   // k_texels work items with marked texels
-    GM_STAT_TX_STAGED = 11,  // triangles staged per item (sum)
-    GM_STAT_TX_LIST = 12,    // coarse-bin list entries scanned per item (sum)
-    GM_STAT_TX_ITER = 13,    // warp iterations of the selection walk
-    GM_STAT_TX_EDGE = 14,    // lane x triangle edge-function evaluations in the walk
-    GM_STAT_TX_CROWDED = 15, // tiles deferred to the sorted crowded pass
-    GM_STAT_TX_CHUNKED = 16, // tiles walked chunk by chunk (> TW_CAP staged triangles, no fast path)
-    GM_STAT_TX_CHUNKED_PAIRS = 17,   // exact evaluations in those tiles
-    GM_STAT_TX_CHUNKED_TEXELS = 18,  // marked texels in those tiles
-    GM_STAT_N = 19
+    GM_CHK_TX_TEXELS = 0,        // texels checked (k_texels stores)
+    GM_CHK_TX_BOUND_WRONG = 1,   // fast-path [lo, hi] does not contain the exact depth of the writer
+    GM_CHK_TX_WINNER_WRONG = 2,  // stored depth / writer's depth != brute-force min over the tile's coarse list
+    GM_CHK_CAND_PAIRS = 3,       // exact (sample, fixation) candidates checked (all pairs of the batch)
+    GM_CHK_CAND_L1_WRONG = 4,    // exact candidate whose super-chunk level-1 ballot misses the fixation
+    GM_CHK_CAND_L3_WRONG = 5,    // exact candidate missing from k_mark's per-chunk fixation word
+    GM_CHK_MASK_WRONG = 6,       // texel of an exact candidate's 3x3 depth_match block left unmarked
+    GM_CHK_DEPTH_TESTS = 7,      // depth tests checked in k_samples
+    GM_CHK_DEPTH_WRONG = 8,      // depth_test_iv (bounds) != the reference test on exact texel depths
+    GM_CHK_TILEOCC_WRONG = 9,    // tile-max occlusion said "occluded" but the exact test passes
+    GM_CHK_N = 16
 };
-#define GM_FLAG_STATS 1
-#define GM_FLAG_ONE_STREAM 2   // force batches onto one stream/buffer set
-#define GM_FLAG_TWO_STREAMS 4  // force the two-stream batch pipeline
-#ifndef GM_OVERLAP_MAX_TRIS
-#define GM_OVERLAP_MAX_TRIS 400000  // default: overlap batches for scenes up to this many occluders
-#endif
-#define GM_STAT_STRIPES 128  // counter copies (summed by gm_plan_stats): keeps the stats pass free of atomic hot spots
+__device__ __forceinline__ void chk_add(unsigned long long* c, int idx, unsigned long long v) {
+    if (v) atomicAdd(c + idx, v);
+}
+
 
 // Warp-aggregated add of a per-lane count to stripe (block % GM_STAT_STRIPES)
 // of counter idx.  Every lane of the warp must call it.
@@ -812,6 +861,7 @@ struct gm_plan {
     uint2* d_bbox = nullptr;
     int* d_count = nullptr;
     int64_t cap_seg = 0, cap_seg_B = 0;
+    int64_t seg_init = 16384;  // first per-fixation screen-triangle capacity (gm_plan_set_segment_capacity)
     long long* d_fail = nullptr;
     int* d_maxcount = nullptr;
     unsigned long long* d_ntris = nullptr;
@@ -828,6 +878,7 @@ struct gm_plan {
     int64_t cap_citems = 0, cap_cB = 0;
     unsigned long long* d_max = nullptr;
     unsigned long long* d_stats = nullptr;  // GM_STAT_N counters
+    unsigned long long* d_check = nullptr;  // GM_CHK_N self-check counters (GM_CHECK builds)
     // peer accumulators of the other ranks (CUDA IPC over NVLink), gm_plan_open_peers
     int peer_rank = 0, peer_world = 0;
     std::vector<cudaIpcMemHandle_t> peer_handle;
@@ -903,6 +954,9 @@ static void plan_free_scene(gm_plan* p) {
     p->tstart.clear(); p->nsamp.clear(); p->include.clear();
 }
 
+extern "C" void gm_plan_destroy(gm_plan* p);
+static int plan_init(gm_plan* p);
+
 extern "C" int gm_plan_create(int device, gm_plan** out) {
     if (!out) return set_err(GM_ERR_ARG, "null out");
     int rc = use_device(device);
@@ -915,6 +969,17 @@ extern "C" int gm_plan_create(int device, gm_plan** out) {
         return set_err(GM_ERR_CUDA, cudaGetErrorString(e));
     }
     cudaDeviceGetAttribute(&p->sms, cudaDevAttrMultiProcessorCount, device);
+    rc = plan_init(p);
+    if (rc) {
+        gm_plan_destroy(p);  // frees whatever plan_init allocated
+        return rc;
+    }
+    *out = p;
+    return GM_OK;
+}
+
+// Kernel attributes and the plan's fixed device buffers (gm_plan_create).
+static int plan_init(gm_plan* p) {
     CK(cudaFuncSetAttribute(k_texels<false, false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
     CK(cudaFuncSetAttribute(k_texels<false, false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_DYN_SMEM));
     CK(cudaFuncSetAttribute(k_texels<false, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
@@ -934,6 +999,8 @@ extern "C" int gm_plan_create(int device, gm_plan** out) {
     CK(cudaMalloc(&p->d_max, sizeof(unsigned long long)));
     CK(cudaMalloc(&p->d_stats, GM_STAT_STRIPES * GM_STAT_N * sizeof(unsigned long long)));
     CK(cudaMemset(p->d_stats, 0, GM_STAT_STRIPES * GM_STAT_N * sizeof(unsigned long long)));
+    CK(cudaMalloc(&p->d_check, GM_CHK_N * sizeof(unsigned long long)));
+    CK(cudaMemset(p->d_check, 0, GM_CHK_N * sizeof(unsigned long long)));
     CK(cudaMalloc(&p->d_fail, sizeof(long long)));
     CK(cudaMalloc(&p->d_maxcount, sizeof(int)));
     CK(cudaMalloc(&p->d_ntris, sizeof(unsigned long long)));
@@ -942,7 +1009,6 @@ extern "C" int gm_plan_create(int device, gm_plan** out) {
     for (int r = 0; r < GM_RING; r++) CK(cudaEventCreateWithFlags(&p->h_ev[r], cudaEventDisableTiming));
     unsigned hc = std::thread::hardware_concurrency();
     p->host_threads = hc > 0 ? (int)hc : 8;
-    *out = p;
     return GM_OK;
 }
 
@@ -976,7 +1042,7 @@ extern "C" void gm_plan_destroy(gm_plan* p) {
     for (int r = 0; r < p->peer_world; r++)
         if (r != p->peer_rank && p->peer_ptr[r]) cudaIpcCloseMemHandle(p->peer_ptr[r]);
     cudaFree(p->d_peer_ptr);
-    cudaFree(p->d_scan_tmp); cudaFree(p->d_max); cudaFree(p->d_stats);
+    cudaFree(p->d_scan_tmp); cudaFree(p->d_max); cudaFree(p->d_stats); cudaFree(p->d_check);
     cudaFree(p->d_fix_all); cudaFree(p->d_cull_all); cudaFree(p->d_flush);
     cudaFree(p->d_key);
     if (p->ev_order) cudaEventDestroy(p->ev_order);
@@ -1261,10 +1327,12 @@ static int launch_texels(gm_plan* p, cudaStream_t s, const TriStore& ts, DepthVi
     if (dv.crowd_depth <= 0) dv.crowd_depth = CROWD_DEPTH;  // raster API / renderer views
     dv.crowd_count = p->d_crowd_count;
     CK(cudaMemsetAsync(p->d_crowd_count, 0, 2 * sizeof(int), s));
-    k_texels<ATTRS, STATS, false, EXACT><<<(unsigned)((items + TW_WARPS - 1) / TW_WARPS), TW_WARPS * 32, TX_DYN_SMEM, s>>>(
-        ts, dv, cb, tiles_x, tiles_per_fix, items, fix, b0);
-    k_texels<ATTRS, STATS, true, EXACT><<<p->sms * (20 / TC_WARPS), TC_WARPS * 32, TC_DYN_SMEM, s>>>(ts, dv, cb, tiles_x, tiles_per_fix,
-                                                                              items, fix, b0);
+    const int tiles_y = tiles_per_fix / tiles_x;
+    const dim3 grid((unsigned)tiles_x, (unsigned)((tiles_y + TW_WARPS - 1) / TW_WARPS), (unsigned)(items / tiles_per_fix));
+    k_texels<ATTRS, STATS, false, EXACT><<<grid, TW_WARPS * 32, TX_DYN_SMEM, s>>>(ts, dv, cb, tiles_x, tiles_per_fix,
+                                                                              tiles_y, fix, b0);
+    k_texels<ATTRS, STATS, true, EXACT><<<p->sms * (20 / TC_WARPS), TC_WARPS * 32, TC_DYN_SMEM, s>>>(
+        ts, dv, cb, tiles_x, tiles_per_fix, tiles_y, fix, b0);
     CK(cudaGetLastError());
     return GM_OK;
 }
@@ -1285,6 +1353,9 @@ static int enqueue_batch(gm_plan* p, const GmFixExact* d_fix, const GmFixCull* d
     TriStore ts{p->d_tris, p->d_t32, p->d_bbox, p->d_count, p->cap_seg, p->d_fail, p->d_maxcount, p->d_ntris};
     DepthView dv{p->d_depth, p->d_mask, W, H, wwords, (cfg->flags & GM_FLAG_STATS) ? p->d_stats : nullptr,
                  p->d_vbuf};
+#ifdef GM_CHECK
+    dv.check = p->d_check;
+#endif
     dv.win = p->d_win;
     dv.carry = p->d_carry;
     dv.tmax = p->d_tmax;
@@ -1321,10 +1392,14 @@ static int enqueue_batch(gm_plan* p, const GmFixExact* d_fix, const GmFixCull* d
         k_mark<<<grid_m, 256, 0, s>>>(p->d_pxf, p->d_pyf, p->d_pzf, p->d_px, p->d_py, p->d_pz, p->d_chunk, p->d_lvl1,
                                     p->d_lorder2, p->d_work, p->N, p->n_chunks, p->n_supers, d_fix, p->d_fix32,
                                     d_cull, nb, dv, inv_sigma, p->d_cbits, p->d_fail, b0);
+#ifdef GM_CHECK
+        k_check_candidates<<<blocks_for(p->N, 128), 128, 0, s>>>(p->d_px, p->d_py, p->d_pz, p->N, d_fix, nb, dv,
+                                                                 inv_sigma, p->d_cbits, p->d_lvl1, p->d_fail, b0);
+#endif
         if (ev) CK(cudaEventRecord(ev[2], s));
         const int64_t items = (int64_t)nb * tiles_x * tiles_y;
         CoarseBins cbins = coarse_bins(p, W, H);
-        k_coarse<<<nb, 256, 0, s>>>(ts, cbins, p->d_fail, b0);
+        k_coarse<<<nb, 256, 0, s>>>(ts, cbins, p->d_fail, b0, dv.stats);
         int trc = dv.stats
                       ? launch_texels<false, true, false>(p, s, ts, dv, cbins, tiles_x, tiles_x * tiles_y, items, d_fix, b0)
                       : launch_texels<false, false, false>(p, s, ts, dv, cbins, tiles_x, tiles_x * tiles_y, items, d_fix, b0);
@@ -1376,7 +1451,7 @@ static int run_batches(gm_plan* p, const double* fx, int64_t F, const GmConfig* 
     // batches only thrash L2 (C5: +14%), so they run on one stream
     const bool two = (cfg->flags & GM_FLAG_TWO_STREAMS) ||
                      (!(cfg->flags & GM_FLAG_ONE_STREAM) && p->T <= GM_OVERLAP_MAX_TRIS);
-    int rc = ensure_batch(p, B, W, H, std::max<int64_t>(p->cap_seg, 16384), two);
+    int rc = ensure_batch(p, B, W, H, std::max<int64_t>(p->cap_seg, p->seg_init), two);
     if (rc) return rc;
     cudaStream_t s = p->stream;          // primary stream (even batches)
 
@@ -1798,25 +1873,25 @@ extern "C" int gm_layout(int device, const double* tri_local, int64_t T, double 
     }
     int rc = use_device(device);
     if (rc) return rc;
+    DevScratch scratch;
     double* d_tri = nullptr;
     int64_t *d_res = nullptr, *d_cnt = nullptr, *d_off = nullptr;
     void* tmp = nullptr;
     size_t tb = 0;
-    CK(cudaMalloc(&d_tri, sizeof(double) * 9 * T));
-    CK(cudaMalloc(&d_res, sizeof(int64_t) * T));
-    CK(cudaMalloc(&d_cnt, sizeof(int64_t) * (T + 1)));
-    CK(cudaMalloc(&d_off, sizeof(int64_t) * (T + 1)));
+    CK(scratch.alloc(&d_tri, sizeof(double) * 9 * T));
+    CK(scratch.alloc(&d_res, sizeof(int64_t) * T));
+    CK(scratch.alloc(&d_cnt, sizeof(int64_t) * (T + 1)));
+    CK(scratch.alloc(&d_off, sizeof(int64_t) * (T + 1)));
     CK(cudaMemcpy(d_tri, tri_local, sizeof(double) * 9 * T, cudaMemcpyHostToDevice));
     k_layout<<<blocks_for(T, 256), 256>>>(d_tri, T, 8.0 * k, nullptr, d_res, d_cnt);
     CK(cudaMemset(d_cnt + T, 0, sizeof(int64_t)));
     cub::DeviceScan::ExclusiveSum(nullptr, tb, d_cnt, d_off, T + 1);
-    CK(cudaMalloc(&tmp, tb));
+    CK(scratch.alloc(&tmp, tb));
     CK(cub::DeviceScan::ExclusiveSum(tmp, tb, d_cnt, d_off, T + 1));
     if (res) CK(cudaMemcpy(res, d_res, sizeof(int64_t) * T, cudaMemcpyDeviceToHost));
     if (counts) CK(cudaMemcpy(counts, d_cnt, sizeof(int64_t) * T, cudaMemcpyDeviceToHost));
     if (offsets) CK(cudaMemcpy(offsets, d_off, sizeof(int64_t) * T, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(total, d_off + T, sizeof(int64_t), cudaMemcpyDeviceToHost));
-    cudaFree(d_tri); cudaFree(d_res); cudaFree(d_cnt); cudaFree(d_off); cudaFree(tmp);
     CK(cudaGetLastError());
     return GM_OK;
 }
@@ -1829,26 +1904,26 @@ extern "C" int gm_sample_positions(int device, const double* tri_local, int64_t 
     if (N == 0 || T == 0) return GM_OK;
     int rc = use_device(device);
     if (rc) return rc;
+    DevScratch scratch;
     double *d_tri = nullptr, *d_out = nullptr, *d_M = nullptr;
     int64_t *d_res = nullptr, *d_off = nullptr;
-    CK(cudaMalloc(&d_tri, sizeof(double) * 9 * T));
-    CK(cudaMalloc(&d_res, sizeof(int64_t) * T));
-    CK(cudaMalloc(&d_off, sizeof(int64_t) * T));
-    CK(cudaMalloc(&d_out, sizeof(double) * 3 * N));
+    CK(scratch.alloc(&d_tri, sizeof(double) * 9 * T));
+    CK(scratch.alloc(&d_res, sizeof(int64_t) * T));
+    CK(scratch.alloc(&d_off, sizeof(int64_t) * T));
+    CK(scratch.alloc(&d_out, sizeof(double) * 3 * N));
     CK(cudaMemcpy(d_tri, tri_local, sizeof(double) * 9 * T, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(d_res, res, sizeof(int64_t) * T, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(d_off, offsets, sizeof(int64_t) * T, cudaMemcpyHostToDevice));
     if (xform) {
         double Mt[12];
         xform_matrix(xform, Mt, Mt + 9);
-        CK(cudaMalloc(&d_M, sizeof(double) * 12));
+        CK(scratch.alloc(&d_M, sizeof(double) * 12));
         CK(cudaMemcpy(d_M, Mt, sizeof(double) * 12, cudaMemcpyHostToDevice));
     }
     k_positions<<<blocks_for(N, 256), 256>>>(d_tri, T, d_res, d_off, N, d_M, d_M ? d_M + 9 : nullptr, d_out,
                                             nullptr, nullptr, nullptr);
     CK(cudaGetLastError());
     CK(cudaMemcpy(out, d_out, sizeof(double) * 3 * N, cudaMemcpyDeviceToHost));
-    cudaFree(d_tri); cudaFree(d_res); cudaFree(d_off); cudaFree(d_out); cudaFree(d_M);
     return GM_OK;
 }
 
@@ -1858,14 +1933,14 @@ extern "C" int gm_normalize(int device, const double* values, int64_t n, double 
     if (n == 0) return GM_OK;
     int rc = use_device(device);
     if (rc) return rc;
+    DevScratch scratch;
     double *d_in = nullptr, *d_out = nullptr;
-    CK(cudaMalloc(&d_in, sizeof(double) * n));
-    CK(cudaMalloc(&d_out, sizeof(double) * n));
+    CK(scratch.alloc(&d_in, sizeof(double) * n));
+    CK(scratch.alloc(&d_out, sizeof(double) * n));
     CK(cudaMemcpy(d_in, values, sizeof(double) * n, cudaMemcpyHostToDevice));
     k_normalize<<<blocks_for(n, 256), 256>>>(d_in, n, gmax, d_out);
     CK(cudaGetLastError());
     CK(cudaMemcpy(out, d_out, sizeof(double) * n, cudaMemcpyDeviceToHost));
-    cudaFree(d_in); cudaFree(d_out);
     return GM_OK;
 }
 
@@ -1932,7 +2007,7 @@ static int raster_pass(gm_plan* p, int W, int H, bool attrs) {
     DepthView dv{p->d_depth, p->d_mask, W, H, wwords, nullptr, p->d_vbuf, attrs ? p->d_key : nullptr};
     k_mark_all<<<blocks_for((int64_t)H * wwords, 256), 256, 0, s>>>(p->d_mask, W, H, wwords);
     CoarseBins cbins = coarse_bins(p, W, H);
-    k_coarse<<<1, 256, 0, s>>>(ts, cbins, p->d_fail, 0);
+    k_coarse<<<1, 256, 0, s>>>(ts, cbins, p->d_fail, 0, nullptr);
     const int64_t items = (int64_t)tiles_x * tiles_y;
     return attrs ? launch_texels<true, false, true>(p, s, ts, dv, cbins, tiles_x, tiles_x * tiles_y, items, p->d_fix, 0)
                  : launch_texels<false, false, true>(p, s, ts, dv, cbins, tiles_x, tiles_x * tiles_y, items, p->d_fix, 0);
@@ -2025,4 +2100,100 @@ extern "C" int gm_device_count(void) {
     int n = 0;
     if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
     return n;
+}
+
+// ------------------------------------------------ measured SIMT peaks
+// Roofline denominators for bench.py: FP64 / FP32 FMA throughput of this GPU,
+// measured (MEASURED_PEAKS.json only carries HBM and tensor-core figures).
+// Every thread runs 8 independent FMA chains (latency hidden by ILP and by
+// the 8 resident 256-thread CTAs per SM); 2 flops per FMA.
+template <typename T>
+__global__ void __launch_bounds__(256) k_peak_fma(T* out, int iters, T m, T c) {
+    T a[8];
+#pragma unroll
+    for (int i = 0; i < 8; i++) a[i] = (T)(threadIdx.x + i) * (T)1e-3;
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+        for (int i = 0; i < 8; i++) a[i] = fma(a[i], m, c);
+    }
+    T s = 0;
+#pragma unroll
+    for (int i = 0; i < 8; i++) s += a[i];
+    if (s == (T)-1.2345) out[threadIdx.x] = s;  // never true; keeps the chains live
+}
+
+// FMA throughput in TFLOP/s (fp64 != 0: float64, else float32), best of 3
+// timed launches after a warm-up, CUDA events on a private stream.
+extern "C" int gm_peak_flops(int device, int fp64, double* tflops) {
+    if (!tflops) return set_err(GM_ERR_ARG, "null argument");
+    int rc = use_device(device);
+    if (rc) return rc;
+    int sms = 148;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    DevScratch scratch;
+    void* out = nullptr;
+    CK(scratch.alloc(&out, 256 * sizeof(double)));
+    cudaStream_t s;
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const int blocks = sms * 8, iters = fp64 ? 8192 : 32768;
+    float best = 1e30f;
+    for (int rep = 0; rep < 4; rep++) {
+        cudaEventRecord(e0, s);
+        if (fp64)
+            k_peak_fma<double><<<blocks, 256, 0, s>>>((double*)out, iters, 0.999999, 1e-7);
+        else
+            k_peak_fma<float><<<blocks, 256, 0, s>>>((float*)out, iters, 0.9999f, 1e-4f);
+        cudaEventRecord(e1, s);
+        cudaEventSynchronize(e1);
+        float ms = 0.0f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (rep > 0 && ms < best) best = ms;
+    }
+    cudaError_t err = cudaGetLastError();
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaStreamDestroy(s);
+    if (err != cudaSuccess) return set_err(GM_ERR_CUDA, cudaGetErrorString(err));
+    const double flops = 2.0 * 8.0 * (double)iters * (double)blocks * 256.0;
+    *tflops = flops / (best * 1e-3) / 1e12;
+    return GM_OK;
+}
+
+// Self-check counters (GM_CHK_* order, GM_CHK_N x uint64) accumulated since the
+// last reset by a GM_CHECK build of the extension; all zero in production
+// builds (nothing increments them).  is_check_build: 1 for a GM_CHECK build.
+extern "C" int gm_plan_check(gm_plan* p, unsigned long long* out, int reset, int* is_check_build) {
+    if (!p) return set_err(GM_ERR_ARG, "null plan");
+    CK(cudaSetDevice(p->device));
+    CK(cudaDeviceSynchronize());
+    if (out) CK(cudaMemcpy(out, p->d_check, GM_CHK_N * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    if (reset) CK(cudaMemset(p->d_check, 0, GM_CHK_N * sizeof(unsigned long long)));
+#ifdef GM_CHECK
+    if (is_check_build) *is_check_build = 1;
+#else
+    if (is_check_build) *is_check_build = 0;
+#endif
+    return GM_OK;
+}
+
+// Restart the per-fixation screen-triangle segments at `cap` entries (testing
+// hook for the overflow / resume path of run_batches; the segments still grow
+// on demand).  The plan's batch buffers are reallocated on the next run.
+extern "C" int gm_plan_set_segment_capacity(gm_plan* p, int64_t cap) {
+    if (!p || cap < 1) return set_err(GM_ERR_ARG, "bad segment capacity");
+    CK(cudaSetDevice(p->device));
+    CK(cudaDeviceSynchronize());
+    for (int k = 0; k < GM_NSETS; k++) {
+        if (k) swap_batch_bufs(p, k);
+        cudaFree(p->d_tris); cudaFree(p->d_t32); cudaFree(p->d_bbox);
+        p->d_tris = nullptr; p->d_t32 = nullptr; p->d_bbox = nullptr;
+        p->cap_seg = 0;
+        p->cap_seg_B = 0;
+        if (k) swap_batch_bufs(p, k);
+    }
+    p->seg_init = cap;
+    return GM_OK;
 }

@@ -253,6 +253,63 @@ __global__ void KM_BOUNDS k_mark(const float* __restrict__ pxf, const float* __r
     }
 }
 
+#ifdef GM_CHECK
+// Self-check of the sample-side culls (GM_CHECK builds only): every
+// (sample, fixation) pair of the batch through the exact float64 candidate
+// test of kernels.py:305-339; an exact candidate must be in its super-chunk's
+// level-1 ballot and in k_mark's per-chunk fixation word, and every texel of
+// its exact 3x3 depth_match block must be marked.
+__global__ void k_check_candidates(const double* __restrict__ px, const double* __restrict__ py,
+                                   const double* __restrict__ pz, int64_t N, const GmFixExact* __restrict__ fixes,
+                                   int B, DepthView dv, double inv_sigma, const uint32_t* __restrict__ cbits,
+                                   const uint32_t* __restrict__ lvl1, const long long* __restrict__ fail, long long b0) {
+    if (*fail <= b0) return;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    const int W = dv.W, H = dv.H, ngroups = (B + 31) >> 5;
+    const double lo = -1.0 - GM_NDC_SLACK, hi = 1.0 + GM_NDC_SLACK;
+    const double wx = px[i], wy = py[i], wz = pz[i];
+    const int64_t ch = i >> 5, sc = ch >> 3;
+    unsigned long long n = 0, l1w = 0, l3w = 0, mw = 0;
+    for (int f = 0; f < B; f++) {
+        const GmFixExact& F = fixes[f];
+        const double x = F.rot[0] * wx + F.rot[1] * wy + F.rot[2] * wz + F.trans[0];
+        const double y = F.rot[3] * wx + F.rot[4] * wy + F.rot[5] * wz + F.trans[1];
+        const double z = F.rot[6] * wx + F.rot[7] * wy + F.rot[8] * wz + F.trans[2];
+        const double w = -z;
+        if (w <= 0.0 || w < F.near_lo || w > F.far_hi) continue;
+        const double ndc_x = (F.p00 * x + F.p02 * z) / w, ndc_y = (F.p11 * y + F.p12 * z) / w;
+        if (ndc_x < lo || ndc_x > hi || ndc_y < lo || ndc_y > hi) continue;
+        const double d1 = x * F.gaze[0] + y * F.gaze[1] + z * F.gaze[2];
+        if (d1 <= 0.0) continue;
+        double d2sq = x * x + y * y + z * z - d1 * d1;
+        if (d2sq < 0.0) d2sq = 0.0;
+        if (d2sq * inv_sigma * inv_sigma / (d1 * d1) > 16.0) continue;
+        n++;
+        const int g = f >> 5, j = f & 31;
+        if (!((lvl1[sc * ngroups + g] >> j) & 1u)) {
+            l1w++;
+            continue;  // k_mark never looked at this pair (its word is not meaningful)
+        }
+        if (!((cbits[ch * 32 + g] >> j) & 1u)) l3w++;
+        const double gx = (ndc_x + 1.0) * 0.5 * (double)W - 0.5, gy = (1.0 - ndc_y) * 0.5 * (double)H - 0.5;
+        long long cx = x86_i64(rint(gx)), cy = x86_i64(rint(gy));
+        cx = cx < 0 ? 0 : (cx > W - 1 ? W - 1 : cx);
+        cy = cy < 0 ? 0 : (cy > H - 1 ? H - 1 : cy);
+        const uint32_t* m = dv.mask + (int64_t)f * H * dv.wwords;
+        for (long long yy = cy - 1; yy <= cy + 1; yy++)
+            for (long long xx = cx - 1; xx <= cx + 1; xx++) {
+                if (yy < 0 || yy > H - 1 || xx < 0 || xx > W - 1) continue;
+                if (!((m[yy * dv.wwords + (xx >> 5)] >> (xx & 31)) & 1u)) mw++;
+            }
+    }
+    chk_add(dv.check, GM_CHK_CAND_PAIRS, n);
+    chk_add(dv.check, GM_CHK_CAND_L1_WRONG, l1w);
+    chk_add(dv.check, GM_CHK_CAND_L3_WRONG, l3w);
+    chk_add(dv.check, GM_CHK_MASK_WRONG, mw);
+}
+#endif
+
 template <bool STATS>
 __global__ void KS_BOUNDS k_samples(const double* __restrict__ px, const double* __restrict__ py,
                                                  const double* __restrict__ pz, const float4* __restrict__ chunks,
@@ -346,11 +403,23 @@ __global__ void KS_BOUNDS k_samples(const double* __restrict__ px, const double*
                 if (eps_rel * d > eps) eps = eps_rel * d;
                 if (dv.tmax && occluded_by_tiles(dv, f, bx0, bx1, by0, by1, d, eps)) {
                     if (STATS) c_tocc++;
+#ifdef GM_CHECK
+                    chk_add(dv.check, GM_CHK_DEPTH_TESTS, 1);
+                    chk_add(dv.check, GM_CHK_TILEOCC_WRONG,
+                            depth_test_exact(dv, tris + (int64_t)f * cap_seg, F.near_, F.far_, f, gx, gy, bx0, bx1,
+                                             by0, by1, d, eps) ? 1 : 0);
+#endif
                     continue;
                 }
-                if (!depth_test_iv(dv, tris + (int64_t)f * cap_seg, F.near_, F.far_, f, gx, gy, bx0, bx1, by0, by1, d,
-                                   eps))
-                    continue;
+                const bool seen = depth_test_iv(dv, tris + (int64_t)f * cap_seg, F.near_, F.far_, f, gx, gy, bx0, bx1,
+                                                by0, by1, d, eps);
+#ifdef GM_CHECK
+                chk_add(dv.check, GM_CHK_DEPTH_TESTS, 1);
+                chk_add(dv.check, GM_CHK_DEPTH_WRONG,
+                        seen != depth_test_exact(dv, tris + (int64_t)f * cap_seg, F.near_, F.far_, f, gx, gy, bx0,
+                                                 bx1, by0, by1, d, eps) ? 1 : 0);
+#endif
+                if (!seen) continue;
                 if (STATS) c_vis++;
                 v += F.amp * exp(-0.5 * ratio_sq);  // kernels.py:340
             }

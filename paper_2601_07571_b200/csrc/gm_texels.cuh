@@ -5,6 +5,9 @@
 #pragma once
 
 #define TW_CAP 32
+#ifndef RANK_SORT_MAX
+#define RANK_SORT_MAX 16  // staged lists up to this long are ordered by rank counting, longer by bitonic sort
+#endif
 #define TW_SEL 128  // overlapping triangles remembered per tile (more: rescanned per round)
 #ifndef TW_WARPS
 #define TW_WARPS 2  // warps (independent tile items) per k_texels CTA
@@ -85,14 +88,13 @@ __device__ __forceinline__ int kth_set_bit(uint32_t w, int k) {
 // selection slices; KEY (crowded mode only): sort keys of SEL.
 template <bool ATTRS, bool STATS, bool CROWDED, bool EXACT>
 __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __restrict__ SEL, float* __restrict__ KEY,
-                                           int64_t item, const TriStore& ts, const DepthView& dv,
+                                           int f, int tx, int ty, const TriStore& ts, const DepthView& dv,
                                            const CoarseBins& cb, int tiles_x, int tiles_per_fix,
                                            const GmFixExact* __restrict__ fixes) {
     const int lane = threadIdx.x & 31;
-    const int f = (int)(item / tiles_per_fix);
-    const int tile = (int)(item - (int64_t)f * tiles_per_fix);
+    const int64_t item = (int64_t)f * tiles_per_fix + ty * tiles_x + tx;
     const int W = dv.W, H = dv.H;
-    const int xb = (tile % tiles_x) * TW, yb = (tile / tiles_x) * TH;
+    const int xb = tx * TW, yb = ty * TH;
     const unsigned FULL = 0xffffffffu;
     // marked texels: lane r < TH holds the mask word of row yb + r
     uint32_t wr = 0;
@@ -114,7 +116,8 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
     const int pref_ex = pref - cnt_r;
     // written iff near' <= 1/inv_w <= far' (kernels.py:123-127): certainly inside
     // [inv_far_hi, inv_near_lo], certainly outside beyond [inv_far_lo, inv_near_hi]
-    const float inv_near = (float)(1.0 / near_), inv_far = (float)(1.0 / far_);
+    // float32 reciprocals (<= 2 ulp from (float)(1/near')): far inside the 1e-5 margins below
+    const float inv_near = __frcp_rn(__double2float_rn(near_)), inv_far = __frcp_rn(__double2float_rn(far_));
     const float inv_near_lo = inv_near * (1.0f - 1e-5f), inv_near_hi = inv_near * (1.0f + 1e-5f);
     const float inv_far_lo = inv_far * (1.0f - 1e-5f), inv_far_hi = inv_far * (1.0f + 1e-5f);
     const GmScreenTri* seg = ts.tris + (int64_t)f * ts.cap_seg;
@@ -132,6 +135,8 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
 
     // 1. triangles overlapping the tile -> S.sel (scan cursor resumes if > TW_SEL)
     int cover = 0;  // this lane's share of the selected bboxes' area inside the tile (depth complexity)
+    // only lists longer than CROWD_MIN can be routed by their depth complexity
+    const bool want_cover = n > CROWD_MIN;
     auto gather = [&](int& cursor) {
         int cnt = 0;
         while (cursor < n && cnt < TW_SEL) {
@@ -151,7 +156,7 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
                 }
                 const int x0 = bbx.x & 0xffff, x1 = bbx.x >> 16, y0 = bbx.y & 0xffff, y1 = bbx.y >> 16;
                 sel = !(x1 < xb || x0 > xe || y1 < yb || y0 > ye);
-                if (sel) cover += (min(x1, xe) - max(x0, xb) + 1) * (min(y1, ye) - max(y0, yb) + 1);
+                if (want_cover && sel) cover += (min(x1, xe) - max(x0, xb) + 1) * (min(y1, ye) - max(y0, yb) + 1);
             }
             const unsigned bal = __ballot_sync(FULL, sel);
             if (sel) {
@@ -166,31 +171,44 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
         return cnt;  // may exceed TW_SEL by < 32 (S.sel has the room)
     };
 
-    // 2. stage SEL[c0 .. c0 + kend) (float32 forms) in ascending min-depth order
+    // 2. stage SEL[c0 .. c0 + kend) (float32 forms) in ascending min-depth order.
+    // Short lists: lane l's rank = the entries that sort before it (key, then list
+    // position), one shuffle per entry; long ones: 32-wide bitonic network.
     auto stage = [&](int c0, int kend) {
         __syncwarp();
         const int gi = lane < kend ? SEL[c0 + lane] : 0;
-        float key = lane < kend ? KEY[c0 + lane] : CUDART_INF_F;  // ascending min depth
-        int slot = lane;
+        float key = lane < kend ? KEY[c0 + lane] : CUDART_INF_F;
+        int dst, src;
+        if (kend <= RANK_SORT_MAX) {
+            int rank = 0;
+            for (int j = 0; j < kend; j++) {
+                const float kj = __shfl_sync(FULL, key, j);
+                rank += (kj < key || (kj == key && j < lane)) ? 1 : 0;
+            }
+            dst = rank;  // this lane's record goes to slot `rank`
+            src = gi;
+        } else {
+            int slot = lane;
 #pragma unroll
-        for (int size = 2; size <= 32; size <<= 1) {
+            for (int size = 2; size <= 32; size <<= 1) {
 #pragma unroll
-            for (int stride = size >> 1; stride > 0; stride >>= 1) {
-                const float ok = __shfl_xor_sync(FULL, key, stride);
-                const int os = __shfl_xor_sync(FULL, slot, stride);
-                const bool keep_min = ((lane & stride) == 0) == ((lane & size) == 0);
-                const bool less = ok < key || (ok == key && os < slot);
-                if (keep_min ? less : !less && !(ok == key && os == slot)) {
-                    key = ok;
-                    slot = os;
+                for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                    const float ok = __shfl_xor_sync(FULL, key, stride);
+                    const int os = __shfl_xor_sync(FULL, slot, stride);
+                    const bool keep_min = ((lane & stride) == 0) == ((lane & size) == 0);
+                    const bool less = ok < key || (ok == key && os < slot);
+                    if (keep_min ? less : !less && !(ok == key && os == slot)) {
+                        key = ok;
+                        slot = os;
+                    }
                 }
             }
+            dst = lane;  // lane = rank; it copies the record of sorted position `lane`
+            src = __shfl_sync(FULL, gi, slot);
         }
-        // lane = rank; it copies the record of sorted position `lane`
-        const int src = __shfl_sync(FULL, gi, slot);
         if (lane < kend) {
             const uint4* from = reinterpret_cast<const uint4*>(segf + src);
-            uint4* to = reinterpret_cast<uint4*>(&T32[lane]);
+            uint4* to = reinterpret_cast<uint4*>(&T32[dst]);
 #pragma unroll
             for (int part = 0; part < 6; part++) to[part] = from[part];
         }
@@ -238,6 +256,7 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
     auto walk = [&](int kend, int nst, bool valid, int row, int colo, float& V, double& best, int& bkey, int& bwin,
                     bool allow_fast, float2& fastb) -> bool {
         const int px = xb + colo, py = yb + row;
+        const float pxc = (float)px + 0.5f, pyc = (float)py + 0.5f;  // pixel centre
         int cs0 = -1, cs1 = -1;  // exact candidates (global record index) and their bounds
         float ch0 = 0.0f, ch1 = 0.0f;
         float cl0 = 0.0f, cl1 = 0.0f;   // their lower inverse-depth bounds
@@ -245,15 +264,17 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
         bool overflow = false;
         for (int kk = 0; kk < kend; kk++) {
             const TriF32& t = tri_at(kk, nst);
-            const float inv_minw = t.inv_minw;
+            // (inv_minw, ox, oy, wx) and (wy, gidx): both loads up front, so the bbox test
+            // below is one predicate and one branch
+            const float4 hd = *reinterpret_cast<const float4*>(&t.inv_minw);
+            const float wy = t.wy;
+            const float inv_minw = hd.x;
             if (__all_sync(FULL, !(inv_minw >= V))) break;  // nothing later can be nearer
             if (STATS) c_iter++;
-            const uint32_t tbx = t.bx, tby = t.by;
-            if (!(inv_minw >= V) || px < (int)(tbx & 0xffff) || px > (int)(tbx >> 16) || py < (int)(tby & 0xffff) ||
-                py > (int)(tby >> 16))
-                continue;
+            const float fx = pxc - hd.y, fy = pyc - hd.z;  // bbox-local centre (exact)
+            const bool in = (inv_minw >= V) & (fx > 0.0f) & (fx < hd.w) & (fy > 0.0f) & (fy < wy);
+            if (!in) continue;
             if (STATS) c_edge++;
-            const float fx = (float)(px - t.ox) + 0.5f, fy = (float)(py - t.oy) + 0.5f;  // bbox-local centre
             bool maybe = true, certain = true;
 #pragma unroll
             for (int i = 0; i < 3; i++) {
@@ -318,9 +339,8 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
         } else {  // slow path: every staged triangle whose bbox covers the texel
             for (int k = 0; k < kend; k++) {
                 const TriF32& t = tri_at(k, nst);
-                if (px < (int)(t.bx & 0xffff) || px > (int)(t.bx >> 16) || py < (int)(t.by & 0xffff) ||
-                    py > (int)(t.by >> 16))
-                    continue;
+                const float fx = pxc - t.ox, fy = pyc - t.oy;
+                if (!(fx > 0.0f) || !(fx < t.wx) || !(fy > 0.0f) || !(fy < t.wy)) continue;
                 const double d = texel_depth(seg[t.gidx], px, py, near_, far_);
                 if (STATS) c_pairs++;
                 if (STATS) c_cov += d < CUDART_INF;
@@ -341,9 +361,38 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
     // there (+ the writer's order key with attributes).  Otherwise: rigorous float32
     // bounds [lo, hi] of that depth and the writing triangle's segment index, from
     // which k_samples re-evaluates the exact depth when a test is undecided.
+#ifdef GM_CHECK
+    // self-check (GM_CHECK builds): the exact min over every screen triangle whose
+    // bbox holds the texel (the tile's coarse list, or the whole segment), against
+    // what is stored -- EXACT: the depth bits; otherwise the writer's exact depth
+    // and, on the fast path, the float32 bounds [lo, hi] around it
+    auto check_texel = [&](int64_t at, double best, int w, float2 o, bool fast) {
+        const int cx = (int)(at % W), cy = (int)(at / W);
+        double bm = CUDART_INF;
+        for (int i = 0; i < n; i++) {
+            const int idx = clist ? clist[i].x : i;
+            const GmScreenTri& T = seg[idx];
+            if (cx < T.x0 || cx > T.x1 || cy < T.y0 || cy > T.y1) continue;
+            bm = fmin(bm, texel_depth(T, cx, cy, near_, far_));
+        }
+        bool bad = false;
+        if (EXACT) {
+            bad = __double_as_longlong(best) != __double_as_longlong(bm);
+        } else {
+            const double dw = w >= 0 ? texel_depth(seg[w], cx, cy, near_, far_) : CUDART_INF;
+            bad = __double_as_longlong(dw) != __double_as_longlong(bm);
+            if (fast && !(dw >= (double)o.x && dw <= (double)o.y)) chk_add(dv.check, GM_CHK_TX_BOUND_WRONG, 1);
+        }
+        chk_add(dv.check, GM_CHK_TX_TEXELS, 1);
+        chk_add(dv.check, GM_CHK_TX_WINNER_WRONG, bad ? 1 : 0);
+    };
+#endif
     auto store_at = [&](int64_t at, bool fast, float2 fb, double best, int bkey, int bwin) {
         if (EXACT) {
             dep[at] = best;
+#ifdef GM_CHECK
+            if (!ATTRS) check_texel(at, best, -1, make_float2(0.0f, 0.0f), false);
+#endif
             if (ATTRS) dv.key[at] = best < CUDART_INF ? bkey : -1;
             return;
         }
@@ -360,14 +409,7 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
 #else
             o = make_float2(__frcp_rd(fb.y), __frcp_ru(fb.x));
 #endif
-#ifdef GM_CHECK_BOUNDS  // debug build: verify the bounds against the exact depth
-            {
-                const double ex = texel_depth(seg[w], (int)(at % W), (int)(at / W), near_, far_);
-                if (!(ex >= (double)o.x && ex <= (double)o.y))
-                    printf("BOUND VIOLATION f=%d at=%lld exact=%.17g lo=%.9g hi=%.9g fb=(%.9g,%.9g)\n", f,
-                           (long long)at, ex, o.x, o.y, fb.x, fb.y);
-            }
-#endif
+
         } else if (best < CUDART_INF) {
             o = make_float2(__double2float_rd(best), __double2float_ru(best));
         } else {
@@ -377,6 +419,9 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
         dep2[at] = o;
         win[at] = w;
         if (o.y < CUDART_INF_F) tmax = fmaxf(tmax, o.y);
+#ifdef GM_CHECK
+        check_texel(at, best, w, o, fast);
+#endif
     };
     auto store = [&](int row, int colo, bool fast, float2 fb, double best, int bkey, int bwin) {
         store_at((int64_t)(yb + row) * W + xb + colo, fast, fb, best, bkey, bwin);
@@ -606,20 +651,23 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
     }
 }
 
+// First pass: grid (tiles_x, ceil(tiles_y / TW_WARPS), fixations); warp w of a
+// CTA takes tile row blockIdx.y * TW_WARPS + w.  Crowded pass: persistent warps
+// over the deferred items.
 template <bool ATTRS, bool STATS, bool CROWDED, bool EXACT>
 __global__ void TX_BOUNDS k_texels(TriStore ts, DepthView dv, CoarseBins cb, int tiles_x,
-                                   int tiles_per_fix, int64_t n_items,
+                                   int tiles_per_fix, int tiles_y,
                                    const GmFixExact* __restrict__ fixes, long long b0) {
     extern __shared__ __align__(16) unsigned char tx_dyn[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (*ts.fail <= b0) return;
     if (!CROWDED) {
-        const int64_t item = (int64_t)blockIdx.x * TW_WARPS + warp;
-        if (item < n_items)
+        const int ty = blockIdx.y * TW_WARPS + warp;
+        if (ty < tiles_y)
             texel_item<ATTRS, STATS, false, EXACT>(reinterpret_cast<TexelWarpSmem*>(tx_dyn)[warp].t32,
                                             reinterpret_cast<TexelWarpSmem*>(tx_dyn)[warp].sel,
-                                            reinterpret_cast<TexelWarpSmem*>(tx_dyn)[warp].key, item, ts, dv,
-                                            cb, tiles_x, tiles_per_fix, fixes);
+                                            reinterpret_cast<TexelWarpSmem*>(tx_dyn)[warp].key, blockIdx.z,
+                                            blockIdx.x, ty, ts, dv, cb, tiles_x, tiles_per_fix, fixes);
         return;
     }
     // crowded tiles (deferred by the pass above): persistent warps over the list
@@ -630,7 +678,10 @@ __global__ void TX_BOUNDS k_texels(TriStore ts, DepthView dv, CoarseBins cb, int
         if (lane == 0) w = atomicAdd(dv.crowd_count + 1, 1);
         w = __shfl_sync(0xffffffffu, w, 0);
         if (w >= n_crowd) break;
-        texel_item<ATTRS, STATS, true, EXACT>(C.t32, C.sel, C.key, dv.crowd[w], ts, dv, cb, tiles_x, tiles_per_fix, fixes);
+        const int item = dv.crowd[w];
+        const int f = item / tiles_per_fix, tile = item - f * tiles_per_fix;
+        texel_item<ATTRS, STATS, true, EXACT>(C.t32, C.sel, C.key, f, tile % tiles_x, tile / tiles_x, ts, dv, cb,
+                                              tiles_x, tiles_per_fix, fixes);
     }
 }
 

@@ -15,6 +15,7 @@ import ctypes
 import os
 import math
 import time
+import weakref
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -62,9 +63,22 @@ class GenerationConfig:
 
 @dataclass
 class DensityMap:
+    """Per-object value arrays + tracked global max (reference density.py:74-91).
+
+    A map fed by accumulate_fixation may hold its newest values on the GPU
+    only (see _DeviceLink): reading `.values` brings them back first, into the
+    same arrays, so the map always looks like the reference's."""
+
     values: dict
     global_max: float = 0.0
     normalized: bool = False
+
+    def __getattribute__(self, name):
+        if name == "values":
+            link = object.__getattribute__(self, "__dict__").get("_device_link")
+            if link is not None:
+                link.expose(self)
+        return object.__getattribute__(self, name)
 
     @classmethod
     def zeros(cls, sampled_meshes: dict) -> "DensityMap":
@@ -158,6 +172,14 @@ class ScenePlan:
         if n != self.n_samples:
             raise RuntimeError(f"plan sample count {n} != layout total {self.n_samples}")
         self._keep = None
+        self._owner = None  # _DeviceLink of the DensityMap whose values the accumulator holds
+
+    def release(self) -> None:
+        """Hand the device accumulator back: the linked map (accumulate_fixation)
+        gets its values read back first if the device is ahead of it."""
+        owner, self._owner = self._owner, None
+        if owner is not None:
+            owner.pull()
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -170,9 +192,11 @@ class ScenePlan:
 
     # ----------------------------------------------------------------- ops
     def accumulate(self, fixations, config: GenerationConfig, reset: bool = True, progress=None,
-                   timers: Timings | None = None, batch: int = 0, flags: int = 0) -> None:
+                   timers: Timings | None = None, batch: int = 0, flags: int = 0, _owner_ok: bool = False) -> None:
         """Add the fixations' contributions to the device values (`flags`:
         GmConfig.flags, e.g. _native.GM_FLAG_ONE_STREAM)."""
+        if not _owner_ok:
+            self.release()
         table = fixation_table(fixations)
         F = len(table)
         cfg = _native.GmConfig(float(config.theta), float(config.epsilon_abs), float(config.epsilon_rel),
@@ -218,16 +242,19 @@ class ScenePlan:
         self._pose_key = key
 
     def accumulate_log(self, fixations, config: GenerationConfig, reset: bool = True, progress=None,
-                       timers: Timings | None = None, batch: int = 0) -> None:
+                       timers: Timings | None = None, batch: int = 0, _owner_ok: bool = False) -> None:
         """accumulate() over a log that may carry pose overrides (dynamic
         scenes, reference density.py:123-127,161-165): the log is cut into
         runs of consecutive fixations with the same effective override set;
         each run is accumulated with the scene posed for it, in log order."""
+        if not _owner_ok:
+            self.release()
         table = fixation_table(fixations)
         ovs = _override_list(fixations)
         if ovs is None:
             self.set_overrides(None)
-            self.accumulate(table, config, reset=reset, progress=progress, timers=timers, batch=batch)
+            self.accumulate(table, config, reset=reset, progress=progress, timers=timers, batch=batch,
+                            _owner_ok=True)
             return
         F = len(table)
         keys = [_pose_key(o, self._obj_index) for o in ovs]
@@ -242,11 +269,12 @@ class ScenePlan:
                 cb = None
                 if progress is not None:
                     cb = (lambda off: (lambda i, _t: progress(off + i, F)))(a)
-                self.accumulate(table[a:b], config, reset=reset and first, progress=cb, timers=timers, batch=batch)
+                self.accumulate(table[a:b], config, reset=reset and first, progress=cb, timers=timers, batch=batch,
+                                _owner_ok=True)
                 first = False
                 a = b
             if first and reset:
-                self.accumulate(table[:0], config, reset=True)
+                self.accumulate(table[:0], config, reset=True, _owner_ok=True)
         finally:
             self.set_overrides(None)
 
@@ -265,6 +293,7 @@ class ScenePlan:
         return out
 
     def write(self, values: np.ndarray) -> None:
+        self.release()
         v = np.ascontiguousarray(values, dtype=np.float64)
         _native.check(self._lib.gm_plan_write(self._h, _native.dptr(v)), "gm_plan_write")
 
@@ -397,26 +426,80 @@ def generate(scene, sampled_meshes: dict, fixations, config: GenerationConfig, w
     is accepted for API compatibility; the GPU result does not depend on it.
     """
     config.validate()
+    t0 = time.perf_counter()
     plan = get_plan(scene, sampled_meshes, config, device)
+    t1 = time.perf_counter()
     plan.accumulate_log(fixations, config, reset=True, progress=progress, timers=timers, batch=batch)
+    t2 = time.perf_counter()
     gmax = plan.global_max() if len(fixations) else 0.0
+    t3 = time.perf_counter()
     values = plan.split(plan.read(), sampled_meshes)
+    if timers is not None:  # wall-clock stages beside the device phases accumulate_log records
+        timers.add("upload", t1 - t0)      # scene -> ScenePlan (first call for this scene only)
+        timers.add("generate_wall", t2 - t1)
+        timers.add("max", t3 - t2)
+        timers.add("readback", time.perf_counter() - t3)
     return DensityMap(values, global_max=gmax, normalized=False)
+
+
+class _DeviceLink:
+    """Ties a DensityMap to the ScenePlan whose device accumulator holds its
+    values, so a loop of accumulate_fixation calls moves one scalar (the
+    running max) per call instead of the whole map both ways.
+
+    * device_ahead: the plan holds newer values than the host arrays; any read
+      of `dmap.values` copies them back into those arrays (in place) first.
+    * exposed: `dmap.values` was handed out since the last upload, so the caller
+      may have edited the arrays: the next accumulate_fixation re-uploads them.
+    The plan remembers its owner link; before the plan's accumulator is used for
+    anything else (generate, another map) the owner's values are read back."""
+
+    def __init__(self, plan: "ScenePlan", dmap: DensityMap):
+        self.plan = plan
+        self.dmap_ref = weakref.ref(dmap)
+        self.device_ahead = False
+        self.exposed = False
+
+    def pull(self, dmap: DensityMap | None = None) -> None:
+        dmap = dmap if dmap is not None else self.dmap_ref()
+        if not self.device_ahead or dmap is None:
+            self.device_ahead = False
+            return
+        self.device_ahead = False
+        flat = self.plan.read()
+        values = object.__getattribute__(dmap, "__dict__")["values"]
+        for oid, (a, b) in self.plan.slices.items():
+            values[oid][...] = flat[a:b]
+
+    def expose(self, dmap: DensityMap) -> None:
+        self.pull(dmap)
+        self.exposed = True
 
 
 def accumulate_fixation(dmap: DensityMap, scene, sampled_meshes: dict, fixation, config: GenerationConfig,
                         cache=None, timers: Timings | None = None, device: int = 0) -> DensityMap:
-    """Add one fixation to `dmap` in place (running max updated), return it."""
+    """Add one fixation to `dmap` in place (running max updated), return it.
+
+    The map's values stay resident on the GPU between calls (_DeviceLink):
+    they are uploaded when the plan does not hold them already or the caller
+    has read `dmap.values` since, and read back when `dmap.values` is next
+    read.  The running max (reference density.py:180-194) is the device max
+    over the included objects, one scalar per call."""
     plan = cache if isinstance(cache, ScenePlan) else get_plan(scene, sampled_meshes, config, device)
-    plan.write(plan.gather(dmap.values))
-    plan.accumulate_log([fixation], config, reset=False, timers=timers)
-    flat = plan.read()
-    running = dmap.global_max
-    for oid, (a, b) in plan.slices.items():
-        dmap.values[oid][...] = flat[a:b]
-        if b > a:
-            running = max(running, float(flat[a:b].max()))
-    dmap.global_max = running
+    d = object.__getattribute__(dmap, "__dict__")
+    link = d.get("_device_link")
+    if link is None or link.plan is not plan or plan._owner is not link or link.exposed:
+        if link is not None:
+            link.pull(dmap)
+        plan.release()
+        plan.write(plan.gather(d["values"]))
+        link = _DeviceLink(plan, dmap)
+        d["_device_link"] = link
+        plan._owner = link
+    plan.accumulate_log([fixation], config, reset=False, timers=timers, _owner_ok=True)
+    link.device_ahead = True
+    if plan.slices and any(b > a for a, b in plan.slices.values()):
+        dmap.global_max = max(dmap.global_max, plan.global_max())
     return dmap
 
 

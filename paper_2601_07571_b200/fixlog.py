@@ -54,6 +54,30 @@ class FixationLog(list):
     def has_overrides(self) -> bool:
         return any(f.overrides for f in self)
 
+    def _stale(self) -> None:
+        # the cached table / line numbers / override count describe the list as
+        # parsed; any in-place edit makes consumers rebuild from the Fixation objects
+        for name in ("table", "line", "n_override_groups"):
+            self.__dict__.pop(name, None)
+
+
+def _invalidating(name: str):
+    base = getattr(list, name)
+
+    def method(self, *args, **kwargs):
+        self._stale()
+        return base(self, *args, **kwargs)
+
+    method.__name__ = name
+    method.__doc__ = base.__doc__
+    return method
+
+
+for _name in ("__setitem__", "__delitem__", "__iadd__", "__imul__", "append", "extend", "insert", "pop", "remove",
+              "clear", "sort", "reverse"):
+    setattr(FixationLog, _name, _invalidating(_name))
+del _name
+
 
 def _parse_line(raw: str, path, ln: int):
     """One line of the reference loop (gaze.py:148-185): None for blank and

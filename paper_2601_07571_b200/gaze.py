@@ -18,7 +18,7 @@ import numpy as np
 from . import _native
 from .errors import GazeOutsideFrustumError, InvalidFrustumError
 
-__all__ = ["GazeCone", "Fixation", "EllipseParams", "CropFrustum", "DEFAULT_THETA", "SQRT_TWO_PI", "fixation_table",
+__all__ = ["GazeCone", "Fixation", "world_to_camera", "EllipseParams", "CropFrustum", "DEFAULT_THETA", "SQRT_TWO_PI", "fixation_table",
            "fixation_setup", "perspective_matrix", "frustum_from_matrix", "gaussian_weight", "ellipse_intersection",
            "crop_bounds", "crop_projection_matrix", "build_crop_frustum"]
 
@@ -96,18 +96,26 @@ class Fixation:
         return r
 
     def view_matrix(self) -> np.ndarray:
-        """World-to-camera 4x4 (host utility)."""
-        from .geometry import quat_to_matrix
-
-        rt = quat_to_matrix(self.camera_rotation).T
-        m = np.eye(4)
-        m[:3, :3] = rt
-        m[:3, 3] = -rt @ self.camera_position
-        return m
+        """World-to-camera 4x4 (host utility, reference gaze.py:114-122)."""
+        return world_to_camera(self.camera_position, self.camera_rotation)
 
     def projection_matrix(self) -> np.ndarray:
         left, right, top, bottom, near, far = self.frustum
         return perspective_matrix(left, right, bottom, top, near, far)
+
+
+def world_to_camera(position, rotation) -> np.ndarray:
+    """4x4 view matrix of a camera at `position` with orientation `rotation`
+    (xyzw): rotation block R^T, translation -R^T p (numpy matmul, i.e. the
+    BLAS FMA chain the reference's view matrices carry)."""
+    from .geometry import quat_to_matrix
+
+    r_inv = quat_to_matrix(rotation).T
+    view = np.zeros((4, 4))
+    view[3, 3] = 1.0
+    view[:3, :3] = r_inv
+    view[:3, 3] = -r_inv @ np.asarray(position, dtype=np.float64)
+    return view
 
 
 def fixation_table(fixations) -> np.ndarray:

@@ -19,6 +19,9 @@ accumulator is the fallback when peer mapping fails on some rank
 
 from __future__ import annotations
 
+import socket
+import time
+
 import numpy as np
 
 from .density import DensityMap, GenerationConfig, get_plan
@@ -53,7 +56,18 @@ def reduce_peers(plan, group=None, collective: str = "auto") -> tuple:
     rank = dist.get_rank(group)
     if collective not in ("auto", "p2p", "nccl"):
         raise ValueError(f"unknown collective {collective!r}")
-    use_p2p = collective != "nccl"
+    # every rank must hold the same sample layout: the peer kernel addresses the
+    # peers' maps by this rank's slice bounds, NCCL needs equal buffer lengths
+    me = (int(plan.n_samples), socket.gethostname())
+    peers = [None] * world
+    dist.all_gather_object(peers, me, group=group)
+    sizes = sorted({n for n, _ in peers})
+    if len(sizes) != 1:
+        raise ValueError(f"ranks hold different sample layouts (n_samples {sizes}); cannot reduce their maps")
+    same_node = len({h for _, h in peers}) == 1
+    if collective == "p2p" and not same_node:
+        raise RuntimeError("collective='p2p' needs every rank on one node (CUDA IPC peer mapping)")
+    use_p2p = collective != "nccl" and same_node
     if use_p2p:
         handles = [None] * world
         dist.all_gather_object(handles, plan.ipc_handle(), group=group)
@@ -87,7 +101,8 @@ def reduce_peers(plan, group=None, collective: str = "auto") -> tuple:
 
 
 def generate_sharded(scene, sampled_meshes: dict, fixations, config: GenerationConfig, group=None,
-                     device: int | None = None, local_compute=None, collective: str = "auto") -> DensityMap:
+                     device: int | None = None, local_compute=None, collective: str = "auto",
+                     timers=None) -> DensityMap:
     """generate() over all ranks of `group` (torch.distributed); every rank
     returns the full reduced, un-normalized map.
 
@@ -108,15 +123,23 @@ def generate_sharded(scene, sampled_meshes: dict, fixations, config: GenerationC
     if local_compute is None:
         dev = torch.cuda.current_device() if device is None else device
         objs = shard if isinstance(fixations, np.ndarray) else list(fixations)[a:b]
+        t0 = time.perf_counter()
         plan = get_plan(scene, sampled_meshes, config, dev)
-        plan.accumulate_log(objs, config, reset=True)
+        if timers is not None:
+            timers.add("upload", time.perf_counter() - t0)
+        plan.accumulate_log(objs, config, reset=True, timers=timers)
         plan.sync()
+        t0 = time.perf_counter()
         if world > 1:
             gmax, _, _ = reduce_peers(plan, group, collective)
         else:
             gmax = plan.global_max()
         gmax = gmax if len(table) else 0.0
+        t1 = time.perf_counter()
         values = plan.split(plan.read(), sampled_meshes)
+        if timers is not None:
+            timers.add("reduce_max", t1 - t0)
+            timers.add("readback", time.perf_counter() - t1)
         return DensityMap(values, global_max=gmax)
     flat = np.ascontiguousarray(local_compute(scene, sampled_meshes, shard, config), dtype=np.float64)
     t = torch.from_numpy(flat)

@@ -77,20 +77,6 @@ def test_save_map_bytes_and_roundtrip(tmp_path):
         gm.load_map(bad)
 
 
-def test_load_config(tmp_path):
-    p = tmp_path / "c.cfg"
-    p.write_text("k = 2500  # samples/m2\ntheta_deg=2\nfiltering_enabled = no\nobjects = a, b\ntime_window=1:5\n")
-    cfg = gm.load_config(p)
-    assert cfg.k == 2500.0 and cfg.filtering_enabled is False and cfg.object_include_list == {"a", "b"}
-    assert cfg.time_window == (1.0, 5.0) and cfg.theta == pytest.approx(np.radians(2.0), rel=0, abs=0)
-    p.write_text("bogus = 1\n")
-    with pytest.raises(gm.ConfigError, match="unknown config key 'bogus'"):
-        gm.load_config(p)
-    p.write_text("k\n")
-    with pytest.raises(gm.ParseError, match="line 1: expected key = value"):
-        gm.load_config(p)
-
-
 @pytest.mark.gpu
 def test_write_export_gpu_matches_reference(tmp_path):
     scene, ids, dm = _setup()

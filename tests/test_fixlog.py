@@ -84,3 +84,48 @@ def test_multithreaded_chunks_line_numbers(tmp_path):
     for th in (1, 3, 8):
         with pytest.raises(gm.ParseError, match="line 10001: bad numeric field"):
             fixlog.parse_fixation_table(p, threads=th)
+
+
+def _log_text(n):
+    lines = ["# start dur px py pz qx qy qz qw l r t b n f gx gy gz"]
+    for i in range(n):
+        lines.append(f"{0.25 * i} {0.1 + 0.01 * i} {0.1 * i} 1.5 2.0 0 0 0 1 -0.1 0.1 0.1 -0.1 0.1 100 "
+                     f"{0.01 * i} 0.02 -1")
+    return "\n".join(lines) + "\n"
+
+
+def test_in_place_edits_invalidate_cached_table(tmp_path):
+    # FixationLog caches the parsed (F, 18) table; list edits must not leave it stale
+    p = tmp_path / "f.log"
+    p.write_text(_log_text(6))
+    log = gm.parse_fixation_log(p)
+    rows = [f.row() for f in log]
+    np.testing.assert_array_equal(gm.fixation_table(log), np.array(rows))
+    log.reverse()
+    np.testing.assert_array_equal(gm.fixation_table(log), np.array(rows[::-1]))
+    log[0] = log[1]
+    np.testing.assert_array_equal(gm.fixation_table(log)[0], rows[::-1][1])
+    for edit in (lambda L: L.sort(key=lambda f: f.duration), lambda L: L.append(L[0]), lambda L: L.pop(),
+                 lambda L: L.insert(2, L[3]), lambda L: L.__delitem__(0), lambda L: L.extend(L[:2])):
+        fresh = gm.parse_fixation_log(p)
+        edit(fresh)
+        np.testing.assert_array_equal(gm.fixation_table(fresh), np.array([f.row() for f in fresh]))
+    again = gm.parse_fixation_log(p)
+    again += again[:1]
+    assert isinstance(again, fixlog.FixationLog) and len(again) == 7
+    np.testing.assert_array_equal(gm.fixation_table(again), np.array([f.row() for f in again]))
+
+
+def test_overrides_placed_into_parsed_log_are_seen(tmp_path):
+    from paper_2601_07571_b200.density import _override_list
+
+    p = tmp_path / "f.log"
+    p.write_text(_log_text(3))
+    log = gm.parse_fixation_log(p)
+    assert _override_list(log) is None
+    f0 = log[0]
+    moved = gm.Fixation(f0.start_time, f0.duration, f0.camera_position, f0.camera_rotation, f0.frustum, f0.gaze_dir,
+                        overrides={"a": gm.Transform([1.0, 0.0, 0.0], [0, 0, 0, 1], [1, 1, 1])})
+    log[0] = moved
+    ovs = _override_list(log)
+    assert ovs is not None and ovs[0] is moved.overrides

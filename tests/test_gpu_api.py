@@ -198,6 +198,43 @@ def test_accumulate_fixation_in_place():
     assert dm.global_max == full.global_max
 
 
+def test_accumulate_fixation_loop_stays_on_device():
+    """A loop of accumulate_fixation keeps the map on the GPU (no full-map
+    copies per call) and still matches generate bit for bit; reading
+    .values mid-loop, editing the arrays, interleaving generate() on the same
+    plan and a second map on the same plan all behave like the reference."""
+    scene, k, table = W.c1()
+    cfg = gm.GenerationConfig(k=k)
+    sampled = gm.build_sampled_meshes(scene, k)
+    fx = [gm.Fixation(r[0], r[1], r[2:5], r[5:9], tuple(r[9:15]), r[15:18]) for r in table[:24]]
+    dm = gm.DensityMap.zeros(sampled)
+    held = dm.values["icosphere"]  # the array object must keep receiving the values
+    for f in fx[:12]:
+        gm.accumulate_fixation(dm, scene, sampled, f, cfg)
+    half = gm.generate(scene, sampled, fx[:12], cfg)  # reuses the plan: dm is read back first
+    np.testing.assert_array_equal(held, half.values["icosphere"])
+    assert dm.global_max == half.global_max
+    for f in fx[12:18]:
+        gm.accumulate_fixation(dm, scene, sampled, f, cfg)
+    v = dm.values["icosphere"]  # readback, and the caller may now edit the arrays
+    assert v is held
+    np.testing.assert_array_equal(v, gm.generate(scene, sampled, fx[:18], cfg).values["icosphere"])
+    other = gm.DensityMap.zeros(sampled)
+    gm.accumulate_fixation(other, scene, sampled, fx[0], cfg)  # takes the plan over
+    for f in fx[18:]:
+        gm.accumulate_fixation(dm, scene, sampled, f, cfg)
+    full = gm.generate(scene, sampled, fx, cfg)
+    np.testing.assert_array_equal(dm.values["icosphere"], full.values["icosphere"])
+    assert dm.global_max == full.global_max
+    np.testing.assert_array_equal(other.values["icosphere"],
+                                  gm.generate(scene, sampled, fx[:1], cfg).values["icosphere"])
+    # an edit of the host arrays after reading them is honoured by the next call
+    dm.values["icosphere"][:] = 0.0
+    gm.accumulate_fixation(dm, scene, sampled, fx[0], cfg)
+    np.testing.assert_array_equal(dm.values["icosphere"],
+                                  gm.generate(scene, sampled, fx[:1], cfg).values["icosphere"])
+
+
 def test_normalize_and_estimator():
     scene = sphere_in_box()
     dm, _, _ = run(scene, [fix([0.0, 0.0, 3.0], target=[0, 0, 0])], k=5000.0)

@@ -209,32 +209,88 @@ def c2(n_fix: int = 100_000):
     return scene, 10_000.0, room_fixations(n_fix, 1, scene)
 
 
-def session_fixations(users: int = 50, per_user: int = 20_000, scene: Scene | None = None) -> np.ndarray:
-    """C4: per-user camera random walks (step N(0, 0.05) m, eye height 1.6 +-
-    0.1) with a new target every ~5 fixations; users concatenated."""
+def look_at_quats(positions, targets, up=(0.0, 1.0, 0.0)) -> np.ndarray:
+    """Row-wise look_at_quat for (F, 3) cameras and targets (same formulas,
+    vectorised; results can differ from the scalar version in the last bit)."""
+    p = np.asarray(positions, np.float64)
+    fwd = np.asarray(targets, np.float64) - p
+    fwd /= np.sqrt((fwd * fwd).sum(axis=1))[:, None]
+    upv = np.broadcast_to(np.asarray(up, np.float64), fwd.shape).copy()
+    upv[np.abs(fwd @ np.asarray(up, np.float64)) > 0.999] = (1.0, 0.0, 0.0)
+    right = np.cross(fwd, upv)
+    right /= np.sqrt((right * right).sum(axis=1))[:, None]
+    true_up = np.cross(right, fwd)
+    m = np.stack([right, true_up, -fwd], axis=2)  # columns
+    tr = m[:, 0, 0] + m[:, 1, 1] + m[:, 2, 2]
+    q = np.empty((len(p), 4))
+    c0 = tr > 0
+    c1 = ~c0 & (m[:, 0, 0] > m[:, 1, 1]) & (m[:, 0, 0] > m[:, 2, 2])
+    c2 = ~c0 & ~c1 & (m[:, 1, 1] > m[:, 2, 2])
+    c3 = ~(c0 | c1 | c2)
+    with np.errstate(invalid="ignore", divide="ignore"):
+        s0 = np.sqrt(tr + 1.0) * 2
+        s1 = np.sqrt(1.0 + m[:, 0, 0] - m[:, 1, 1] - m[:, 2, 2]) * 2
+        s2 = np.sqrt(1.0 + m[:, 1, 1] - m[:, 0, 0] - m[:, 2, 2]) * 2
+        s3 = np.sqrt(1.0 + m[:, 2, 2] - m[:, 0, 0] - m[:, 1, 1]) * 2
+        cand = [
+            (c0, np.stack([(m[:, 2, 1] - m[:, 1, 2]) / s0, (m[:, 0, 2] - m[:, 2, 0]) / s0,
+                           (m[:, 1, 0] - m[:, 0, 1]) / s0, 0.25 * s0], axis=1)),
+            (c1, np.stack([0.25 * s1, (m[:, 0, 1] + m[:, 1, 0]) / s1, (m[:, 0, 2] + m[:, 2, 0]) / s1,
+                           (m[:, 2, 1] - m[:, 1, 2]) / s1], axis=1)),
+            (c2, np.stack([(m[:, 0, 1] + m[:, 1, 0]) / s2, 0.25 * s2, (m[:, 1, 2] + m[:, 2, 1]) / s2,
+                           (m[:, 0, 2] - m[:, 2, 0]) / s2], axis=1)),
+            (c3, np.stack([(m[:, 0, 2] + m[:, 2, 0]) / s3, (m[:, 1, 2] + m[:, 2, 1]) / s3, 0.25 * s3,
+                           (m[:, 1, 0] - m[:, 0, 1]) / s3], axis=1)),
+        ]
+    for mask, val in cand:
+        q[mask] = val[mask]
+    return q / np.sqrt((q * q).sum(axis=1))[:, None]
+
+
+def session_fixations(users: int = 50, per_user: int = 20_000, scene: Scene | None = None,
+                      first_user: int = 0) -> np.ndarray:
+    """C4: users first_user .. first_user + users - 1, concatenated; user u
+    (seed 100 + u) walks the room (steps N(0, 0.05) m, eye height 1.6 +- 0.1,
+    clamped to the room) and picks a new target every 5 fixations (a prop
+    centre with p = 0.6, else a random wall point); gaze tilted U(0, 0.15) rad,
+    durations U(0.1, 0.6) s.  Vectorised per user."""
     scene = scene or room_scene()
-    props = [o.mesh.vertices.mean(axis=0) for o in scene.objects if o.object_id.startswith(("prop", "bowl"))]
+    props = np.array([o.mesh.vertices.mean(axis=0) for o in scene.objects
+                      if o.object_id.startswith(("prop", "bowl"))])
     rows = []
-    for u in range(users):
+    n = per_user
+    for u in range(first_user, first_user + users):
         rng = np.random.default_rng(100 + u)
-        p = np.array([rng.uniform(-3, 3), 1.6 + rng.uniform(-0.1, 0.1), rng.uniform(-2, 2)])
-        pos, tgt, gz, dur = [], [], [], []
-        t = props[rng.integers(len(props))]
-        for i in range(per_user):
-            p = p + rng.normal(0.0, 0.05, 3)
-            p[0] = np.clip(p[0], -3.7, 3.7)
-            p[1] = np.clip(p[1], 1.5, 1.7)
-            p[2] = np.clip(p[2], -2.7, 2.7)
-            if i % 5 == 0:
-                t = props[rng.integers(len(props))] if rng.uniform() < 0.6 else np.array(
-                    [rng.uniform(-3.9, 3.9), rng.uniform(0.1, 2.9), rng.choice([-3.0, 3.0])])
-            tt = t if np.linalg.norm(t - p) > 0.3 else t + np.array([0.0, 0.0, -1.0])
-            pos.append(p.copy())
-            tgt.append(tt)
-            gz.append(tilted_gaze(rng, 0.15))
-            dur.append(rng.uniform(0.1, 0.6))
-        rows.append(fixation_rows(pos, tgt, gz, dur))
-    return np.concatenate(rows)
+        p0 = np.array([rng.uniform(-3, 3), 1.6 + rng.uniform(-0.1, 0.1), rng.uniform(-2, 2)])
+        steps = rng.normal(0.0, 0.05, (n, 3))
+        lo, hi = np.array([-3.7, 1.5, -2.7]), np.array([3.7, 1.7, 2.7])
+        pos = np.empty((n, 3))
+        p = p0
+        for i in range(n):  # clamped random walk (sequential by nature)
+            p = np.minimum(np.maximum(p + steps[i], lo), hi)
+            pos[i] = p
+        n_t = (n + 4) // 5
+        pick_prop = rng.uniform(size=n_t) < 0.6
+        prop_idx = rng.integers(len(props), size=n_t)
+        wall = np.column_stack([rng.uniform(-3.9, 3.9, n_t), rng.uniform(0.1, 2.9, n_t),
+                                rng.choice([-3.0, 3.0], n_t)])
+        tgt = np.where(pick_prop[:, None], props[prop_idx], wall)[np.arange(n) // 5]
+        near = np.sqrt(((tgt - pos) ** 2).sum(axis=1)) <= 0.3
+        tgt = tgt + near[:, None] * np.array([0.0, 0.0, -1.0])
+        a = rng.uniform(0.0, 2.0 * math.pi, n)
+        ang = rng.uniform(0.0, 0.15, n)
+        g = np.column_stack([np.sin(ang) * np.sin(a), -np.sin(ang) * np.cos(a), -np.cos(ang)])
+        g /= np.sqrt((g * g).sum(axis=1))[:, None]
+        dur = rng.uniform(0.1, 0.6, n)
+        t = np.empty((n, 18))
+        t[:, 0] = 0.25 * np.arange(n)
+        t[:, 1] = dur
+        t[:, 2:5] = pos
+        t[:, 5:9] = look_at_quats(pos, tgt)
+        t[:, 9:15] = FRUSTUM
+        t[:, 15:18] = g
+        rows.append(t)
+    return np.concatenate(rows) if rows else np.zeros((0, 18))
 
 
 def shells_scene() -> Scene:
