@@ -44,7 +44,7 @@
 // launch bounds of the hot kernels; -DTX_MINB=n etc. (build variants) cap
 // their registers for n CTAs per SM
 #ifndef TX_MINB
-#define TX_MINB 7  // 72 registers (the tile-max reduction would otherwise push k_texels to 80)
+#define TX_MINB 14  // 64-thread CTAs: 72 registers (uncapped the first pass takes 88)
 #endif
 #if TX_MINB > 0
 #define TX_BOUNDS __launch_bounds__(TX_MAX_THREADS, TX_MINB)
@@ -980,22 +980,22 @@ extern "C" int gm_plan_create(int device, gm_plan** out) {
 
 // Kernel attributes and the plan's fixed device buffers (gm_plan_create).
 static int plan_init(gm_plan* p) {
-    CK(cudaFuncSetAttribute(k_texels<false, false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
-    CK(cudaFuncSetAttribute(k_texels<false, false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_DYN_SMEM));
-    CK(cudaFuncSetAttribute(k_texels<false, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
-    CK(cudaFuncSetAttribute(k_texels<false, false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_DYN_SMEM));
-    CK(cudaFuncSetAttribute(k_texels<false, true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
-    CK(cudaFuncSetAttribute(k_texels<false, true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_DYN_SMEM));
-    CK(cudaFuncSetAttribute(k_texels<false, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
-    CK(cudaFuncSetAttribute(k_texels<false, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_DYN_SMEM));
-    CK(cudaFuncSetAttribute(k_texels<true, false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
-    CK(cudaFuncSetAttribute(k_texels<true, false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_DYN_SMEM));
-    CK(cudaFuncSetAttribute(k_texels<true, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
-    CK(cudaFuncSetAttribute(k_texels<true, false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_DYN_SMEM));
-    CK(cudaFuncSetAttribute(k_texels<true, true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
-    CK(cudaFuncSetAttribute(k_texels<true, true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_DYN_SMEM));
-    CK(cudaFuncSetAttribute(k_texels<true, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
-    CK(cudaFuncSetAttribute(k_texels<true, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels<false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels_crowded<false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels_crowded<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels<false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels_crowded<false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels<false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels_crowded<false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels<true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels_crowded<true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels<true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels_crowded<true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels<true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels_crowded<true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels<true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels_crowded<true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_DYN_SMEM));
     CK(cudaMalloc(&p->d_max, sizeof(unsigned long long)));
     CK(cudaMalloc(&p->d_stats, GM_STAT_STRIPES * GM_STAT_N * sizeof(unsigned long long)));
     CK(cudaMemset(p->d_stats, 0, GM_STAT_STRIPES * GM_STAT_N * sizeof(unsigned long long)));
@@ -1329,10 +1329,10 @@ static int launch_texels(gm_plan* p, cudaStream_t s, const TriStore& ts, DepthVi
     CK(cudaMemsetAsync(p->d_crowd_count, 0, 2 * sizeof(int), s));
     const int tiles_y = tiles_per_fix / tiles_x;
     const dim3 grid((unsigned)tiles_x, (unsigned)((tiles_y + TW_WARPS - 1) / TW_WARPS), (unsigned)(items / tiles_per_fix));
-    k_texels<ATTRS, STATS, false, EXACT><<<grid, TW_WARPS * 32, TX_DYN_SMEM, s>>>(ts, dv, cb, tiles_x, tiles_per_fix,
-                                                                              tiles_y, fix, b0);
-    k_texels<ATTRS, STATS, true, EXACT><<<p->sms * (20 / TC_WARPS), TC_WARPS * 32, TC_DYN_SMEM, s>>>(
-        ts, dv, cb, tiles_x, tiles_per_fix, tiles_y, fix, b0);
+    k_texels<ATTRS, STATS, EXACT><<<grid, TW_WARPS * 32, TX_DYN_SMEM, s>>>(ts, dv, cb, tiles_x, tiles_per_fix,
+                                                                       tiles_y, fix, b0);
+    k_texels_crowded<ATTRS, STATS, EXACT><<<p->sms * HV_MINB, HV_WARPS * 32, TC_DYN_SMEM, s>>>(
+        ts, dv, cb, tiles_x, tiles_per_fix, fix, b0);
     CK(cudaGetLastError());
     return GM_OK;
 }

@@ -18,20 +18,20 @@ struct __align__(16) TexelWarpSmem {
     float key[TW_SEL + 32];  // -inv_minw of sel[] (sort key: ascending min depth)
 };
 #define TX_DYN_SMEM (TW_WARPS * (int)sizeof(TexelWarpSmem))
-#ifndef TC_SEL
-#define TC_SEL 512   // crowded tiles: overlap list sorted per pass (longer lists: several passes)
+#ifndef HV_WARPS
+#define HV_WARPS 8      // warps per CTA of the crowded pass (the tile's rounds of texels are shared out)
 #endif
-#ifndef TC_RES
-#define TC_RES 64    // crowded tiles: nearest triangles staged in shared memory
+#ifndef HV_MINB
+#define HV_MINB 3       // resident crowded-pass CTAs per SM the register budget is sized for
 #endif
-struct __align__(16) CrowdedWarpSmem {
-    TriF32 t32[TC_RES];
-    int sel[TC_SEL];
-    float key[TC_SEL];
+#ifndef HV_SEL
+#define HV_SEL 2048     // crowded tiles: overlap list gathered + sorted per pass (longer lists: several passes)
+#endif
+struct __align__(16) HeavySmem {
+    TriF32 t32[HV_WARPS][32];  // each warp's staging slice
+    int sel[HV_SEL + 4];       // sorted segment indices; [HV_SEL]: pass count, [+1]: tile max, [+2]: claimed item
+    float key[HV_SEL];         // -inv_minw of sel[] (sort key: ascending min depth)
 };
-#ifndef TC_WARPS
-#define TC_WARPS 4  // warps per CTA of the crowded pass
-#endif
 #ifndef CROWD_DEPTH
 #define CROWD_DEPTH 10  // ... and whose triangle bboxes cover the tile more than this many times
 #endif
@@ -41,11 +41,14 @@ struct __align__(16) CrowdedWarpSmem {
 #ifndef CROWD_MID
 #define CROWD_MID 128  // ... and, in crop-frustum batches, tiles overlapping TW_CAP < n <= this many triangles
 #endif
+#ifndef CROWD_ALL
+#define CROWD_ALL 0  // 1: every tile with more than TW_CAP overlapping triangles goes to the crowded pass
+#endif
 #ifndef CROWD_MIN
 #define CROWD_MIN 128  // tiles overlapping more triangles than this go to the crowded pass
 #endif
-#define TC_DYN_SMEM (TC_WARPS * (int)sizeof(CrowdedWarpSmem))
-#define TX_MAX_THREADS (32 * (TW_WARPS > TC_WARPS ? TW_WARPS : TC_WARPS))
+#define TC_DYN_SMEM ((int)sizeof(HeavySmem))
+#define TX_MAX_THREADS (32 * TW_WARPS)
 
 // position of the k-th (0-based) set bit of w (k < popc(w))
 __device__ __forceinline__ int kth_set_bit(uint32_t w, int k) {
@@ -247,14 +250,16 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
             bwin = cs;
         }
     };
-    // triangle kk of the walk: staged in shared memory (kk < nst) or, crowded mode, from global
-    auto tri_at = [&](int kk, int nst) -> const TriF32& { return (!CROWDED || kk < nst) ? T32[kk] : segf[SEL[kk]]; };
+    // triangle kk of the walk: staged in shared memory
+    auto tri_at = [&](int kk) -> const TriF32& { return T32[kk]; };
     // Returns true when (allow_fast) one certainly-written candidate provably wins:
     // then its segment index is in bwin and fastb holds rigorous float32 bounds of
     // its inverse depth at the texel -- no float64 evaluation (the accumulation pass
     // decides its depth tests on these bounds and evaluates only undecided ones).
-    auto walk = [&](int kend, int nst, bool valid, int row, int colo, float& V, double& best, int& bkey, int& bwin,
-                    bool allow_fast, float2& fastb) -> bool {
+    // fetch(kk): the kk-th triangle in walk order (warp-uniform kk); tri_all(k): the
+    // same record for the slow path.
+    auto walk_with = [&](int kend, auto&& fetch, auto&& tri_all, bool valid, int row, int colo, float& V,
+                         double& best, int& bkey, int& bwin, bool allow_fast, float2& fastb) -> bool {
         const int px = xb + colo, py = yb + row;
         const float pxc = (float)px + 0.5f, pyc = (float)py + 0.5f;  // pixel centre
         int cs0 = -1, cs1 = -1;  // exact candidates (global record index) and their bounds
@@ -263,7 +268,7 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
         bool ce0 = false, ce1 = false;  // certainly covering and written
         bool overflow = false;
         for (int kk = 0; kk < kend; kk++) {
-            const TriF32& t = tri_at(kk, nst);
+            const TriF32& t = fetch(kk);
             // (inv_minw, ox, oy, wx) and (wy, gidx): both loads up front, so the bbox test
             // below is one predicate and one branch
             const float4 hd = *reinterpret_cast<const float4*>(&t.inv_minw);
@@ -338,7 +343,7 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
             }
         } else {  // slow path: every staged triangle whose bbox covers the texel
             for (int k = 0; k < kend; k++) {
-                const TriF32& t = tri_at(k, nst);
+                const TriF32& t = tri_all(k);
                 const float fx = pxc - t.ox, fy = pyc - t.oy;
                 if (!(fx > 0.0f) || !(fx < t.wx) || !(fy > 0.0f) || !(fy < t.wy)) continue;
                 const double d = texel_depth(seg[t.gidx], px, py, near_, far_);
@@ -348,6 +353,10 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
             }
         }
         return false;
+    };
+    auto walk = [&](int kend, bool valid, int row, int colo, float& V, double& best, int& bkey, int& bwin,
+                    bool allow_fast, float2& fastb) -> bool {
+        return walk_with(kend, tri_at, tri_at, valid, row, colo, V, best, bkey, bwin, allow_fast, fastb);
     };
 
     double* dep = dv.depth + (int64_t)f * W * H;
@@ -427,6 +436,16 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
         store_at((int64_t)(yb + row) * W + xb + colo, fast, fb, best, bkey, bwin);
     };
     if (!CROWDED) {
+        auto defer = [&]() {  // k_texels_crowded sorts the whole list (one CTA per tile)
+            if (lane == 0) dv.crowd[atomicAdd(dv.crowd_count, 1)] = (int)item;
+            if (STATS) stat_add(dv.stats, GM_STAT_TX_CROWDED, lane == 0 ? 1ull : 0ull);
+        };
+#if CROWD_ALL
+        if (dv.crowd && n > TW_SEL) {  // a long list: leave even the gather to the CTA pass
+            defer();
+            return;
+        }
+#endif
         int nsel = gather(cursor);
         if (STATS) nsel_total = nsel;
         // deep tiles (overlapping surfaces: the selected bboxes cover the tile more than
@@ -435,14 +454,19 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
         // mid-size lists (TW_CAP < nsel <= CROWD_MID) go there too: the crowded pass stages
         // them whole (TC_RES) and walks them in one pass with the float32 fast path, where
         // the multi-chunk walk here must resolve every chunk's candidates exactly
+#if CROWD_ALL
+        if (dv.crowd && (cursor < n || nsel > TW_CAP)) {  // every multi-chunk tile
+            defer();
+            return;
+        }
+#else
         const bool mid = cursor >= n && nsel > TW_CAP && nsel <= dv.crowd_mid;
         if (dv.crowd && (mid || ((cursor < n || nsel > CROWD_MIN) &&
                                  __reduce_add_sync(FULL, (unsigned)cover) > (unsigned)(dv.crowd_depth * TW * TH)))) {
-            // more than TW_CAP triangles: k_texels<CROWDED> sorts the whole list (deferred)
-            if (lane == 0) dv.crowd[atomicAdd(dv.crowd_count, 1)] = (int)item;
-            if (STATS) stat_add(dv.stats, GM_STAT_TX_CROWDED, lane == 0 ? 1ull : 0ull);
+            defer();
             return;
         }
+#endif
         if (cursor >= n && nsel <= TW_CAP) {
             // common case: one staging serves every round, per-texel state in registers
             if (nsel > 0) stage(0, nsel);
@@ -456,7 +480,7 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
                 int bkey = INT_MAX, bwin = -1;
                 float2 fb = make_float2(0.0f, 0.0f);
                 bool fast = false;
-                if (nsel > 0) fast = walk(nsel, nsel, valid, row, colo, V, best, bkey, bwin, !EXACT, fb);
+                if (nsel > 0) fast = walk(nsel, valid, row, colo, V, best, bkey, bwin, !EXACT, fb);
                 if (valid) store(row, colo, fast, fb, best, bkey, bwin);
             }
         } else {
@@ -482,7 +506,7 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
                         if (ATTRS && valid && !first) bkey = dv.key[at];
                         if (!EXACT && valid && !first) bwin = win[at];
                         float2 fb;
-                        walk(kend, kend, valid, row, colo, V, best, bkey, bwin, false, fb);
+                        walk(kend, valid, row, colo, V, best, bkey, bwin, false, fb);
                         if (valid) {
                             vb[at] = V;
                             if (last) {
@@ -526,21 +550,27 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
             }
         }
     } else {
-        // crowded tile: gather the whole overlap list (TC_SEL at a time), sort it by
-        // ascending min depth, stage the nearest TC_RES float32 forms; the walk reads
-        // any later one from global memory.  The nearest certain cover then proves
-        // (V) that every later triangle is behind it, so a texel's walk usually ends
-        // in the first chunk -- nested surfaces cost one sort, not one pass each.
+        // crowded tile, one CTA (HV_WARPS warps) per tile: the CTA gathers the whole
+        // overlap list (HV_SEL entries per pass), sorts it by ascending min depth (then
+        // segment index) in shared memory, and its warps take the tile's rounds of 32
+        // marked texels; each walks the sorted list, staging 32 float32 forms at a time
+        // into its own slice.  The nearest certain cover proves (V) every later
+        // triangle hidden, so a round usually ends after the first chunks -- nested
+        // surfaces cost one sort, not one pass each; rounds run side by side.
+        const int tid = threadIdx.x, warp = tid >> 5, nthr = blockDim.x;
+        int* s_cnt = SEL + HV_SEL;  // scalar slot after the arrays
         float* vb = dv.vbuf + (int64_t)f * W * H;
         bool first = true;
         do {
+            if (tid == 0) *s_cnt = 0;
+            __syncthreads();
             int cnt = 0;
-            while (cursor < n && cnt < TC_SEL - 32) {
-                int i = cursor + lane;
-                bool sel = false;
-                float key = 0.0f;
-                if (i < n) {
+            while (true) {  // blocks of nthr list entries until the pass is full or the list ends
+                const int i0 = cursor + tid;
+                if (i0 < n) {
+                    int i = i0;
                     uint2 bbx;
+                    float key;
                     if (clist) {
                         const int4 e = clist[i];
                         i = e.x;
@@ -551,56 +581,63 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
                         key = -__ldg(&segf[i].inv_minw);
                     }
                     const int x0 = bbx.x & 0xffff, x1 = bbx.x >> 16, y0 = bbx.y & 0xffff, y1 = bbx.y >> 16;
-                    sel = !(x1 < xb || x0 > xe || y1 < yb || y0 > ye);
+                    if (!(x1 < xb || x0 > xe || y1 < yb || y0 > ye)) {
+                        const int at = atomicAdd(s_cnt, 1);
+                        SEL[at] = i;
+                        KEY[at] = key;
+                    }
                 }
-                const unsigned bal = __ballot_sync(FULL, sel);
-                if (sel) {
-                    const int at = cnt + __popc(bal & ((1u << lane) - 1u));
-                    SEL[at] = i;
-                    KEY[at] = key;
-                }
-                cnt += __popc(bal);
-                cursor += 32;
+                cursor += nthr;
+                __syncthreads();
+                cnt = *s_cnt;
+                if (cursor >= n || cnt > HV_SEL - nthr) break;
+                __syncthreads();  // every thread has read the count before the next block adds to it
             }
             if (STATS) nsel_total += cnt;
             int P = 32;
             while (P < cnt) P <<= 1;
-            for (int k = cnt + lane; k < P; k += 32) {
+            for (int k = cnt + tid; k < P; k += nthr) {
                 KEY[k] = CUDART_INF_F;
-                SEL[k] = -1;
+                SEL[k] = INT_MAX;
             }
-            __syncwarp();
-            // warp bitonic sort of (KEY, SEL) ascending, P <= TC_SEL
+            __syncthreads();
+            // CTA bitonic sort of (KEY, SEL) ascending, P <= HV_SEL
             for (int size = 2; size <= P; size <<= 1) {
                 for (int stride = size >> 1; stride > 0; stride >>= 1) {
-                    for (int a = lane; a < P; a += 32) {
-                        const int b = a ^ stride;
-                        if (b > a) {
-                            const float ka = KEY[a], kb = KEY[b];
-                            const int sa = SEL[a], sb = SEL[b];
-                            const bool up = (a & size) == 0;
-                            const bool gt = ka > kb || (ka == kb && sa > sb);
-                            if (gt == up) {
-                                KEY[a] = kb;
-                                KEY[b] = ka;
-                                SEL[a] = sb;
-                                SEL[b] = sa;
-                            }
+                    for (int t = tid; t < (P >> 1); t += nthr) {
+                        const int a = 2 * t - (t & (stride - 1)), b = a + stride;
+                        const float ka = KEY[a], kb = KEY[b];
+                        const int sa = SEL[a], sb = SEL[b];
+                        const bool up = (a & size) == 0;
+                        const bool gt = ka > kb || (ka == kb && sa > sb);
+                        if (gt == up) {
+                            KEY[a] = kb;
+                            KEY[b] = ka;
+                            SEL[a] = sb;
+                            SEL[b] = sa;
                         }
+                    }
+                    __syncthreads();
+                }
+            }
+            const bool last = cursor >= n;
+            // walk order: the sorted list, staged 32 records at a time into this warp's slice
+            auto fetch = [&](int kk) -> const TriF32& {
+                if ((kk & 31) == 0) {
+                    __syncwarp();
+                    const int k = kk + lane;
+                    if (k < cnt) {
+                        const uint4* from = reinterpret_cast<const uint4*>(segf + SEL[k]);
+                        uint4* to = reinterpret_cast<uint4*>(&T32[lane]);
+#pragma unroll
+                        for (int part = 0; part < 6; part++) to[part] = from[part];
                     }
                     __syncwarp();
                 }
-            }
-            const int ns = min(cnt, TC_RES);
-            for (int k = lane; k < ns; k += 32) {
-                const uint4* from = reinterpret_cast<const uint4*>(segf + SEL[k]);
-                uint4* to = reinterpret_cast<uint4*>(&T32[k]);
-#pragma unroll
-                for (int part = 0; part < 6; part++) to[part] = from[part];
-            }
-            __syncwarp();
-            const bool last = cursor >= n;
-            for (int r0 = 0; r0 < total; r0 += 32) {
+                return T32[kk & 31];
+            };
+            auto from_global = [&](int k) -> const TriF32& { return segf[SEL[k]]; };
+            for (int r0 = warp * 32; r0 < total; r0 += nthr) {
                 const int q = r0 + lane;
                 const bool valid = q < total;
                 int row, colo;
@@ -614,7 +651,9 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
                 float2 fb = make_float2(0.0f, 0.0f);
                 bool fast = false;
                 // a single pass (the usual case) may take the float32 fast path
-                if (cnt > 0) fast = walk(cnt, ns, valid, row, colo, V, best, bkey, bwin, !EXACT && first && last, fb);
+                if (cnt > 0)
+                    fast = walk_with(cnt, fetch, from_global, valid, row, colo, V, best, bkey, bwin,
+                                     !EXACT && first && last, fb);
                 if (valid) {
                     if (last) {
                         store_at(at, fast, fb, best, bkey, bwin);
@@ -627,20 +666,30 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
                 }
             }
             first = false;
-            __syncwarp();
+            __syncthreads();  // the next pass overwrites SEL / KEY
         } while (cursor < n);
     }
     if (!EXACT && dv.tmax) {
         // depths are > 0: the float bit patterns order like ints (-inf < every depth)
         const int m = __reduce_max_sync(FULL, __float_as_int(tmax));
-        if (lane == 0) dv.tmax[item] = __int_as_float(m);
+        if (!CROWDED) {
+            if (lane == 0) dv.tmax[item] = __int_as_float(m);
+        } else {  // every warp of the CTA holds a share of the tile's texels
+            int* s_max = SEL + HV_SEL + 1;
+            if (threadIdx.x == 0) *s_max = __float_as_int(-CUDART_INF_F);
+            __syncthreads();
+            if (lane == 0) atomicMax(s_max, m);
+            __syncthreads();
+            if (threadIdx.x == 0) dv.tmax[item] = __int_as_float(*s_max);
+        }
     }
     if (STATS) {
         const bool l0 = lane == 0;
-        stat_add(dv.stats, GM_STAT_TEXELS, l0 ? (unsigned long long)total : 0ull);
-        stat_add(dv.stats, GM_STAT_TX_TILES, l0 ? 1ull : 0ull);
-        stat_add(dv.stats, GM_STAT_TX_STAGED, l0 ? (unsigned long long)nsel_total : 0ull);
-        stat_add(dv.stats, GM_STAT_TX_LIST, l0 ? (unsigned long long)n : 0ull);
+        const bool t0 = l0 && (!CROWDED || threadIdx.x == 0);  // per-tile counts: one warp of the CTA
+        stat_add(dv.stats, GM_STAT_TEXELS, t0 ? (unsigned long long)total : 0ull);
+        stat_add(dv.stats, GM_STAT_TX_TILES, t0 ? 1ull : 0ull);
+        stat_add(dv.stats, GM_STAT_TX_STAGED, t0 ? (unsigned long long)nsel_total : 0ull);
+        stat_add(dv.stats, GM_STAT_TX_LIST, t0 ? (unsigned long long)n : 0ull);
         stat_add(dv.stats, GM_STAT_TX_ITER, l0 ? c_iter : 0ull);
         stat_add(dv.stats, GM_STAT_PAIRS, c_pairs);
         stat_add(dv.stats, GM_STAT_TX_CHUNKED, (l0 && chunked) ? 1ull : 0ull);
@@ -652,36 +701,44 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
 }
 
 // First pass: grid (tiles_x, ceil(tiles_y / TW_WARPS), fixations); warp w of a
-// CTA takes tile row blockIdx.y * TW_WARPS + w.  Crowded pass: persistent warps
-// over the deferred items.
-template <bool ATTRS, bool STATS, bool CROWDED, bool EXACT>
+// CTA takes tile row blockIdx.y * TW_WARPS + w.
+template <bool ATTRS, bool STATS, bool EXACT>
 __global__ void TX_BOUNDS k_texels(TriStore ts, DepthView dv, CoarseBins cb, int tiles_x,
                                    int tiles_per_fix, int tiles_y,
                                    const GmFixExact* __restrict__ fixes, long long b0) {
     extern __shared__ __align__(16) unsigned char tx_dyn[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
     if (*ts.fail <= b0) return;
-    if (!CROWDED) {
-        const int ty = blockIdx.y * TW_WARPS + warp;
-        if (ty < tiles_y)
-            texel_item<ATTRS, STATS, false, EXACT>(reinterpret_cast<TexelWarpSmem*>(tx_dyn)[warp].t32,
-                                            reinterpret_cast<TexelWarpSmem*>(tx_dyn)[warp].sel,
-                                            reinterpret_cast<TexelWarpSmem*>(tx_dyn)[warp].key, blockIdx.z,
-                                            blockIdx.x, ty, ts, dv, cb, tiles_x, tiles_per_fix, fixes);
-        return;
-    }
-    // crowded tiles (deferred by the pass above): persistent warps over the list
-    CrowdedWarpSmem& C = reinterpret_cast<CrowdedWarpSmem*>(tx_dyn)[warp];
+    const int ty = blockIdx.y * TW_WARPS + warp;
+    if (ty < tiles_y)
+        texel_item<ATTRS, STATS, false, EXACT>(reinterpret_cast<TexelWarpSmem*>(tx_dyn)[warp].t32,
+                                               reinterpret_cast<TexelWarpSmem*>(tx_dyn)[warp].sel,
+                                               reinterpret_cast<TexelWarpSmem*>(tx_dyn)[warp].key, blockIdx.z,
+                                               blockIdx.x, ty, ts, dv, cb, tiles_x, tiles_per_fix, fixes);
+}
+
+// Crowded pass: persistent CTAs of HV_WARPS warps over the tiles the first
+// pass deferred, one tile per CTA at a time (texel_item, CROWDED branch).
+template <bool ATTRS, bool STATS, bool EXACT>
+__global__ void __launch_bounds__(HV_WARPS * 32, HV_MINB) k_texels_crowded(TriStore ts, DepthView dv, CoarseBins cb,
+                                                                          int tiles_x, int tiles_per_fix,
+                                                                          const GmFixExact* __restrict__ fixes,
+                                                                          long long b0) {
+    extern __shared__ __align__(16) unsigned char tx_dyn[];
+    HeavySmem& C = *reinterpret_cast<HeavySmem*>(tx_dyn);
+    const int warp = threadIdx.x >> 5;
+    if (*ts.fail <= b0) return;
     const int n_crowd = *dv.crowd_count;
+    int* claim = C.sel + HV_SEL + 2;
     for (;;) {
-        int w = 0;
-        if (lane == 0) w = atomicAdd(dv.crowd_count + 1, 1);
-        w = __shfl_sync(0xffffffffu, w, 0);
+        if (threadIdx.x == 0) *claim = atomicAdd(dv.crowd_count + 1, 1);
+        __syncthreads();
+        const int w = *claim;
+        __syncthreads();  // every warp has read the claim before thread 0 replaces it
         if (w >= n_crowd) break;
         const int item = dv.crowd[w];
         const int f = item / tiles_per_fix, tile = item - f * tiles_per_fix;
-        texel_item<ATTRS, STATS, true, EXACT>(C.t32, C.sel, C.key, f, tile % tiles_x, tile / tiles_x, ts, dv, cb,
-                                              tiles_x, tiles_per_fix, fixes);
+        texel_item<ATTRS, STATS, true, EXACT>(C.t32[warp], C.sel, C.key, f, tile % tiles_x, tile / tiles_x, ts, dv,
+                                              cb, tiles_x, tiles_per_fix, fixes);
     }
 }
-

@@ -280,3 +280,28 @@ def test_reference_dataclasses_accepted():
     vals, gmax = O.generate(scene, rows, k=cfg.k)
     for oid in vals:
         np.testing.assert_allclose(dm.values[oid], vals[oid], rtol=1e-12, atol=0)
+
+
+def test_integration_md_ctypes_stub_runs():
+    """The ctypes stub INTEGRATION.md section 2 tells a reference maintainer to
+    add (gazemap/_b200.py replacing density.generate) is executed as written,
+    against the built library, and gives the package's own result."""
+    import re
+    from pathlib import Path
+
+    from paper_2601_07571_b200 import _native
+
+    text = (Path(__file__).resolve().parents[1] / "INTEGRATION.md").read_text()
+    block = re.findall(r"```python\n(# gazemap/_b200\.py.*?)```", text, re.S)[0]
+    block = block.replace("/path/to/_gazemap_b200.so", str(_native.SO_PATH))
+    ns = {"DensityMap": gm.DensityMap, "InvalidFrustumError": gm.InvalidFrustumError}
+    exec(compile(block, "INTEGRATION.md", "exec"), ns)
+    scene, k, table = W.c1()
+    fx = [gm.Fixation(r[0], r[1], r[2:5], r[5:9], tuple(r[9:15]), r[15:18]) for r in table[:64]]
+    cfg = gm.GenerationConfig(k=k)
+    sampled = gm.build_sampled_meshes(scene, k)
+    got = ns["generate"](scene, sampled, fx, cfg)
+    want = gm.generate(scene, sampled, fx, cfg)
+    assert got.global_max == want.global_max > 0
+    for oid in want.values:
+        np.testing.assert_array_equal(got.values[oid], want.values[oid])

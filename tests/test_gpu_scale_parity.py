@@ -51,6 +51,7 @@ def _stream(name):
 
 
 def _layout(scene, k, key):
+    key = ("layout", key)
     if key not in _CACHE:
         _CACHE[key] = (gm.build_sampled_meshes(scene, k), O.build_layouts(scene, k))
     return _CACHE[key]
