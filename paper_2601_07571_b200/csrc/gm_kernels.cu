@@ -345,6 +345,9 @@ struct TriStore {
 #ifndef TS_WARPS
 #define TS_WARPS 2  // warps (independent cluster groups) per k_tri_setup CTA
 #endif
+#ifndef TS_VEC_STORE
+#define TS_VEC_STORE 1  // TriF32 assembled in registers, six 16-byte stores (C5 cull 352 -> 258 ms)
+#endif
 __global__ void __launch_bounds__(TS_WARPS * 32) k_tri_setup(const double* __restrict__ tw, int64_t T,
                                                    const float4* __restrict__ tsph, const float4* __restrict__ csph,
                                                    int64_t n_clu, const GmFixExact* __restrict__ fixes,
@@ -395,7 +398,18 @@ __global__ void __launch_bounds__(TS_WARPS * 32) k_tri_setup(const double* __res
         for (int q = 0; q < n; q++) {
             if (at + q < ts.cap_seg) {
                 seg[at + q] = out[q];
+#if TS_VEC_STORE
+                {  // assemble the float32 form in registers, then six 16-byte stores
+                    TriF32 tf;
+                    make_tri_f32(out[q], at + q, tf);
+                    uint4* dst = reinterpret_cast<uint4*>(&ts.t32[(int64_t)f * ts.cap_seg + at + q]);
+                    const uint4* src = reinterpret_cast<const uint4*>(&tf);
+#pragma unroll
+                    for (int part = 0; part < 6; part++) dst[part] = src[part];
+                }
+#else
                 make_tri_f32(out[q], at + q, ts.t32[(int64_t)f * ts.cap_seg + at + q]);
+#endif
                 segb[at + q] = make_uint2((uint32_t)out[q].x0 | ((uint32_t)out[q].x1 << 16),
                                           (uint32_t)out[q].y0 | ((uint32_t)out[q].y1 << 16));
             }
@@ -552,6 +566,7 @@ struct DepthView {
     int tiles_x, tiles_per_fix;
     int crowd_mid;    // k_texels: lists of TW_CAP < n <= crowd_mid triangles also go to the crowded pass
     int crowd_depth;  // k_texels: bbox cover (x tile area) above which a long list goes to the crowded pass
+    int crowd_wide;   // crowded pass with HV_FULL_WARPS-warp CTAs (full-frustum z-buffers), else HV_CROP_WARPS
     unsigned long long* check;  // GM_CHECK builds: violation counters (GM_CHK_*), nullptr = off
 };
 
@@ -980,22 +995,46 @@ extern "C" int gm_plan_create(int device, gm_plan** out) {
 
 // Kernel attributes and the plan's fixed device buffers (gm_plan_create).
 static int plan_init(gm_plan* p) {
-    CK(cudaFuncSetAttribute(k_texels<false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
-    CK(cudaFuncSetAttribute(k_texels_crowded<false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_DYN_SMEM));
+CK(cudaFuncSetAttribute(k_texels<false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels_crowded<false, false, false, HV_CROP_WARPS, HV_CROP_SEL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)sizeof(HeavySmem<HV_CROP_WARPS, HV_CROP_SEL>)));
+    CK(cudaFuncSetAttribute(k_texels_crowded<false, false, false, HV_FULL_WARPS, HV_FULL_SEL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)sizeof(HeavySmem<HV_FULL_WARPS, HV_FULL_SEL>)));
     CK(cudaFuncSetAttribute(k_texels<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
-    CK(cudaFuncSetAttribute(k_texels_crowded<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels_crowded<false, false, true, HV_CROP_WARPS, HV_CROP_SEL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)sizeof(HeavySmem<HV_CROP_WARPS, HV_CROP_SEL>)));
+    CK(cudaFuncSetAttribute(k_texels_crowded<false, false, true, HV_FULL_WARPS, HV_FULL_SEL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)sizeof(HeavySmem<HV_FULL_WARPS, HV_FULL_SEL>)));
     CK(cudaFuncSetAttribute(k_texels<false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
-    CK(cudaFuncSetAttribute(k_texels_crowded<false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels_crowded<false, true, false, HV_CROP_WARPS, HV_CROP_SEL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)sizeof(HeavySmem<HV_CROP_WARPS, HV_CROP_SEL>)));
+    CK(cudaFuncSetAttribute(k_texels_crowded<false, true, false, HV_FULL_WARPS, HV_FULL_SEL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)sizeof(HeavySmem<HV_FULL_WARPS, HV_FULL_SEL>)));
     CK(cudaFuncSetAttribute(k_texels<false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
-    CK(cudaFuncSetAttribute(k_texels_crowded<false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels_crowded<false, true, true, HV_CROP_WARPS, HV_CROP_SEL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)sizeof(HeavySmem<HV_CROP_WARPS, HV_CROP_SEL>)));
+    CK(cudaFuncSetAttribute(k_texels_crowded<false, true, true, HV_FULL_WARPS, HV_FULL_SEL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)sizeof(HeavySmem<HV_FULL_WARPS, HV_FULL_SEL>)));
     CK(cudaFuncSetAttribute(k_texels<true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
-    CK(cudaFuncSetAttribute(k_texels_crowded<true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels_crowded<true, false, false, HV_CROP_WARPS, HV_CROP_SEL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)sizeof(HeavySmem<HV_CROP_WARPS, HV_CROP_SEL>)));
+    CK(cudaFuncSetAttribute(k_texels_crowded<true, false, false, HV_FULL_WARPS, HV_FULL_SEL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)sizeof(HeavySmem<HV_FULL_WARPS, HV_FULL_SEL>)));
     CK(cudaFuncSetAttribute(k_texels<true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
-    CK(cudaFuncSetAttribute(k_texels_crowded<true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels_crowded<true, false, true, HV_CROP_WARPS, HV_CROP_SEL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)sizeof(HeavySmem<HV_CROP_WARPS, HV_CROP_SEL>)));
+    CK(cudaFuncSetAttribute(k_texels_crowded<true, false, true, HV_FULL_WARPS, HV_FULL_SEL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)sizeof(HeavySmem<HV_FULL_WARPS, HV_FULL_SEL>)));
     CK(cudaFuncSetAttribute(k_texels<true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
-    CK(cudaFuncSetAttribute(k_texels_crowded<true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels_crowded<true, true, false, HV_CROP_WARPS, HV_CROP_SEL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)sizeof(HeavySmem<HV_CROP_WARPS, HV_CROP_SEL>)));
+    CK(cudaFuncSetAttribute(k_texels_crowded<true, true, false, HV_FULL_WARPS, HV_FULL_SEL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)sizeof(HeavySmem<HV_FULL_WARPS, HV_FULL_SEL>)));
     CK(cudaFuncSetAttribute(k_texels<true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
-    CK(cudaFuncSetAttribute(k_texels_crowded<true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels_crowded<true, true, true, HV_CROP_WARPS, HV_CROP_SEL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)sizeof(HeavySmem<HV_CROP_WARPS, HV_CROP_SEL>)));
+    CK(cudaFuncSetAttribute(k_texels_crowded<true, true, true, HV_FULL_WARPS, HV_FULL_SEL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)sizeof(HeavySmem<HV_FULL_WARPS, HV_FULL_SEL>)));
     CK(cudaMalloc(&p->d_max, sizeof(unsigned long long)));
     CK(cudaMalloc(&p->d_stats, GM_STAT_STRIPES * GM_STAT_N * sizeof(unsigned long long)));
     CK(cudaMemset(p->d_stats, 0, GM_STAT_STRIPES * GM_STAT_N * sizeof(unsigned long long)));
@@ -1331,8 +1370,15 @@ static int launch_texels(gm_plan* p, cudaStream_t s, const TriStore& ts, DepthVi
     const dim3 grid((unsigned)tiles_x, (unsigned)((tiles_y + TW_WARPS - 1) / TW_WARPS), (unsigned)(items / tiles_per_fix));
     k_texels<ATTRS, STATS, EXACT><<<grid, TW_WARPS * 32, TX_DYN_SMEM, s>>>(ts, dv, cb, tiles_x, tiles_per_fix,
                                                                        tiles_y, fix, b0);
-    k_texels_crowded<ATTRS, STATS, EXACT><<<p->sms * HV_MINB, HV_WARPS * 32, TC_DYN_SMEM, s>>>(
-        ts, dv, cb, tiles_x, tiles_per_fix, fix, b0);
+    if (dv.crowd_wide) {  // full-frustum batches and the raster API: few, long tiles
+        k_texels_crowded<ATTRS, STATS, EXACT, HV_FULL_WARPS, HV_FULL_SEL>
+            <<<p->sms * (24 / HV_FULL_WARPS), HV_FULL_WARPS * 32, (int)sizeof(HeavySmem<HV_FULL_WARPS, HV_FULL_SEL>),
+               s>>>(ts, dv, cb, tiles_x, tiles_per_fix, fix, b0);
+    } else {
+        k_texels_crowded<ATTRS, STATS, EXACT, HV_CROP_WARPS, HV_CROP_SEL>
+            <<<p->sms * (24 / HV_CROP_WARPS), HV_CROP_WARPS * 32, (int)sizeof(HeavySmem<HV_CROP_WARPS, HV_CROP_SEL>),
+               s>>>(ts, dv, cb, tiles_x, tiles_per_fix, fix, b0);
+    }
     CK(cudaGetLastError());
     return GM_OK;
 }
@@ -1365,6 +1411,7 @@ static int enqueue_batch(gm_plan* p, const GmFixExact* d_fix, const GmFixCull* d
     // the persistent crowded pass is slower for them (unfiltered C2 +6%)
     dv.crowd_mid = cfg->filtering ? CROWD_MID : 0;
     dv.crowd_depth = cfg->filtering ? CROWD_DEPTH_CROP : CROWD_DEPTH;
+    dv.crowd_wide = cfg->filtering ? 0 : 1;
     dv.tiles_x = (W + TW - 1) / TW;
     dv.tiles_per_fix = dv.tiles_x * ((H + TH - 1) / TH);
     if (ev) CK(cudaEventRecord(ev[0], s));
@@ -2005,6 +2052,7 @@ static int raster_pass(gm_plan* p, int W, int H, bool attrs) {
     TriStore ts{p->d_tris, p->d_t32, p->d_bbox, p->d_count, p->cap_seg, p->d_fail, p->d_maxcount, p->d_ntris};
     const int tiles_x = (W + TW - 1) / TW, tiles_y = (H + TH - 1) / TH;
     DepthView dv{p->d_depth, p->d_mask, W, H, wwords, nullptr, p->d_vbuf, attrs ? p->d_key : nullptr};
+    dv.crowd_wide = 1;  // every texel is marked: long tiles, many rounds each
     k_mark_all<<<blocks_for((int64_t)H * wwords, 256), 256, 0, s>>>(p->d_mask, W, H, wwords);
     CoarseBins cbins = coarse_bins(p, W, H);
     k_coarse<<<1, 256, 0, s>>>(ts, cbins, p->d_fail, 0, nullptr);

@@ -18,19 +18,32 @@ struct __align__(16) TexelWarpSmem {
     float key[TW_SEL + 32];  // -inv_minw of sel[] (sort key: ascending min depth)
 };
 #define TX_DYN_SMEM (TW_WARPS * (int)sizeof(TexelWarpSmem))
-#ifndef HV_WARPS
-#define HV_WARPS 8      // warps per CTA of the crowded pass (the tile's rounds of texels are shared out)
+// Crowded pass: one CTA of NW warps per tile; SELN overlap-list entries are
+// gathered + sorted per pass (longer lists: several passes).  Crop-frustum
+// (filtering) batches: 2 warps -- their crowded tiles are many and deep (C5:
+// every tile), so the GPU is full either way and small CTAs waste the least at
+// barriers (C2 texels -3%, C5 -11% against one warp per tile).  Full-frustum
+// batches: 8 warps -- only ~7 tiles per fixation hold marked texels and the
+// long lists (up to ~3,000 triangles over distant props) made a few serial
+// tiles the whole launch; spreading a tile's rounds over 8 warps cut unfiltered
+// C2 texels 398 -> 105 ms.
+#ifndef HV_CROP_WARPS
+#define HV_CROP_WARPS 2
 #endif
-#ifndef HV_MINB
-#define HV_MINB 3       // resident crowded-pass CTAs per SM the register budget is sized for
+#ifndef HV_CROP_SEL
+#define HV_CROP_SEL 1024
 #endif
-#ifndef HV_SEL
-#define HV_SEL 2048     // crowded tiles: overlap list gathered + sorted per pass (longer lists: several passes)
+#ifndef HV_FULL_WARPS
+#define HV_FULL_WARPS 8
 #endif
+#ifndef HV_FULL_SEL
+#define HV_FULL_SEL 2048
+#endif
+template <int NW, int SELN>
 struct __align__(16) HeavySmem {
-    TriF32 t32[HV_WARPS][32];  // each warp's staging slice
-    int sel[HV_SEL + 4];       // sorted segment indices; [HV_SEL]: pass count, [+1]: tile max, [+2]: claimed item
-    float key[HV_SEL];         // -inv_minw of sel[] (sort key: ascending min depth)
+    TriF32 t32[NW][32];    // each warp's staging slice
+    int sel[SELN + 4];     // sorted segment indices; [SELN]: pass count, [+1]: tile max, [+2]: claimed item
+    float key[SELN];       // -inv_minw of sel[] (sort key: ascending min depth)
 };
 #ifndef CROWD_DEPTH
 #define CROWD_DEPTH 10  // ... and whose triangle bboxes cover the tile more than this many times
@@ -42,12 +55,11 @@ struct __align__(16) HeavySmem {
 #define CROWD_MID 128  // ... and, in crop-frustum batches, tiles overlapping TW_CAP < n <= this many triangles
 #endif
 #ifndef CROWD_ALL
-#define CROWD_ALL 0  // 1: every tile with more than TW_CAP overlapping triangles goes to the crowded pass
+#define CROWD_ALL 1  // every tile with more than TW_CAP overlapping triangles goes to the crowded pass
 #endif
 #ifndef CROWD_MIN
 #define CROWD_MIN 128  // tiles overlapping more triangles than this go to the crowded pass
 #endif
-#define TC_DYN_SMEM ((int)sizeof(HeavySmem))
 #define TX_MAX_THREADS (32 * TW_WARPS)
 
 // position of the k-th (0-based) set bit of w (k < popc(w))
@@ -93,7 +105,7 @@ template <bool ATTRS, bool STATS, bool CROWDED, bool EXACT>
 __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __restrict__ SEL, float* __restrict__ KEY,
                                            int f, int tx, int ty, const TriStore& ts, const DepthView& dv,
                                            const CoarseBins& cb, int tiles_x, int tiles_per_fix,
-                                           const GmFixExact* __restrict__ fixes) {
+                                           const GmFixExact* __restrict__ fixes, int sel_cap = 0) {
     const int lane = threadIdx.x & 31;
     const int64_t item = (int64_t)f * tiles_per_fix + ty * tiles_x + tx;
     const int W = dv.W, H = dv.H;
@@ -550,15 +562,15 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
             }
         }
     } else {
-        // crowded tile, one CTA (HV_WARPS warps) per tile: the CTA gathers the whole
-        // overlap list (HV_SEL entries per pass), sorts it by ascending min depth (then
+        // crowded tile, one CTA (NW warps) per tile: the CTA gathers the whole
+        // overlap list (sel_cap entries per pass), sorts it by ascending min depth (then
         // segment index) in shared memory, and its warps take the tile's rounds of 32
         // marked texels; each walks the sorted list, staging 32 float32 forms at a time
         // into its own slice.  The nearest certain cover proves (V) every later
         // triangle hidden, so a round usually ends after the first chunks -- nested
         // surfaces cost one sort, not one pass each; rounds run side by side.
         const int tid = threadIdx.x, warp = tid >> 5, nthr = blockDim.x;
-        int* s_cnt = SEL + HV_SEL;  // scalar slot after the arrays
+        int* s_cnt = SEL + sel_cap;  // scalar slot after the arrays
         float* vb = dv.vbuf + (int64_t)f * W * H;
         bool first = true;
         do {
@@ -590,7 +602,7 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
                 cursor += nthr;
                 __syncthreads();
                 cnt = *s_cnt;
-                if (cursor >= n || cnt > HV_SEL - nthr) break;
+                if (cursor >= n || cnt > sel_cap - nthr) break;
                 __syncthreads();  // every thread has read the count before the next block adds to it
             }
             if (STATS) nsel_total += cnt;
@@ -601,7 +613,7 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
                 SEL[k] = INT_MAX;
             }
             __syncthreads();
-            // CTA bitonic sort of (KEY, SEL) ascending, P <= HV_SEL
+            // CTA bitonic sort of (KEY, SEL) ascending, P <= sel_cap
             for (int size = 2; size <= P; size <<= 1) {
                 for (int stride = size >> 1; stride > 0; stride >>= 1) {
                     for (int t = tid; t < (P >> 1); t += nthr) {
@@ -675,7 +687,7 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
         if (!CROWDED) {
             if (lane == 0) dv.tmax[item] = __int_as_float(m);
         } else {  // every warp of the CTA holds a share of the tile's texels
-            int* s_max = SEL + HV_SEL + 1;
+            int* s_max = SEL + sel_cap + 1;
             if (threadIdx.x == 0) *s_max = __float_as_int(-CUDART_INF_F);
             __syncthreads();
             if (lane == 0) atomicMax(s_max, m);
@@ -717,19 +729,19 @@ __global__ void TX_BOUNDS k_texels(TriStore ts, DepthView dv, CoarseBins cb, int
                                                blockIdx.x, ty, ts, dv, cb, tiles_x, tiles_per_fix, fixes);
 }
 
-// Crowded pass: persistent CTAs of HV_WARPS warps over the tiles the first
-// pass deferred, one tile per CTA at a time (texel_item, CROWDED branch).
-template <bool ATTRS, bool STATS, bool EXACT>
-__global__ void __launch_bounds__(HV_WARPS * 32, HV_MINB) k_texels_crowded(TriStore ts, DepthView dv, CoarseBins cb,
-                                                                          int tiles_x, int tiles_per_fix,
-                                                                          const GmFixExact* __restrict__ fixes,
-                                                                          long long b0) {
+// Crowded pass: persistent CTAs of NW warps over the tiles the first pass
+// deferred, one tile per CTA at a time (texel_item, CROWDED branch).
+template <bool ATTRS, bool STATS, bool EXACT, int NW, int SELN>
+__global__ void __launch_bounds__(NW * 32, 24 / NW) k_texels_crowded(TriStore ts, DepthView dv, CoarseBins cb,
+                                                                     int tiles_x, int tiles_per_fix,
+                                                                     const GmFixExact* __restrict__ fixes,
+                                                                     long long b0) {
     extern __shared__ __align__(16) unsigned char tx_dyn[];
-    HeavySmem& C = *reinterpret_cast<HeavySmem*>(tx_dyn);
+    HeavySmem<NW, SELN>& C = *reinterpret_cast<HeavySmem<NW, SELN>*>(tx_dyn);
     const int warp = threadIdx.x >> 5;
     if (*ts.fail <= b0) return;
     const int n_crowd = *dv.crowd_count;
-    int* claim = C.sel + HV_SEL + 2;
+    int* claim = C.sel + SELN + 2;
     for (;;) {
         if (threadIdx.x == 0) *claim = atomicAdd(dv.crowd_count + 1, 1);
         __syncthreads();
@@ -739,6 +751,6 @@ __global__ void __launch_bounds__(HV_WARPS * 32, HV_MINB) k_texels_crowded(TriSt
         const int item = dv.crowd[w];
         const int f = item / tiles_per_fix, tile = item - f * tiles_per_fix;
         texel_item<ATTRS, STATS, true, EXACT>(C.t32[warp], C.sel, C.key, f, tile % tiles_x, tile / tiles_x, ts, dv,
-                                              cb, tiles_x, tiles_per_fix, fixes);
+                                              cb, tiles_x, tiles_per_fix, fixes, SELN);
     }
 }

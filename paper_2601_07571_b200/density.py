@@ -74,11 +74,18 @@ class DensityMap:
     normalized: bool = False
 
     def __getattribute__(self, name):
-        if name == "values":
+        if name == "values" or name == "global_max":
             link = object.__getattribute__(self, "__dict__").get("_device_link")
             if link is not None:
-                link.expose(self)
+                link.expose(self) if name == "values" else link.flush()
         return object.__getattribute__(self, name)
+
+    def __setattr__(self, name, value):
+        if name == "values" or name == "global_max":
+            link = self.__dict__.get("_device_link")
+            if link is not None:  # a caller overwriting the map: settle the queued fixations first
+                link.expose(self)
+        object.__setattr__(self, name, value)
 
     @classmethod
     def zeros(cls, sampled_meshes: dict) -> "DensityMap":
@@ -444,23 +451,46 @@ def generate(scene, sampled_meshes: dict, fixations, config: GenerationConfig, w
 
 class _DeviceLink:
     """Ties a DensityMap to the ScenePlan whose device accumulator holds its
-    values, so a loop of accumulate_fixation calls moves one scalar (the
-    running max) per call instead of the whole map both ways.
+    values, so a loop of accumulate_fixation calls runs as batched generation:
 
-    * device_ahead: the plan holds newer values than the host arrays; any read
-      of `dmap.values` copies them back into those arrays (in place) first.
-    * exposed: `dmap.values` was handed out since the last upload, so the caller
-      may have edited the arrays: the next accumulate_fixation re-uploads them.
-    The plan remembers its owner link; before the plan's accumulator is used for
-    anything else (generate, another map) the owner's values are read back."""
+    * pending: fixations accepted by accumulate_fixation (validated on the host
+      at the call, like the reference raises there) and not yet run; they run
+      in log order, in batches, when PENDING_MAX are queued or when the map is
+      observed -- reading `dmap.values` or `dmap.global_max`, or any other use
+      of the plan.  The running max (reference density.py:180-194) is the max of
+      the final values, since values only grow.
+    * device_ahead: the plan holds newer values than the host arrays; reading
+      `dmap.values` copies them back into those arrays (in place) first.
+    * exposed: `dmap.values` was handed out since the last upload, so the
+      caller may have edited the arrays: the next call re-uploads them.
+    The plan remembers its owner link; before its accumulator is used for
+    anything else (generate, another map) the owner is settled and read back."""
 
-    def __init__(self, plan: "ScenePlan", dmap: DensityMap):
+    PENDING_MAX = 8192
+
+    def __init__(self, plan: "ScenePlan", dmap: DensityMap, config: GenerationConfig):
         self.plan = plan
         self.dmap_ref = weakref.ref(dmap)
+        self.config = config
+        self.key = _config_key(config)
+        self.pending = []
+        self.timers = None
         self.device_ahead = False
         self.exposed = False
 
+    def flush(self) -> None:
+        if not self.pending:
+            return
+        todo, self.pending = self.pending, []
+        self.plan.accumulate_log(todo, self.config, reset=False, timers=self.timers, _owner_ok=True)
+        self.device_ahead = True
+        dmap = self.dmap_ref()
+        if dmap is not None and any(b > a for a, b in self.plan.slices.values()):
+            d = object.__getattribute__(dmap, "__dict__")
+            d["global_max"] = max(d["global_max"], self.plan.global_max())
+
     def pull(self, dmap: DensityMap | None = None) -> None:
+        self.flush()
         dmap = dmap if dmap is not None else self.dmap_ref()
         if not self.device_ahead or dmap is None:
             self.device_ahead = False
@@ -476,30 +506,44 @@ class _DeviceLink:
         self.exposed = True
 
 
+def _config_key(config: GenerationConfig) -> tuple:
+    return (float(config.theta), float(config.epsilon_abs), float(config.epsilon_rel), int(config.zbuffer_resolution),
+            bool(config.filtering_enabled))
+
+
 def accumulate_fixation(dmap: DensityMap, scene, sampled_meshes: dict, fixation, config: GenerationConfig,
                         cache=None, timers: Timings | None = None, device: int = 0) -> DensityMap:
-    """Add one fixation to `dmap` in place (running max updated), return it.
+    """Add one fixation to `dmap` in place (running max updated), return it
+    (reference density.py:136-200).
 
-    The map's values stay resident on the GPU between calls (_DeviceLink):
-    they are uploaded when the plan does not hold them already or the caller
-    has read `dmap.values` since, and read back when `dmap.values` is next
-    read.  The running max (reference density.py:180-194) is the device max
-    over the included objects, one scalar per call."""
+    The map lives on the GPU while it is being fed (_DeviceLink): consecutive
+    calls queue their fixations and run them as one batched generation when
+    the map is next observed, so a loop over a log costs about one `generate`.
+    A fixation whose crop frustum is degenerate raises InvalidFrustumError at
+    its own call, as in the reference.  `timers` phases are recorded when the
+    queued batch runs."""
+    config.validate()
     plan = cache if isinstance(cache, ScenePlan) else get_plan(scene, sampled_meshes, config, device)
+    from .gaze import fixation_setup
+
+    fixation_setup([fixation], config.theta, config.filtering_enabled, config.zbuffer_resolution)  # raises here
     d = object.__getattribute__(dmap, "__dict__")
     link = d.get("_device_link")
-    if link is None or link.plan is not plan or plan._owner is not link or link.exposed:
+    if (link is None or link.plan is not plan or plan._owner is not link or link.exposed
+            or link.key != _config_key(config)):
         if link is not None:
             link.pull(dmap)
         plan.release()
         plan.write(plan.gather(d["values"]))
-        link = _DeviceLink(plan, dmap)
+        link = _DeviceLink(plan, dmap, config)
         d["_device_link"] = link
         plan._owner = link
-    plan.accumulate_log([fixation], config, reset=False, timers=timers, _owner_ok=True)
-    link.device_ahead = True
-    if plan.slices and any(b > a for a, b in plan.slices.values()):
-        dmap.global_max = max(dmap.global_max, plan.global_max())
+    link.config = config
+    if timers is not None:
+        link.timers = timers
+    link.pending.append(fixation)
+    if len(link.pending) >= link.PENDING_MAX:
+        link.flush()
     return dmap
 
 
