@@ -56,7 +56,8 @@ STAT_NAMES = ["l1_tests", "l2_tests", "exact_evals", "ndc_candidates", "cone_can
               "tx_chunked", "tx_chunked_pairs", "tx_chunked_texels", "bbox_px"]
 
 CHECK_NAMES = ["tx_texels", "tx_bound_wrong", "tx_winner_wrong", "cand_pairs", "cand_l1_wrong", "cand_l3_wrong",
-               "mask_wrong", "depth_tests", "depth_wrong", "tileocc_wrong"] + [f"reserved{i}" for i in range(6)]
+               "mask_wrong", "depth_tests", "depth_wrong", "tileocc_wrong", "cull_tris", "cull_texels",
+               "cull_wrong"] + [f"reserved{i}" for i in range(3)]
 
 PROGRESS_FN = ctypes.CFUNCTYPE(None, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p)
 

@@ -285,8 +285,9 @@ struct __align__(16) TriF32 {
     float wx, wy;                    // bbox extent x1 - x0 + 1, y1 - y0 + 1: pixel centre c = (px + 0.5,
                                      // py + 0.5) is in the bbox iff 0 < c - o < w (exact in float32)
     int gidx;                        // index of the float64 record in the fixation's segment
-    int pad;
+    int pad[2];                      // (explicit: every byte of the 96 is written and copied)
 };  // 96 B
+static_assert(sizeof(TriF32) == 96, "TriF32 is six 16-byte words");
 
 __device__ __forceinline__ void make_tri_f32(const GmScreenTri& T, int gidx, TriF32& o) {
     const double ox = T.x0, oy = T.y0;
@@ -325,7 +326,7 @@ __device__ __forceinline__ void make_tri_f32(const GmScreenTri& T, int gidx, Tri
     o.wx = (float)(T.x1 - T.x0 + 1);
     o.wy = (float)(T.y1 - T.y0 + 1);
     o.gidx = gidx;
-    o.pad = 0;
+    o.pad[0] = o.pad[1] = 0;
 }
 
 struct TriStore {
@@ -585,6 +586,9 @@ enum {
     GM_CHK_DEPTH_TESTS = 7,      // depth tests checked in k_samples
     GM_CHK_DEPTH_WRONG = 8,      // depth_test_iv (bounds) != the reference test on exact texel depths
     GM_CHK_TILEOCC_WRONG = 9,    // tile-max occlusion said "occluded" but the exact test passes
+    GM_CHK_CULL_TRIS = 10,       // occluder triangles the cone cull dropped, projected exactly anyway
+    GM_CHK_CULL_TEXELS = 11,     // marked texels inside those triangles' pixel bboxes, tested
+    GM_CHK_CULL_WRONG = 12,      // ... where a dropped triangle is nearer than the stored texel (it would have won)
     GM_CHK_N = 16
 };
 __device__ __forceinline__ void chk_add(unsigned long long* c, int idx, unsigned long long v) {
@@ -732,6 +736,62 @@ __device__ __forceinline__ bool occluded_by_tiles(const DepthView& dv, int f, in
     const double mm = (double)m;
     return (d - mm) - eps > 1e-12 * (fabs(d) + eps + mm);
 }
+
+#ifdef GM_CHECK
+// Self-check of the occluder cone cull (GM_CHECK builds): every triangle
+// k_tri_setup dropped (cluster or triangle sphere test) is projected exactly
+// anyway; at each marked texel inside its pixel bbox its exact depth must not be
+// nearer than the depth k_texels stored there (else the cull changed a texel a
+// depth test reads).  Runs after k_texels, before k_samples.
+__global__ void __launch_bounds__(TS_WARPS * 32) k_check_cull(const double* __restrict__ tw, int64_t T,
+                                                    const float4* __restrict__ tsph, const float4* __restrict__ csph,
+                                                    int64_t n_clu, const GmFixExact* __restrict__ fixes,
+                                                    const GmFixCull* __restrict__ culls, int W, int H, TriStore ts,
+                                                    DepthView dv, long long b0) {
+    if (*ts.fail <= b0) return;
+    const int f = blockIdx.y;
+    const int lane = threadIdx.x & 31;
+    const int64_t c0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32;
+    if (c0 >= n_clu) return;
+    const GmFixCull cull = culls[f];
+    const GmFixExact& F = fixes[f];
+    const GmScreenTri* seg = ts.tris + (int64_t)f * ts.cap_seg;
+    const uint32_t* mask = dv.mask + (int64_t)f * H * dv.wwords;
+    const int* win = dv.win + (int64_t)f * W * H;
+    unsigned long long n_tri = 0, n_tex = 0, n_bad = 0;
+    for (int c = 0; c < 32; c++) {
+        const int64_t clu = c0 + c;
+        if (clu >= n_clu) break;
+        const bool clu_pass = sphere_visible(cull, csph[clu], true);
+        const int64_t t = clu * 32 + lane;
+        if (t >= T || (clu_pass && sphere_visible(cull, tsph[t], true))) continue;  // kept by the cull
+        GmScreenTri out[2];
+        const int n = project_triangle(tw + 9 * t, F, W, H, out);
+        n_tri++;
+        for (int q = 0; q < n; q++) {
+            const GmScreenTri& S = out[q];
+            for (int y = S.y0; y <= S.y1; y++)
+                for (int w0 = S.x0 >> 5; w0 <= (S.x1 >> 5); w0++) {
+                    uint32_t bits = mask[(int64_t)y * dv.wwords + w0];
+                    while (bits) {
+                        const int x = w0 * 32 + __ffs(bits) - 1;
+                        bits &= bits - 1;
+                        if (x < S.x0 || x > S.x1) continue;
+                        const double d = texel_depth(S, x, y, F.near_, F.far_);
+                        if (!(d < CUDART_INF)) continue;
+                        n_tex++;
+                        const int wr = win[(int64_t)y * W + x];
+                        const double stored = wr >= 0 ? texel_depth(seg[wr], x, y, F.near_, F.far_) : CUDART_INF;
+                        if (d < stored) n_bad++;
+                    }
+                }
+        }
+    }
+    chk_add(dv.check, GM_CHK_CULL_TRIS, n_tri);
+    chk_add(dv.check, GM_CHK_CULL_TEXELS, n_tex);
+    chk_add(dv.check, GM_CHK_CULL_WRONG, n_bad);
+}
+#endif
 
 #include "gm_samples.cuh"
 
@@ -1451,6 +1511,13 @@ static int enqueue_batch(gm_plan* p, const GmFixExact* d_fix, const GmFixCull* d
                       ? launch_texels<false, true, false>(p, s, ts, dv, cbins, tiles_x, tiles_x * tiles_y, items, d_fix, b0)
                       : launch_texels<false, false, false>(p, s, ts, dv, cbins, tiles_x, tiles_x * tiles_y, items, d_fix, b0);
         if (trc) return trc;
+#ifdef GM_CHECK
+        if (p->n_clu > 0) {
+            dim3 grid(blocks_for((p->n_clu + 31) / 32, TS_WARPS), nb);
+            k_check_cull<<<grid, TS_WARPS * 32, 0, s>>>(p->d_tw, p->T, p->d_tsph, p->d_csph, p->n_clu, d_fix, d_cull, W,
+                                                       H, ts, dv, b0);
+        }
+#endif
         if (ev) CK(cudaEventRecord(ev[3], s));
         // accumulation passes run in batch order across the two streams (log order per sample)
         CK(cudaStreamWaitEvent(s, p->ev_order, 0));

@@ -11,6 +11,7 @@ fixation log order, so results are deterministic run to run.
 
 from __future__ import annotations
 
+import atexit
 import ctypes
 import os
 import math
@@ -381,6 +382,19 @@ class ScenePlan:
 
 _PLANS: dict = {}
 _PLAN_LIMIT = 4
+
+
+def release_plans() -> None:
+    """Destroy the cached ScenePlans (their device buffers are freed now, not at
+    interpreter teardown, which CUDA may already have begun).  Runs at exit."""
+    plans = list(_PLANS.values())
+    _PLANS.clear()
+    for plan in plans:
+        plan.release()
+        plan.__del__()
+
+
+atexit.register(release_plans)
 
 
 def get_plan(scene, sampled_meshes: dict, config: GenerationConfig, device: int = 0) -> ScenePlan:
