@@ -4,7 +4,9 @@
 // survivors (kernels.py:67-137), and the sorted pass for crowded tiles.
 #pragma once
 
-#define TW_CAP 32
+#ifndef TW_CAP
+#define TW_CAP 64  // triangles staged by the first pass (a multiple of 32); longer lists go to the crowded pass
+#endif
 #ifndef RANK_SORT_MAX
 #define RANK_SORT_MAX 16  // staged lists up to this long are ordered by rank counting, longer by bitonic sort
 #endif
@@ -191,6 +193,40 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
     // position), one shuffle per entry; long ones: 32-wide bitonic network.
     auto stage = [&](int c0, int kend) {
         __syncwarp();
+        if (TW_CAP > 32 && kend > 32) {  // TW_CAP / 32 entries per lane (lane + 32 m), ranks by counting
+            constexpr int E = TW_CAP / 32;
+            int gm_[E], rk[E];
+            float km[E];
+#pragma unroll
+            for (int m = 0; m < E; m++) {
+                const bool h = lane + 32 * m < kend;
+                gm_[m] = h ? SEL[c0 + lane + 32 * m] : 0;
+                km[m] = h ? KEY[c0 + lane + 32 * m] : CUDART_INF_F;
+                rk[m] = 0;
+            }
+#pragma unroll
+            for (int ms = 0; ms < E; ms++) {
+                if (32 * ms >= kend) break;
+                const int jn = min(32, kend - 32 * ms);
+                for (int jl = 0; jl < jn; jl++) {
+                    const float kj = __shfl_sync(FULL, km[ms], jl);
+#pragma unroll
+                    for (int m = 0; m < E; m++)  // entry j = 32 ms + jl sorts before entry 32 m + lane?
+                        rk[m] += (kj < km[m] || (kj == km[m] && (ms < m || (ms == m && jl < lane)))) ? 1 : 0;
+                }
+            }
+#pragma unroll
+            for (int m = 0; m < E; m++) {
+                if (lane + 32 * m < kend) {
+                    const uint4* fr = reinterpret_cast<const uint4*>(segf + gm_[m]);
+                    uint4* to = reinterpret_cast<uint4*>(&T32[rk[m]]);
+#pragma unroll
+                    for (int part = 0; part < 6; part++) to[part] = fr[part];
+                }
+            }
+            __syncwarp();
+            return;
+        }
         const int gi = lane < kend ? SEL[c0 + lane] : 0;
         float key = lane < kend ? KEY[c0 + lane] : CUDART_INF_F;
         int dst, src;
