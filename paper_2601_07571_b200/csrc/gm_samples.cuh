@@ -107,9 +107,6 @@ __global__ void k_fix32(const GmFixExact* __restrict__ ex, int nb, double pmax, 
 // decide (samples within ~E of the camera plane).  dlo: lower bound of the
 // exact depth w (GM_F32_BLOCK; up to float64 rounding).
 enum { GM_F32_REJECT = 0, GM_F32_BLOCK = 1, GM_F32_EXACT = 2 };
-#ifndef KM_AGG
-#define KM_AGG 0  // > 0: warp-aggregated mask marking when the warp's blocks span <= KM_AGG mask words
-#endif
 __device__ __forceinline__ int mark_f32(const GmFixF32& Q, float wx, float wy, float wz, int W, int H, int& cxlo,
                                         int& cxhi, int& cylo, int& cyhi, double& dlo) {
     const float Wf = (float)W, Hf = (float)H;
@@ -208,83 +205,44 @@ __global__ void KM_BOUNDS k_mark(const float* __restrict__ pxf, const float* __r
             while (mask) {
                 const int j = __ffs(mask) - 1;
                 mask &= mask - 1;
+                if (!valid) continue;
                 const int f = g + j;
-                bool cand = false;
-                int bx0 = 0, bx1 = -1, by0 = 0, by1 = -1;
-                if (valid) {
-                    int cxlo, cxhi, cylo, cyhi;
-                    double dlo;
-                    int st = mark_f32(fix32[f], wx, wy, wz, W, H, cxlo, cxhi, cylo, cyhi, dlo);
-                    if (st == GM_F32_EXACT) {
-                        // the exact float64 test of k_samples, for this lane only
-                        st = GM_F32_REJECT;
-                        const GmFixExact& F = fixes[f];
-                        const double X = px[i], Y = py[i], Z = pz[i];
-                        const double xx = F.rot[0] * X + F.rot[1] * Y + F.rot[2] * Z + F.trans[0];
-                        const double yy = F.rot[3] * X + F.rot[4] * Y + F.rot[5] * Z + F.trans[1];
-                        const double zz = F.rot[6] * X + F.rot[7] * Y + F.rot[8] * Z + F.trans[2];
-                        const double ww = -zz;
-                        if (!(ww <= 0.0 || ww < F.near_lo || ww > F.far_hi)) {
-                            const double ndx = (F.p00 * xx + F.p02 * zz) / ww, ndy = (F.p11 * yy + F.p12 * zz) / ww;
-                            const double l = -1.0 - GM_NDC_SLACK, h = 1.0 + GM_NDC_SLACK;
-                            if (!(ndx < l || ndx > h || ndy < l || ndy > h)) {
-                                const double d1 = xx * F.gaze[0] + yy * F.gaze[1] + zz * F.gaze[2];
-                                double d2sq = xx * xx + yy * yy + zz * zz - d1 * d1;
-                                if (d2sq < 0.0) d2sq = 0.0;
-                                if (d1 > 0.0 && !(d2sq * inv_sigma * inv_sigma / (d1 * d1) > 16.0)) {
-                                    const double gxe = (ndx + 1.0) * 0.5 * (double)W - 0.5;
-                                    const double gye = (1.0 - ndy) * 0.5 * (double)H - 0.5;
-                                    long long rx = x86_i64(rint(gxe)), ry = x86_i64(rint(gye));
-                                    cxlo = cxhi = (int)max(min(rx, (long long)W - 1), 0LL);
-                                    cylo = cyhi = (int)max(min(ry, (long long)H - 1), 0LL);
-                                    st = GM_F32_BLOCK;
-                                }
-                            }
-                        }
-                    }
-                    if (st == GM_F32_BLOCK) {
-                        cand = true;
-                        bx0 = max(cxlo - 1, 0);
-                        bx1 = min(cxhi + 1, W - 1);
-                        by0 = max(cylo - 1, 0);
-                        by1 = min(cyhi + 1, H - 1);
-                    }
+                int cxlo, cxhi, cylo, cyhi;
+                double dlo;
+                const int st = mark_f32(fix32[f], wx, wy, wz, W, H, cxlo, cxhi, cylo, cyhi, dlo);
+                if (st == GM_F32_REJECT) continue;
+                if (st == GM_F32_EXACT) {
+                    // the exact float64 test of k_samples, for this lane only
+                    const GmFixExact& F = fixes[f];
+                    const double X = px[i], Y = py[i], Z = pz[i];
+                    const double xx = F.rot[0] * X + F.rot[1] * Y + F.rot[2] * Z + F.trans[0];
+                    const double yy = F.rot[3] * X + F.rot[4] * Y + F.rot[5] * Z + F.trans[1];
+                    const double zz = F.rot[6] * X + F.rot[7] * Y + F.rot[8] * Z + F.trans[2];
+                    const double ww = -zz;
+                    if (ww <= 0.0 || ww < F.near_lo || ww > F.far_hi) continue;
+                    const double ndx = (F.p00 * xx + F.p02 * zz) / ww, ndy = (F.p11 * yy + F.p12 * zz) / ww;
+                    const double l = -1.0 - GM_NDC_SLACK, h = 1.0 + GM_NDC_SLACK;
+                    if (ndx < l || ndx > h || ndy < l || ndy > h) continue;
+                    const double d1 = xx * F.gaze[0] + yy * F.gaze[1] + zz * F.gaze[2];
+                    if (d1 <= 0.0) continue;
+                    double d2sq = xx * xx + yy * yy + zz * zz - d1 * d1;
+                    if (d2sq < 0.0) d2sq = 0.0;
+                    if (d2sq * inv_sigma * inv_sigma / (d1 * d1) > 16.0) continue;
+                    const double gxe = (ndx + 1.0) * 0.5 * (double)W - 0.5, gye = (1.0 - ndy) * 0.5 * (double)H - 0.5;
+                    long long rx = x86_i64(rint(gxe)), ry = x86_i64(rint(gye));
+                    cxlo = cxhi = (int)max(min(rx, (long long)W - 1), 0LL);
+                    cylo = cyhi = (int)max(min(ry, (long long)H - 1), 0LL);
                 }
-                if (!__any_sync(0xffffffffu, cand)) continue;
-                if (cand) my_bits |= 1u << j;
+                const int bx0 = max(cxlo - 1, 0), bx1 = min(cxhi + 1, W - 1);
+                const int by0 = max(cylo - 1, 0), by1 = min(cyhi + 1, H - 1);
+                my_bits |= 1u << j;
                 uint32_t* m = dv.mask + (int64_t)f * H * dv.wwords;
-#if KM_AGG
-                // the chunk's 32 samples are neighbours on a surface: when their 3x3 blocks
-                // fall in a few mask words, OR them across the warp and let one lane per
-                // word do the atomic (dense views -- C5's nested shells -- mark each texel
-                // many times over)
-                const int wlo = __reduce_min_sync(0xffffffffu, cand ? (unsigned)(bx0 >> 5) : 0xffffffffu);
-                const int whi = (int)__reduce_max_sync(0xffffffffu, cand ? (unsigned)(bx1 >> 5) : 0u);
-                const int ylo = __reduce_min_sync(0xffffffffu, cand ? (unsigned)by0 : 0xffffffffu);
-                const int yhi = (int)__reduce_max_sync(0xffffffffu, cand ? (unsigned)by1 : 0u);
-                const int nw = whi - wlo + 1, nr = yhi - ylo + 1;
-                if (nw * nr <= KM_AGG) {
-                    for (int yy = ylo; yy <= yhi; yy++)
-                        for (int wq = wlo; wq <= whi; wq++) {
-                            uint32_t b = 0u;
-                            if (cand && yy >= by0 && yy <= by1) {
-                                const int lo = max(bx0, wq * 32), hi = min(bx1, wq * 32 + 31);
-                                if (lo <= hi) b = (uint32_t)(((1ull << (hi - lo + 1)) - 1ull) << (lo & 31));
-                            }
-                            b = __reduce_or_sync(0xffffffffu, b);
-                            if (lane == 0 && b) atomicOr(m + (int64_t)yy * dv.wwords + wq, b);
-                        }
-                    continue;
-                }
-#endif
-                if (cand) {
-                    const unsigned long long bits = ((1ull << (bx1 - bx0 + 1)) - 1ull) << (bx0 & 31);
-                    const int w0 = bx0 >> 5;
-                    for (int yy = by0; yy <= by1; yy++) {
-                        uint32_t* row = m + (int64_t)yy * dv.wwords + w0;
-                        atomicOr(row, (uint32_t)bits);
-                        if (bits >> 32) atomicOr(row + 1, (uint32_t)(bits >> 32));
-                    }
+                const unsigned long long bits = ((1ull << (bx1 - bx0 + 1)) - 1ull) << (bx0 & 31);
+                const int w0 = bx0 >> 5;
+                for (int yy = by0; yy <= by1; yy++) {
+                    uint32_t* row = m + (int64_t)yy * dv.wwords + w0;
+                    atomicOr(row, (uint32_t)bits);
+                    if (bits >> 32) atomicOr(row + 1, (uint32_t)(bits >> 32));
                 }
             }
             // level 3 for the accumulation pass: the fixations of this group with at
