@@ -357,8 +357,15 @@ def _roofline(st, tm1, ms1, batches, pk, clk_mhz):
     texel_flops = 32.0 * st.get("texels", 0)
     texel_tf = texel_flops / t_s / 1e12 if t_s and texel_flops else None
     kern, src = _ncu_kernels()
-    k1 = kern.get("k_texels<0, 0, 0>") or kern.get("k_texels<0, 0, 0, 0>")
-    k2 = kern.get("k_texels_crowded<0, 0, 0>") or kern.get("k_texels<0, 0, 1, 0>")
+    def pick(*prefixes):  # the production instantiation of each pass (template arguments vary by round)
+        for pre in prefixes:
+            for name, v in kern.items():
+                if name.startswith(pre):
+                    return v
+        return None
+
+    k1 = pick("k_texels<0, 0, 0", "k_texels<0, 0, 0, 0>")
+    k2 = pick("k_texels_crowded<0, 0, 0", "k_texels<0, 0, 1, 0>")
     traffic = hbm = issue = None
     if k1:
         traffic = k1["dram_bytes_per_launch"] + (k2["dram_bytes_per_launch"] if k2 else 0.0)

@@ -546,8 +546,16 @@ __global__ void __launch_bounds__(256) k_coarse(TriStore ts, CoarseBins cb, cons
 }
 
 #define TW 32      // k_texels tile width (pixels) = warp lanes
-#ifndef TH
-#define TH 16      // k_texels tile height (pixels), a power of two <= 32
+// k_texels tile heights (pixels, powers of two <= 32): 32 x 32 tiles (the coarse-bin size) in
+// crop-frustum generation batches -- their marked texels are dense around the cone, so twice the
+// texels share a tile's fixed cost (C2 step 239 -> 228 ms, C5 texels 666 -> 603 ms); 32 x 16 in
+// full-frustum batches (few marked texels, long lists: 32-row tiles double unfiltered C2's texels
+// phase) and for the raster API / renderer
+#ifndef TH_CROP
+#define TH_CROP 32
+#endif
+#ifndef TH_FULL
+#define TH_FULL 16
 #endif
 
 struct DepthView {
@@ -568,6 +576,7 @@ struct DepthView {
     int crowd_mid;    // k_texels: lists of TW_CAP < n <= crowd_mid triangles also go to the crowded pass
     int crowd_depth;  // k_texels: bbox cover (x tile area) above which a long list goes to the crowded pass
     int crowd_wide;   // crowded pass with HV_FULL_WARPS-warp CTAs (full-frustum z-buffers), else HV_CROP_WARPS
+    int th_shift;     // log2 of the k_texels tile height of this batch (4: 32 x 16 tiles, 5: 32 x 32)
     unsigned long long* check;  // GM_CHECK builds: violation counters (GM_CHK_*), nullptr = off
 };
 
@@ -725,7 +734,7 @@ __device__ __forceinline__ bool depth_test_iv(const DepthView& dv, const GmScree
 __device__ __forceinline__ bool occluded_by_tiles(const DepthView& dv, int f, int bx0, int bx1, int by0, int by1,
                                                   double d, double eps) {
     const float* tm = dv.tmax + (int64_t)f * dv.tiles_per_fix;
-    const int tx0 = bx0 / TW, tx1 = bx1 / TW, ty0 = by0 / TH, ty1 = by1 / TH;
+    const int tx0 = bx0 / TW, tx1 = bx1 / TW, ty0 = by0 >> dv.th_shift, ty1 = by1 >> dv.th_shift;
     float m = tm[ty0 * dv.tiles_x + tx0];
     if (tx1 != tx0) m = fmaxf(m, tm[ty0 * dv.tiles_x + tx1]);
     if (ty1 != ty0) {
@@ -1055,46 +1064,56 @@ extern "C" int gm_plan_create(int device, gm_plan** out) {
 
 // Kernel attributes and the plan's fixed device buffers (gm_plan_create).
 static int plan_init(gm_plan* p) {
-CK(cudaFuncSetAttribute(k_texels<false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
-    CK(cudaFuncSetAttribute(k_texels_crowded<false, false, false, HV_CROP_WARPS, HV_CROP_SEL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)sizeof(HeavySmem<HV_CROP_WARPS, HV_CROP_SEL>)));
-    CK(cudaFuncSetAttribute(k_texels_crowded<false, false, false, HV_FULL_WARPS, HV_FULL_SEL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)sizeof(HeavySmem<HV_FULL_WARPS, HV_FULL_SEL>)));
-    CK(cudaFuncSetAttribute(k_texels<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
-    CK(cudaFuncSetAttribute(k_texels_crowded<false, false, true, HV_CROP_WARPS, HV_CROP_SEL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)sizeof(HeavySmem<HV_CROP_WARPS, HV_CROP_SEL>)));
-    CK(cudaFuncSetAttribute(k_texels_crowded<false, false, true, HV_FULL_WARPS, HV_FULL_SEL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)sizeof(HeavySmem<HV_FULL_WARPS, HV_FULL_SEL>)));
-    CK(cudaFuncSetAttribute(k_texels<false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
-    CK(cudaFuncSetAttribute(k_texels_crowded<false, true, false, HV_CROP_WARPS, HV_CROP_SEL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)sizeof(HeavySmem<HV_CROP_WARPS, HV_CROP_SEL>)));
-    CK(cudaFuncSetAttribute(k_texels_crowded<false, true, false, HV_FULL_WARPS, HV_FULL_SEL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)sizeof(HeavySmem<HV_FULL_WARPS, HV_FULL_SEL>)));
-    CK(cudaFuncSetAttribute(k_texels<false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
-    CK(cudaFuncSetAttribute(k_texels_crowded<false, true, true, HV_CROP_WARPS, HV_CROP_SEL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)sizeof(HeavySmem<HV_CROP_WARPS, HV_CROP_SEL>)));
-    CK(cudaFuncSetAttribute(k_texels_crowded<false, true, true, HV_FULL_WARPS, HV_FULL_SEL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)sizeof(HeavySmem<HV_FULL_WARPS, HV_FULL_SEL>)));
-    CK(cudaFuncSetAttribute(k_texels<true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
-    CK(cudaFuncSetAttribute(k_texels_crowded<true, false, false, HV_CROP_WARPS, HV_CROP_SEL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)sizeof(HeavySmem<HV_CROP_WARPS, HV_CROP_SEL>)));
-    CK(cudaFuncSetAttribute(k_texels_crowded<true, false, false, HV_FULL_WARPS, HV_FULL_SEL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)sizeof(HeavySmem<HV_FULL_WARPS, HV_FULL_SEL>)));
-    CK(cudaFuncSetAttribute(k_texels<true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
-    CK(cudaFuncSetAttribute(k_texels_crowded<true, false, true, HV_CROP_WARPS, HV_CROP_SEL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)sizeof(HeavySmem<HV_CROP_WARPS, HV_CROP_SEL>)));
-    CK(cudaFuncSetAttribute(k_texels_crowded<true, false, true, HV_FULL_WARPS, HV_FULL_SEL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)sizeof(HeavySmem<HV_FULL_WARPS, HV_FULL_SEL>)));
-    CK(cudaFuncSetAttribute(k_texels<true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
-    CK(cudaFuncSetAttribute(k_texels_crowded<true, true, false, HV_CROP_WARPS, HV_CROP_SEL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)sizeof(HeavySmem<HV_CROP_WARPS, HV_CROP_SEL>)));
-    CK(cudaFuncSetAttribute(k_texels_crowded<true, true, false, HV_FULL_WARPS, HV_FULL_SEL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)sizeof(HeavySmem<HV_FULL_WARPS, HV_FULL_SEL>)));
-    CK(cudaFuncSetAttribute(k_texels<true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
-    CK(cudaFuncSetAttribute(k_texels_crowded<true, true, true, HV_CROP_WARPS, HV_CROP_SEL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)sizeof(HeavySmem<HV_CROP_WARPS, HV_CROP_SEL>)));
-    CK(cudaFuncSetAttribute(k_texels_crowded<true, true, true, HV_FULL_WARPS, HV_FULL_SEL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)sizeof(HeavySmem<HV_FULL_WARPS, HV_FULL_SEL>)));
+    CK(cudaFuncSetAttribute(k_texels<false, false, false, TH_FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels_crowded<false, false, false, HV_CROP_WARPS, HV_CROP_SEL, TH_FULL>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(HeavySmem<HV_CROP_WARPS, HV_CROP_SEL>)));
+    CK(cudaFuncSetAttribute(k_texels_crowded<false, false, false, HV_FULL_WARPS, HV_FULL_SEL, TH_FULL>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(HeavySmem<HV_FULL_WARPS, HV_FULL_SEL>)));
+    CK(cudaFuncSetAttribute(k_texels<false, false, false, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels_crowded<false, false, false, HV_CROP_WARPS, HV_CROP_SEL, 32>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(HeavySmem<HV_CROP_WARPS, HV_CROP_SEL>)));
+    CK(cudaFuncSetAttribute(k_texels_crowded<false, false, false, HV_FULL_WARPS, HV_FULL_SEL, 32>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(HeavySmem<HV_FULL_WARPS, HV_FULL_SEL>)));
+    CK(cudaFuncSetAttribute(k_texels<false, false, true, TH_FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels_crowded<false, false, true, HV_CROP_WARPS, HV_CROP_SEL, TH_FULL>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(HeavySmem<HV_CROP_WARPS, HV_CROP_SEL>)));
+    CK(cudaFuncSetAttribute(k_texels_crowded<false, false, true, HV_FULL_WARPS, HV_FULL_SEL, TH_FULL>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(HeavySmem<HV_FULL_WARPS, HV_FULL_SEL>)));
+    CK(cudaFuncSetAttribute(k_texels<false, true, false, TH_FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels_crowded<false, true, false, HV_CROP_WARPS, HV_CROP_SEL, TH_FULL>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(HeavySmem<HV_CROP_WARPS, HV_CROP_SEL>)));
+    CK(cudaFuncSetAttribute(k_texels_crowded<false, true, false, HV_FULL_WARPS, HV_FULL_SEL, TH_FULL>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(HeavySmem<HV_FULL_WARPS, HV_FULL_SEL>)));
+    CK(cudaFuncSetAttribute(k_texels<false, true, false, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels_crowded<false, true, false, HV_CROP_WARPS, HV_CROP_SEL, 32>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(HeavySmem<HV_CROP_WARPS, HV_CROP_SEL>)));
+    CK(cudaFuncSetAttribute(k_texels_crowded<false, true, false, HV_FULL_WARPS, HV_FULL_SEL, 32>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(HeavySmem<HV_FULL_WARPS, HV_FULL_SEL>)));
+    CK(cudaFuncSetAttribute(k_texels<false, true, true, TH_FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels_crowded<false, true, true, HV_CROP_WARPS, HV_CROP_SEL, TH_FULL>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(HeavySmem<HV_CROP_WARPS, HV_CROP_SEL>)));
+    CK(cudaFuncSetAttribute(k_texels_crowded<false, true, true, HV_FULL_WARPS, HV_FULL_SEL, TH_FULL>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(HeavySmem<HV_FULL_WARPS, HV_FULL_SEL>)));
+    CK(cudaFuncSetAttribute(k_texels<true, false, false, TH_FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels_crowded<true, false, false, HV_CROP_WARPS, HV_CROP_SEL, TH_FULL>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(HeavySmem<HV_CROP_WARPS, HV_CROP_SEL>)));
+    CK(cudaFuncSetAttribute(k_texels_crowded<true, false, false, HV_FULL_WARPS, HV_FULL_SEL, TH_FULL>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(HeavySmem<HV_FULL_WARPS, HV_FULL_SEL>)));
+    CK(cudaFuncSetAttribute(k_texels<true, false, true, TH_FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels_crowded<true, false, true, HV_CROP_WARPS, HV_CROP_SEL, TH_FULL>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(HeavySmem<HV_CROP_WARPS, HV_CROP_SEL>)));
+    CK(cudaFuncSetAttribute(k_texels_crowded<true, false, true, HV_FULL_WARPS, HV_FULL_SEL, TH_FULL>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(HeavySmem<HV_FULL_WARPS, HV_FULL_SEL>)));
+    CK(cudaFuncSetAttribute(k_texels<true, true, false, TH_FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels_crowded<true, true, false, HV_CROP_WARPS, HV_CROP_SEL, TH_FULL>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(HeavySmem<HV_CROP_WARPS, HV_CROP_SEL>)));
+    CK(cudaFuncSetAttribute(k_texels_crowded<true, true, false, HV_FULL_WARPS, HV_FULL_SEL, TH_FULL>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(HeavySmem<HV_FULL_WARPS, HV_FULL_SEL>)));
+    CK(cudaFuncSetAttribute(k_texels<true, true, true, TH_FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize, TX_DYN_SMEM));
+    CK(cudaFuncSetAttribute(k_texels_crowded<true, true, true, HV_CROP_WARPS, HV_CROP_SEL, TH_FULL>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(HeavySmem<HV_CROP_WARPS, HV_CROP_SEL>)));
+    CK(cudaFuncSetAttribute(k_texels_crowded<true, true, true, HV_FULL_WARPS, HV_FULL_SEL, TH_FULL>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(HeavySmem<HV_FULL_WARPS, HV_FULL_SEL>)));
     CK(cudaMalloc(&p->d_max, sizeof(unsigned long long)));
     CK(cudaMalloc(&p->d_stats, GM_STAT_STRIPES * GM_STAT_N * sizeof(unsigned long long)));
     CK(cudaMemset(p->d_stats, 0, GM_STAT_STRIPES * GM_STAT_N * sizeof(unsigned long long)));
@@ -1367,7 +1386,7 @@ static int ensure_batch_set(gm_plan* p, int B, int W, int H, int64_t seg) {
         p->cap_citems = ci;
         p->cap_cB = B;
     }
-    const int64_t n_tiles = (int64_t)B * ((W + TW - 1) / TW) * ((H + TH - 1) / TH);
+    const int64_t n_tiles = (int64_t)B * ((W + TW - 1) / TW) * ((H + TH_FULL - 1) / TH_FULL);  // the smaller tiles
     if (n_tiles > p->cap_crowd) {
         if ((rc = dev_alloc(&p->d_crowd, (size_t)n_tiles))) return rc;
         if ((rc = dev_alloc(&p->d_tmax, (size_t)n_tiles))) return rc;
@@ -1419,6 +1438,27 @@ static CoarseBins coarse_bins(gm_plan* p, int W, int H) {
 
 // k_texels over `items` (fixation, tile) work items, then the crowded tiles the
 // first pass deferred (k_texels<CROWDED>, persistent, larger shared slices).
+template <bool ATTRS, bool STATS, bool EXACT, int TH>
+static void launch_texels_th(gm_plan* p, cudaStream_t s, const TriStore& ts, const DepthView& dv,
+                             const CoarseBins& cb, int tiles_x, int tiles_per_fix, int64_t items,
+                             const GmFixExact* fix, long long b0) {
+    const int tiles_y = tiles_per_fix / tiles_x;
+    const dim3 grid((unsigned)tiles_x, (unsigned)((tiles_y + TW_WARPS - 1) / TW_WARPS), (unsigned)(items / tiles_per_fix));
+    k_texels<ATTRS, STATS, EXACT, TH><<<grid, TW_WARPS * 32, TX_DYN_SMEM, s>>>(ts, dv, cb, tiles_x, tiles_per_fix,
+                                                                           tiles_y, fix, b0);
+    if (dv.crowd_wide) {  // full-frustum batches and the raster API: few, long tiles
+        k_texels_crowded<ATTRS, STATS, EXACT, HV_FULL_WARPS, HV_FULL_SEL, TH>
+            <<<p->sms * (24 / HV_FULL_WARPS), HV_FULL_WARPS * 32, (int)sizeof(HeavySmem<HV_FULL_WARPS, HV_FULL_SEL>),
+               s>>>(ts, dv, cb, tiles_x, tiles_per_fix, fix, b0);
+    } else {
+        k_texels_crowded<ATTRS, STATS, EXACT, HV_CROP_WARPS, HV_CROP_SEL, TH>
+            <<<p->sms * (24 / HV_CROP_WARPS), HV_CROP_WARPS * 32, (int)sizeof(HeavySmem<HV_CROP_WARPS, HV_CROP_SEL>),
+               s>>>(ts, dv, cb, tiles_x, tiles_per_fix, fix, b0);
+    }
+}
+
+// k_texels over `items` (fixation, tile) work items of height 1 << dv.th_shift, then
+// the crowded tiles the first pass deferred (k_texels_crowded, persistent CTAs).
 template <bool ATTRS, bool STATS, bool EXACT>
 static int launch_texels(gm_plan* p, cudaStream_t s, const TriStore& ts, DepthView dv, const CoarseBins& cb,
                          int tiles_x, int tiles_per_fix, int64_t items, const GmFixExact* fix, long long b0) {
@@ -1426,19 +1466,14 @@ static int launch_texels(gm_plan* p, cudaStream_t s, const TriStore& ts, DepthVi
     if (dv.crowd_depth <= 0) dv.crowd_depth = CROWD_DEPTH;  // raster API / renderer views
     dv.crowd_count = p->d_crowd_count;
     CK(cudaMemsetAsync(p->d_crowd_count, 0, 2 * sizeof(int), s));
-    const int tiles_y = tiles_per_fix / tiles_x;
-    const dim3 grid((unsigned)tiles_x, (unsigned)((tiles_y + TW_WARPS - 1) / TW_WARPS), (unsigned)(items / tiles_per_fix));
-    k_texels<ATTRS, STATS, EXACT><<<grid, TW_WARPS * 32, TX_DYN_SMEM, s>>>(ts, dv, cb, tiles_x, tiles_per_fix,
-                                                                       tiles_y, fix, b0);
-    if (dv.crowd_wide) {  // full-frustum batches and the raster API: few, long tiles
-        k_texels_crowded<ATTRS, STATS, EXACT, HV_FULL_WARPS, HV_FULL_SEL>
-            <<<p->sms * (24 / HV_FULL_WARPS), HV_FULL_WARPS * 32, (int)sizeof(HeavySmem<HV_FULL_WARPS, HV_FULL_SEL>),
-               s>>>(ts, dv, cb, tiles_x, tiles_per_fix, fix, b0);
-    } else {
-        k_texels_crowded<ATTRS, STATS, EXACT, HV_CROP_WARPS, HV_CROP_SEL>
-            <<<p->sms * (24 / HV_CROP_WARPS), HV_CROP_WARPS * 32, (int)sizeof(HeavySmem<HV_CROP_WARPS, HV_CROP_SEL>),
-               s>>>(ts, dv, cb, tiles_x, tiles_per_fix, fix, b0);
+    if constexpr (!ATTRS && !EXACT) {
+        if (dv.th_shift == 5) {
+            launch_texels_th<ATTRS, STATS, EXACT, 32>(p, s, ts, dv, cb, tiles_x, tiles_per_fix, items, fix, b0);
+            CK(cudaGetLastError());
+            return GM_OK;
+        }
     }
+    launch_texels_th<ATTRS, STATS, EXACT, TH_FULL>(p, s, ts, dv, cb, tiles_x, tiles_per_fix, items, fix, b0);
     CK(cudaGetLastError());
     return GM_OK;
 }
@@ -1455,10 +1490,12 @@ static int enqueue_batch(gm_plan* p, const GmFixExact* d_fix, const GmFixCull* d
                          long long b0, double inv_sigma, const GmConfig* cfg, bool accumulate, cudaEvent_t* ev) {
     cudaStream_t s = p->stream;
     const int wwords = (W + 31) / 32;
-    const int tiles_x = (W + TW - 1) / TW, tiles_y = (H + TH - 1) / TH;
+    const int th = cfg->filtering ? TH_CROP : TH_FULL;
+    const int tiles_x = (W + TW - 1) / TW, tiles_y = (H + th - 1) / th;
     TriStore ts{p->d_tris, p->d_t32, p->d_bbox, p->d_count, p->cap_seg, p->d_fail, p->d_maxcount, p->d_ntris};
     DepthView dv{p->d_depth, p->d_mask, W, H, wwords, (cfg->flags & GM_FLAG_STATS) ? p->d_stats : nullptr,
                  p->d_vbuf};
+    dv.th_shift = th == 32 ? 5 : 4;
 #ifdef GM_CHECK
     dv.check = p->d_check;
 #endif
@@ -1473,7 +1510,7 @@ static int enqueue_batch(gm_plan* p, const GmFixExact* d_fix, const GmFixCull* d
     dv.crowd_depth = cfg->filtering ? CROWD_DEPTH_CROP : CROWD_DEPTH;
     dv.crowd_wide = cfg->filtering ? 0 : 1;
     dv.tiles_x = (W + TW - 1) / TW;
-    dv.tiles_per_fix = dv.tiles_x * ((H + TH - 1) / TH);
+    dv.tiles_per_fix = dv.tiles_x * tiles_y;
     if (ev) CK(cudaEventRecord(ev[0], s));
     CK(cudaMemsetAsync(p->d_count, 0, sizeof(int) * nb, s));
     if (p->n_clu > 0) {
@@ -2117,9 +2154,10 @@ static int raster_pass(gm_plan* p, int W, int H, bool attrs) {
         if (attempt == 15) return set_err(GM_ERR_OOM, "screen-triangle segment kept overflowing");
     }
     TriStore ts{p->d_tris, p->d_t32, p->d_bbox, p->d_count, p->cap_seg, p->d_fail, p->d_maxcount, p->d_ntris};
-    const int tiles_x = (W + TW - 1) / TW, tiles_y = (H + TH - 1) / TH;
+    const int tiles_x = (W + TW - 1) / TW, tiles_y = (H + TH_FULL - 1) / TH_FULL;
     DepthView dv{p->d_depth, p->d_mask, W, H, wwords, nullptr, p->d_vbuf, attrs ? p->d_key : nullptr};
     dv.crowd_wide = 1;  // every texel is marked: long tiles, many rounds each
+    dv.th_shift = 4;
     k_mark_all<<<blocks_for((int64_t)H * wwords, 256), 256, 0, s>>>(p->d_mask, W, H, wwords);
     CoarseBins cbins = coarse_bins(p, W, H);
     k_coarse<<<1, 256, 0, s>>>(ts, cbins, p->d_fail, 0, nullptr);

@@ -103,7 +103,7 @@ __device__ __forceinline__ int kth_set_bit(uint32_t w, int k) {
 //      leaves in that pixel.
 // One (fixation, tile) work item of k_texels.  T32/SEL: the warp's staging and
 // selection slices; KEY (crowded mode only): sort keys of SEL.
-template <bool ATTRS, bool STATS, bool CROWDED, bool EXACT>
+template <bool ATTRS, bool STATS, bool CROWDED, bool EXACT, int TH>
 __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __restrict__ SEL, float* __restrict__ KEY,
                                            int f, int tx, int ty, const TriStore& ts, const DepthView& dv,
                                            const CoarseBins& cb, int tiles_x, int tiles_per_fix,
@@ -750,7 +750,7 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
 
 // First pass: grid (tiles_x, ceil(tiles_y / TW_WARPS), fixations); warp w of a
 // CTA takes tile row blockIdx.y * TW_WARPS + w.
-template <bool ATTRS, bool STATS, bool EXACT>
+template <bool ATTRS, bool STATS, bool EXACT, int TH>
 __global__ void TX_BOUNDS k_texels(TriStore ts, DepthView dv, CoarseBins cb, int tiles_x,
                                    int tiles_per_fix, int tiles_y,
                                    const GmFixExact* __restrict__ fixes, long long b0) {
@@ -759,7 +759,7 @@ __global__ void TX_BOUNDS k_texels(TriStore ts, DepthView dv, CoarseBins cb, int
     if (*ts.fail <= b0) return;
     const int ty = blockIdx.y * TW_WARPS + warp;
     if (ty < tiles_y)
-        texel_item<ATTRS, STATS, false, EXACT>(reinterpret_cast<TexelWarpSmem*>(tx_dyn)[warp].t32,
+        texel_item<ATTRS, STATS, false, EXACT, TH>(reinterpret_cast<TexelWarpSmem*>(tx_dyn)[warp].t32,
                                                reinterpret_cast<TexelWarpSmem*>(tx_dyn)[warp].sel,
                                                reinterpret_cast<TexelWarpSmem*>(tx_dyn)[warp].key, blockIdx.z,
                                                blockIdx.x, ty, ts, dv, cb, tiles_x, tiles_per_fix, fixes);
@@ -767,7 +767,7 @@ __global__ void TX_BOUNDS k_texels(TriStore ts, DepthView dv, CoarseBins cb, int
 
 // Crowded pass: persistent CTAs of NW warps over the tiles the first pass
 // deferred, one tile per CTA at a time (texel_item, CROWDED branch).
-template <bool ATTRS, bool STATS, bool EXACT, int NW, int SELN>
+template <bool ATTRS, bool STATS, bool EXACT, int NW, int SELN, int TH>
 __global__ void __launch_bounds__(NW * 32, 24 / NW) k_texels_crowded(TriStore ts, DepthView dv, CoarseBins cb,
                                                                      int tiles_x, int tiles_per_fix,
                                                                      const GmFixExact* __restrict__ fixes,
@@ -786,7 +786,7 @@ __global__ void __launch_bounds__(NW * 32, 24 / NW) k_texels_crowded(TriStore ts
         if (w >= n_crowd) break;
         const int item = dv.crowd[w];
         const int f = item / tiles_per_fix, tile = item - f * tiles_per_fix;
-        texel_item<ATTRS, STATS, true, EXACT>(C.t32[warp], C.sel, C.key, f, tile % tiles_x, tile / tiles_x, ts, dv,
+        texel_item<ATTRS, STATS, true, EXACT, TH>(C.t32[warp], C.sel, C.key, f, tile % tiles_x, tile / tiles_x, ts, dv,
                                               cb, tiles_x, tiles_per_fix, fixes, SELN);
     }
 }

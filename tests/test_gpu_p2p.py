@@ -51,8 +51,22 @@ def _worker(rank, world, port, out_dir):
     # the API path (collective "auto") on a fresh accumulation
     dm = generate_sharded(scene, sampled, fx, cfg)
     api = np.concatenate([dm.values[o.object_id] for o in scene.objects])
+    # the collective fallback (all_reduce on the zero-copy torch view of the accumulator; NCCL in
+    # production, gloo here) on a fresh accumulation of the same shard
+    plan.accumulate_log(fx[a:b], cfg, reset=True)
+    plan.sync()
+    gmax_c, used_c, _ = reduce_peers(plan, None, "nccl")
+    coll = plan.read()
+    # ranks whose plans hold different sample layouts must refuse to reduce
+    inc = gm.GenerationConfig(k=1500.0, object_include_list={scene.objects[0].object_id} if rank else None)
+    other = get_plan(scene, sampled, inc, 0)
+    try:
+        reduce_peers(other, None, "auto")
+        mismatch = "no error"
+    except ValueError as e:
+        mismatch = str(e)
     np.savez(os.path.join(out_dir, f"r{rank}.npz"), partial=partial, reduced=reduced, gmax=gmax, used=used,
-             ms=ms, api=api, api_gmax=dm.global_max)
+             ms=ms, api=api, api_gmax=dm.global_max, coll=coll, gmax_c=gmax_c, used_c=used_c, mismatch=mismatch)
     dist.barrier()
     dist.destroy_process_group()
 
@@ -80,6 +94,11 @@ def test_two_rank_peer_reduce_bitwise():
     assert float(r[0]["gmax"]) == float(want.max()) == float(r[1]["gmax"])
     np.testing.assert_array_equal(r[0]["api"], r[1]["api"])
     np.testing.assert_array_equal(r[0]["api"], want)
+    for k in range(2):  # collective fallback: a + b of two operands is the same bits in either order
+        assert str(r[k]["used_c"]) == "nccl"
+        np.testing.assert_array_equal(r[k]["coll"], want)
+        assert float(r[k]["gmax_c"]) == float(want.max())
+        assert "different sample layouts" in str(r[k]["mismatch"])
     # single-process generate: additivity within the reference's partition tolerance
     scene, fx = _scene()
     cfg = gm.GenerationConfig(k=1500.0)
