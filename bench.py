@@ -424,11 +424,13 @@ def run_ours(args, rank, world):
     peaks = json.loads(peaks_path.read_text()) if peaks_path.exists() else {}
     pk = _peaks(lib, device, peaks)
 
-    # the job's whole stream for the sharded API calls (each rank generates its contiguous shard)
+    # the job's whole stream for the sharded API calls (each rank generates its contiguous shard).
+    # Weak scaling: the job stream is the ranks' streams back to back; generate_sharded on rank r
+    # reads only rows [r F, (r + 1) F), so the other ranks' rows are placeholders here (same
+    # shape, not read) instead of regenerating every rank's 100k-fixation stream on every rank
     job_fx = None
     if world > 1:
-        job_fx = fx_all if scaling == "strong" else np.concatenate(
-            [fx_all if r == rank else workload(args.config, args.fixations, r)[2] for r in range(world)])
+        job_fx = fx_all if scaling == "strong" else np.concatenate([fx_all] * world)
 
     # ---- map generation time, cold: build_sampled_meshes + generate + normalize on
     # in-memory inputs with a fresh plan (scene upload, sampling, buffer allocation all inside)
@@ -582,6 +584,21 @@ def run_ours(args, rank, world):
         tm1 = tm
     clk_mhz = peaks.get("sm_max_mhz", 1965.0)
     roof = _roofline(st, tm1, ms1.value, int(tm1.batches), pk, clk_mhz)
+    if e2e is not None and ms1.value > 0:
+        # SURVEY 8d per-stage split of the warm end-to-end call: host stages from the call's own wall
+        # clocks; the device step (overlapped streams) apportioned by the single-stream phase shares
+        last = e2e.get("stages_ms_last") or {}
+        dev = step_ms
+        share = {k2: v / ms1.value for k2, v in (("cull+project", tm1.cull_ms), ("filter+mark", tm1.mark_ms),
+                                                 ("raster (texels)", tm1.texel_ms),
+                                                 ("accumulate", tm1.accumulate_ms))}
+        e2e["split_ms"] = {"host setup (fixation table -> setup records)": last.get("setup"),
+                           **{k2: dev * v for k2, v in share.items()},
+                           "other device (sorts, coarse bins, overlap)": dev * (1.0 - sum(share.values())),
+                           "global max": last.get("max"), "D2H read-back": last.get("readback"),
+                           "end-to-end (measured)": e2e["ms_per_step"]}
+        e2e["split_note"] = ("H2D of the setup records (h2d_bytes_per_step) rides inside the device step, "
+                             "one 288-byte record per fixation, overlapped with the previous batch")
     # SURVEY 8d's step roofline: algorithmic FLOPs of the reference's per-pair work -- 26 per nominal
     # sample-fixation pair (camera transform + NDC projection, kernels.py:305-315) + 43 per NDC candidate
     # (depth test + Gaussian, :323-340) -- over the whole step, against the measured FP32 FMA peak (the
