@@ -563,18 +563,16 @@ struct DepthView {
     uint32_t* mask;   // [B][H][wwords]: texels the depth tests will read
     int W, H, wwords;
     unsigned long long* stats;  // optional work counters (GM_STAT_*), nullptr = off
-    float* vbuf;      // [B][H][W]: k_texels' inverse-depth bounds for tiles with many triangles
+    float* vbuf;      // [B][H][W] crowded pass, lists longer than one pass: inverse-depth bounds between passes
     int* key;         // [H][W] (ATTRS only): order key 2 t + fan of the triangle that wrote the texel
     int* win;         // [B][H][W] (generation batches): segment index of the texel's writer, -1 none
-    double* carry;    // [B][H][W] (generation batches): exact best depth between chunks of a tile
+    double* carry;    // [B][H][W] ... and exact best depths (generation batches)
     int* crowd;       // work items deferred to k_texels<CROWDED> (nullptr: handle them in place)
     int* crowd_count; // [2]: deferred items, claimed items
     float* tmax;      // [B][tiles] (generation batches): largest finite depth upper bound of the
                       // tile's marked texels, -inf if none (k_texels; tiles without marked
                       // texels are not written); nullptr = off
     int tiles_x, tiles_per_fix;
-    int crowd_mid;    // k_texels: lists of TW_CAP < n <= crowd_mid triangles also go to the crowded pass
-    int crowd_depth;  // k_texels: bbox cover (x tile area) above which a long list goes to the crowded pass
     int crowd_wide;   // crowded pass with HV_FULL_WARPS-warp CTAs (full-frustum z-buffers), else HV_CROP_WARPS
     int th_shift;     // log2 of the k_texels tile height of this batch (4: 32 x 16 tiles, 5: 32 x 32)
     unsigned long long* check;  // GM_CHECK builds: violation counters (GM_CHK_*), nullptr = off
@@ -945,15 +943,16 @@ struct gm_plan {
     uint2* d_bbox = nullptr;
     int* d_count = nullptr;
     int64_t cap_seg = 0, cap_seg_B = 0;
-    int64_t seg_init = 16384;  // first per-fixation screen-triangle capacity (gm_plan_set_segment_capacity)
+    int64_t seg_init = 16384;  // first per-fixation screen-triangle capacity, grown on overflow
+                               // (gm_plan_set_segment_capacity); C2 peaks above 4k, C5 grows it once
     long long* d_fail = nullptr;
     int* d_maxcount = nullptr;
     unsigned long long* d_ntris = nullptr;
     // marked z-buffer texels
     double* d_depth = nullptr;   // [B][H][W] marked texels only
-    float* d_vbuf = nullptr;     // [B][H][W] k_texels state for crowded tiles
+    float* d_vbuf = nullptr;     // [B][H][W] k_texels_crowded state between passes
     int* d_win = nullptr;        // [B][H][W] writer of each marked texel (generation batches)
-    double* d_carry = nullptr;   // [B][H][W] k_texels' exact best between chunks
+    double* d_carry = nullptr;   // [B][H][W] (generation batches)
     uint32_t* d_mask = nullptr;  // [B][H][wwords]
     int64_t cap_depth = 0, cap_mask = 0;
     int4* d_citems = nullptr;  // coarse bins: [B][cap_citems]
@@ -1378,6 +1377,7 @@ static int ensure_batch_set(gm_plan* p, int B, int W, int H, int64_t seg) {
         if ((rc = dev_alloc(&p->d_carry, (size_t)B * W * H))) return rc;
         p->cap_depth = (int64_t)B * W * H;
     }
+
     if (B > p->cap_cB || CB_ITEMS_PER_TRI * p->cap_seg > p->cap_citems) {
         const int64_t ci = CB_ITEMS_PER_TRI * std::max<int64_t>(p->cap_seg, seg);
         if ((rc = dev_alloc(&p->d_citems, (size_t)B * ci))) return rc;
@@ -1463,7 +1463,6 @@ template <bool ATTRS, bool STATS, bool EXACT>
 static int launch_texels(gm_plan* p, cudaStream_t s, const TriStore& ts, DepthView dv, const CoarseBins& cb,
                          int tiles_x, int tiles_per_fix, int64_t items, const GmFixExact* fix, long long b0) {
     dv.crowd = p->d_crowd;
-    if (dv.crowd_depth <= 0) dv.crowd_depth = CROWD_DEPTH;  // raster API / renderer views
     dv.crowd_count = p->d_crowd_count;
     CK(cudaMemsetAsync(p->d_crowd_count, 0, 2 * sizeof(int), s));
     if constexpr (!ATTRS && !EXACT) {
@@ -1506,8 +1505,6 @@ static int enqueue_batch(gm_plan* p, const GmFixExact* d_fix, const GmFixCull* d
     // a small distant object, walked faster whole (crowded pass, float32 fast path) than
     // chunk by chunk (C2 -3%); full-frustum tiles with such lists are far more common and
     // the persistent crowded pass is slower for them (unfiltered C2 +6%)
-    dv.crowd_mid = cfg->filtering ? CROWD_MID : 0;
-    dv.crowd_depth = cfg->filtering ? CROWD_DEPTH_CROP : CROWD_DEPTH;
     dv.crowd_wide = cfg->filtering ? 0 : 1;
     dv.tiles_x = (W + TW - 1) / TW;
     dv.tiles_per_fix = dv.tiles_x * tiles_y;
@@ -1867,6 +1864,52 @@ __global__ void k_reduce_peers(double* const* __restrict__ bufs, int world, int6
     if ((threadIdx.x & 31) == 0 && m > 0.0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
 }
 
+// The same for up to GM_PEER_MAX ranks: the peer pointers in registers, 16-byte
+// (2-sample) peer loads and stores over the 16-byte-aligned body of the slice,
+// the same rank-order sum per sample (identical bits to k_reduce_peers).
+#define GM_PEER_MAX 8
+__global__ void k_reduce_peers_vec(double* const* __restrict__ bufs, int world, int64_t a, int64_t b,
+                                   unsigned long long* __restrict__ out) {
+    double* p[GM_PEER_MAX];
+#pragma unroll
+    for (int r = 0; r < GM_PEER_MAX; r++) p[r] = r < world ? bufs[r] : nullptr;
+    double m = 0.0;
+    auto one = [&](int64_t i) {
+        double s = p[0][i];
+#pragma unroll
+        for (int r = 1; r < GM_PEER_MAX; r++)
+            if (r < world) s += p[r][i];
+#pragma unroll
+        for (int r = 0; r < GM_PEER_MAX; r++)
+            if (r < world) p[r][i] = s;
+        m = fmax(m, s);
+    };
+    const int64_t a2 = (a + 1) & ~(int64_t)1, b2 = b & ~(int64_t)1;  // even bounds of the body
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nthr = (int64_t)gridDim.x * blockDim.x;
+    if (a2 >= b2) {
+        for (int64_t i = a + tid; i < b; i += nthr) one(i);
+    } else {
+        if (tid == 0 && a < a2) one(a);
+        if (tid == 1 && b2 < b) one(b2);
+        for (int64_t j = a2 / 2 + tid; j < b2 / 2; j += nthr) {
+            double2 s = reinterpret_cast<const double2*>(p[0])[j];
+#pragma unroll
+            for (int r = 1; r < GM_PEER_MAX; r++)
+                if (r < world) {
+                    const double2 v = reinterpret_cast<const double2*>(p[r])[j];
+                    s.x += v.x;
+                    s.y += v.y;
+                }
+#pragma unroll
+            for (int r = 0; r < GM_PEER_MAX; r++)
+                if (r < world) reinterpret_cast<double2*>(p[r])[j] = s;
+            m = fmax(m, fmax(s.x, s.y));
+        }
+    }
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0 && m > 0.0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+}
+
 extern "C" int gm_plan_ipc_handle(gm_plan* p, void* out) {
     if (!p || !out) return set_err(GM_ERR_ARG, "null argument");
     if (!p->d_values) return set_err(GM_ERR_ARG, "plan has no scene");
@@ -1920,7 +1963,10 @@ extern "C" int gm_plan_reduce_peers(gm_plan* p, double* slice_max, float* device
     CK(cudaEventCreate(&e1));
     CK(cudaMemsetAsync(p->d_max, 0, sizeof(unsigned long long), s));
     CK(cudaEventRecord(e0, s));
-    if (b > a)
+    if (b > a && p->peer_world <= GM_PEER_MAX)
+        k_reduce_peers_vec<<<std::min<int64_t>(blocks_for((b - a + 1) / 2, 256), (int64_t)p->sms * 8), 256, 0, s>>>(
+            p->d_peer_ptr, p->peer_world, a, b, p->d_max);
+    else if (b > a)
         k_reduce_peers<<<std::min<int64_t>(blocks_for(b - a, 256), (int64_t)p->sms * 8), 256, 0, s>>>(
             p->d_peer_ptr, p->peer_world, a, b, p->d_max);
     CK(cudaGetLastError());

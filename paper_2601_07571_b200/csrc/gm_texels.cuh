@@ -47,21 +47,6 @@ struct __align__(16) HeavySmem {
     int sel[SELN + 4];     // sorted segment indices; [SELN]: pass count, [+1]: tile max, [+2]: claimed item
     float key[SELN];       // -inv_minw of sel[] (sort key: ascending min depth)
 };
-#ifndef CROWD_DEPTH
-#define CROWD_DEPTH 10  // ... and whose triangle bboxes cover the tile more than this many times
-#endif
-#ifndef CROWD_DEPTH_CROP
-#define CROWD_DEPTH_CROP 2  // the same in crop-frustum batches (C5 -1.7%; full-frustum C2 +55% at 2)
-#endif
-#ifndef CROWD_MID
-#define CROWD_MID 128  // ... and, in crop-frustum batches, tiles overlapping TW_CAP < n <= this many triangles
-#endif
-#ifndef CROWD_ALL
-#define CROWD_ALL 1  // every tile with more than TW_CAP overlapping triangles goes to the crowded pass
-#endif
-#ifndef CROWD_MIN
-#define CROWD_MIN 128  // tiles overlapping more triangles than this go to the crowded pass
-#endif
 #define TX_MAX_THREADS (32 * TW_WARPS)
 
 // position of the k-th (0-based) set bit of w (k < popc(w))
@@ -151,9 +136,6 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
     bool chunked = false;  // STATS: the tile took the multi-chunk path
 
     // 1. triangles overlapping the tile -> S.sel (scan cursor resumes if > TW_SEL)
-    int cover = 0;  // this lane's share of the selected bboxes' area inside the tile (depth complexity)
-    // only lists longer than CROWD_MIN can be routed by their depth complexity
-    const bool want_cover = n > CROWD_MIN;
     auto gather = [&](int& cursor) {
         int cnt = 0;
         while (cursor < n && cnt < TW_SEL) {
@@ -173,7 +155,6 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
                 }
                 const int x0 = bbx.x & 0xffff, x1 = bbx.x >> 16, y0 = bbx.y & 0xffff, y1 = bbx.y >> 16;
                 sel = !(x1 < xb || x0 > xe || y1 < yb || y0 > ye);
-                if (want_cover && sel) cover += (min(x1, xe) - max(x0, xb) + 1) * (min(y1, ye) - max(y0, yb) + 1);
             }
             const unsigned bal = __ballot_sync(FULL, sel);
             if (sel) {
@@ -410,7 +391,6 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
     double* dep = dv.depth + (int64_t)f * W * H;
     float2* dep2 = reinterpret_cast<float2*>(dv.depth) + (int64_t)f * W * H;  // !EXACT: depth bounds
     int* win = dv.win + (int64_t)f * W * H;                                    // !EXACT: the writer
-    double* carry = EXACT ? dep : dv.carry + (int64_t)f * W * H;               // best between chunks
     int cursor = 0;
     int nsel_total = 0;
     float tmax = -CUDART_INF_F;  // largest finite upper depth bound this lane stored
@@ -484,39 +464,22 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
         store_at((int64_t)(yb + row) * W + xb + colo, fast, fb, best, bkey, bwin);
     };
     if (!CROWDED) {
-        auto defer = [&]() {  // k_texels_crowded sorts the whole list (one CTA per tile)
+        auto defer = [&]() {  // to k_texels_crowded, which sorts the whole list (one CTA per tile)
             if (lane == 0) dv.crowd[atomicAdd(dv.crowd_count, 1)] = (int)item;
             if (STATS) stat_add(dv.stats, GM_STAT_TX_CROWDED, lane == 0 ? 1ull : 0ull);
         };
-#if CROWD_ALL
-        if (dv.crowd && n > TW_SEL) {  // a long list: leave even the gather to the CTA pass
+        if (n > TW_SEL) {  // a long list: leave even the gather to the CTA pass
             defer();
             return;
         }
-#endif
-        int nsel = gather(cursor);
+        const int nsel = gather(cursor);  // the whole list (n <= TW_SEL)
         if (STATS) nsel_total = nsel;
-        // deep tiles (overlapping surfaces: the selected bboxes cover the tile more than
-        // dv.crowd_depth times) profit from the sorted crowded pass; wide ones (many
-        // side-by-side triangles) stay here
-        // mid-size lists (TW_CAP < nsel <= CROWD_MID) go there too: the crowded pass stages
-        // them whole (TC_RES) and walks them in one pass with the float32 fast path, where
-        // the multi-chunk walk here must resolve every chunk's candidates exactly
-#if CROWD_ALL
-        if (dv.crowd && (cursor < n || nsel > TW_CAP)) {  // every multi-chunk tile
+        if (nsel > TW_CAP) {  // more than this pass stages: the CTA pass sorts the whole list
             defer();
             return;
         }
-#else
-        const bool mid = cursor >= n && nsel > TW_CAP && nsel <= dv.crowd_mid;
-        if (dv.crowd && (mid || ((cursor < n || nsel > CROWD_MIN) &&
-                                 __reduce_add_sync(FULL, (unsigned)cover) > (unsigned)(dv.crowd_depth * TW * TH)))) {
-            defer();
-            return;
-        }
-#endif
-        if (cursor >= n && nsel <= TW_CAP) {
-            // common case: one staging serves every round, per-texel state in registers
+        {
+            // one staging serves every round, per-texel state in registers
             if (nsel > 0) stage(0, nsel);
             for (int r0 = 0; r0 < total; r0 += 32) {
                 const int q = r0 + lane;
@@ -531,71 +494,6 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
                 if (nsel > 0) fast = walk(nsel, valid, row, colo, V, best, bkey, bwin, !EXACT, fb);
                 if (valid) store(row, colo, fast, fb, best, bkey, bwin);
             }
-        } else {
-            if (STATS) chunked = true;
-            // many triangles without a deferral list: chunk by chunk (each staged once),
-            // per-texel state kept in the depth array and the inverse-depth-bound buffer
-            float* vb = dv.vbuf + (int64_t)f * W * H;
-            bool first = true;
-            while (true) {
-                for (int c0 = 0; c0 < nsel; c0 += TW_CAP) {
-                    const int kend = min(TW_CAP, nsel - c0);
-                    const bool last = c0 + TW_CAP >= nsel && cursor >= n;
-                    stage(c0, kend);
-                    for (int r0 = 0; r0 < total; r0 += 32) {
-                        const int q = r0 + lane;
-                        const bool valid = q < total;
-                        int row, colo;
-                        texel_of(q, row, colo);
-                        const int64_t at = (int64_t)(yb + row) * W + xb + colo;
-                        float V = valid ? (first ? 0.0f : vb[at]) : CUDART_INF_F;
-                        double best = (valid && !first) ? carry[at] : CUDART_INF;
-                        int bkey = INT_MAX, bwin = -1;
-                        if (ATTRS && valid && !first) bkey = dv.key[at];
-                        if (!EXACT && valid && !first) bwin = win[at];
-                        float2 fb;
-                        walk(kend, valid, row, colo, V, best, bkey, bwin, false, fb);
-                        if (valid) {
-                            vb[at] = V;
-                            if (last) {
-                                store_at(at, false, fb, best, bkey, bwin);
-                            } else {
-                                carry[at] = best;
-                                if (ATTRS) dv.key[at] = best < CUDART_INF ? bkey : -1;
-                                if (!EXACT) win[at] = bwin;
-                            }
-                        }
-                    }
-                    first = false;
-                }
-                if (cursor >= n) break;
-                nsel = gather(cursor);
-                if (STATS) nsel_total += nsel;
-                if (nsel == 0 && cursor >= n && !first) {
-                    // the final rescan found nothing more: the last staged chunk was not
-                    // flagged `last`, so publish the carried state now
-                    for (int r0 = 0; r0 < total; r0 += 32) {
-                        const int q = r0 + lane;
-                        int row, colo;
-                        texel_of(q, row, colo);
-                        if (q < total) {
-                            const int64_t at = (int64_t)(yb + row) * W + xb + colo;
-                            const double best = carry[at];
-                            store_at(at, false, make_float2(0.0f, 0.0f), best, ATTRS ? dv.key[at] : -1,
-                                     EXACT ? -1 : win[at]);
-                        }
-                    }
-                    break;
-                }
-            }
-            if (first) {  // no triangle at all
-                for (int r0 = 0; r0 < total; r0 += 32) {
-                    const int q = r0 + lane;
-                    int row, colo;
-                    texel_of(q, row, colo);
-                    if (q < total) store(row, colo, false, make_float2(0.0f, 0.0f), CUDART_INF, -1, -1);
-                }
-            }
         }
     } else {
         // crowded tile, one CTA (NW warps) per tile: the CTA gathers the whole
@@ -607,7 +505,10 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
         // surfaces cost one sort, not one pass each; rounds run side by side.
         const int tid = threadIdx.x, warp = tid >> 5, nthr = blockDim.x;
         int* s_cnt = SEL + sel_cap;  // scalar slot after the arrays
+        // state carried between passes of a list longer than sel_cap (the stored writer /
+        // exact depth / order key are the outputs themselves)
         float* vb = dv.vbuf + (int64_t)f * W * H;
+        double* carry = EXACT ? dep : dv.carry + (int64_t)f * W * H;
         bool first = true;
         do {
             if (tid == 0) *s_cnt = 0;

@@ -76,9 +76,12 @@ class DensityMap:
 
     def __getattribute__(self, name):
         if name == "values" or name == "global_max":
-            link = object.__getattribute__(self, "__dict__").get("_device_link")
+            d = object.__getattribute__(self, "__dict__")
+            link = d.get("_device_link")
             if link is not None:
                 link.expose(self) if name == "values" else link.flush()
+            if name == "values":
+                d.pop("_zero", None)
         return object.__getattribute__(self, name)
 
     def __setattr__(self, name, value):
@@ -90,7 +93,9 @@ class DensityMap:
 
     @classmethod
     def zeros(cls, sampled_meshes: dict) -> "DensityMap":
-        return cls({oid: np.zeros(sm.total_samples) for oid, sm in sampled_meshes.items()})
+        dm = cls({oid: np.zeros(sm.total_samples) for oid, sm in sampled_meshes.items()})
+        dm.__dict__["_zero"] = True  # known all-zero until handed out: accumulate_fixation clears the
+        return dm                    # device accumulator instead of uploading zeros
 
     @property
     def total_samples(self) -> int:
@@ -491,6 +496,8 @@ class _DeviceLink:
         self.timers = None
         self.device_ahead = False
         self.exposed = False
+        self.call_key = None  # (scene, layout, config, device) of the calls feeding it
+        self.check = None     # _SetupCheck of that config
 
     def flush(self) -> None:
         if not self.pending:
@@ -525,6 +532,33 @@ def _config_key(config: GenerationConfig) -> tuple:
             bool(config.filtering_enabled))
 
 
+class _SetupCheck:
+    """The host fixation setup of one fixation (gm_fixation_setup), with its
+    buffers and ctypes pointers built once: accumulate_fixation's per-call
+    check that the fixation's crop frustum is valid (the reference raises
+    InvalidFrustumError from perspective_matrix at that call)."""
+
+    def __init__(self, config: GenerationConfig):
+        self.lib = _native.load()
+        self.row = np.zeros(18)
+        self.ex = np.zeros(_native.FIX_EXACT_DOUBLES)
+        self.bad = np.zeros(1, np.int64)
+        self.args = (_native.dptr(self.row), 1, float(config.theta), int(bool(config.filtering_enabled)),
+                     int(config.zbuffer_resolution), _native.dptr(self.ex), None, _native.iptr(self.bad))
+
+    def __call__(self, f) -> None:
+        r = self.row
+        r[0] = f.start_time
+        r[1] = f.duration
+        r[2:5] = f.camera_position
+        r[5:9] = f.camera_rotation
+        r[9:15] = f.frustum
+        r[15:18] = f.gaze_dir
+        rc = self.lib.gm_fixation_setup(*self.args)
+        if rc:
+            _native.check(rc, "fixation 0")
+
+
 def accumulate_fixation(dmap: DensityMap, scene, sampled_meshes: dict, fixation, config: GenerationConfig,
                         cache=None, timers: Timings | None = None, device: int = 0) -> DensityMap:
     """Add one fixation to `dmap` in place (running max updated), return it
@@ -536,23 +570,31 @@ def accumulate_fixation(dmap: DensityMap, scene, sampled_meshes: dict, fixation,
     A fixation whose crop frustum is degenerate raises InvalidFrustumError at
     its own call, as in the reference.  `timers` phases are recorded when the
     queued batch runs."""
-    config.validate()
-    plan = cache if isinstance(cache, ScenePlan) else get_plan(scene, sampled_meshes, config, device)
-    from .gaze import fixation_setup
-
-    fixation_setup([fixation], config.theta, config.filtering_enabled, config.zbuffer_resolution)  # raises here
     d = object.__getattribute__(dmap, "__dict__")
     link = d.get("_device_link")
-    if (link is None or link.plan is not plan or plan._owner is not link or link.exposed
-            or link.key != _config_key(config)):
-        if link is not None:
-            link.pull(dmap)
-        plan.release()
-        plan.write(plan.gather(d["values"]))
-        link = _DeviceLink(plan, dmap, config)
-        d["_device_link"] = link
-        plan._owner = link
-    link.config = config
+    key = (id(scene), id(sampled_meshes), id(config), _config_key(config), device)
+    if (link is not None and link.call_key == key and link.plan._owner is link and not link.exposed
+            and (cache is None or cache is link.plan)):
+        plan = link.plan  # the same map fed with the same scene / layout / config: no lookups
+    else:
+        config.validate()
+        plan = cache if isinstance(cache, ScenePlan) else get_plan(scene, sampled_meshes, config, device)
+        if (link is None or link.plan is not plan or plan._owner is not link or link.exposed
+                or link.key != _config_key(config)):
+            if link is not None:
+                link.pull(dmap)
+            plan.release()
+            if d.get("_zero"):  # a fresh DensityMap.zeros: clear on the device, nothing to upload
+                plan.accumulate(np.zeros((0, 18)), config, reset=True, _owner_ok=True)
+            else:
+                plan.write(plan.gather(d["values"]))
+            link = _DeviceLink(plan, dmap, config)
+            d["_device_link"] = link
+            plan._owner = link
+        link.config = config
+        link.call_key = key
+        link.check = _SetupCheck(config)
+    link.check(fixation)  # raises InvalidFrustumError here, as the reference does
     if timers is not None:
         link.timers = timers
     link.pending.append(fixation)

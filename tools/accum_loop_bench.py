@@ -35,12 +35,13 @@ def main():
     fx = [gm.Fixation(r[0], r[1], r[2:5], r[5:9], tuple(r[9:15]), r[15:18]) for r in table]
     cfg = gm.GenerationConfig(k=k)
     sampled = gm.build_sampled_meshes(scene, k)
-    gm.generate(scene, sampled, fx[:8], cfg)  # plan upload + warm-up
+    gm.generate(scene, sampled, fx, cfg)  # plan upload + batch buffers sized for this batch, warm-up
     t0 = time.perf_counter()
     full = gm.generate(scene, sampled, fx, cfg)
     t_gen = time.perf_counter() - t0
     dm = gm.DensityMap.zeros(sampled)
     gm.accumulate_fixation(dm, scene, sampled, fx[0], cfg)  # warm
+    dm.values  # settle the warm-up map (its queued fixation runs, it is read back)
     dm = gm.DensityMap.zeros(sampled)
     t0 = time.perf_counter()
     for f in fx:

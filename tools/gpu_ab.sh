@@ -10,7 +10,7 @@ for rep in $(seq $REPS); do
 for cfg in $CONFIGS; do
 for v in $VARIANTS; do
   GAZEMAP_B200_SO=paper_2601_07571_b200/$v.so timeout 600 python bench.py --config $cfg --steps 3 --warmup 2 \
-      --no-cpu --no-e2e $EXTRA > gpurun_out/ab_${v}_$cfg.log 2>&1
+      --no-cpu $EXTRA > gpurun_out/ab_${v}_$cfg.log 2>&1
   python - "$cfg" "$v" >> gpurun_out/ab.txt <<'PY'
 import json, sys
 cfg, v = sys.argv[1:3]
