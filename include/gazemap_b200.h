@@ -105,6 +105,14 @@ int gm_normalize(int device, const double* values, int64_t n, double gmax, doubl
 int gm_fixation_setup(const double* fixations, int64_t F, double theta, int filtering, int res, double* ex,
                       void* cull, int64_t* bad_fixation);
 
+/* The per-config constants of that setup (GmSetupConsts in csrc/gm_types.h:
+ * tan / atan / cos / sin of the cone angles), computed once ... */
+void gm_setup_consts(double theta, int filtering, int width, int height, void* consts);
+/* ... and the setup of one fixation row (18 float64) under them: GM_OK, or
+ * GM_ERR_INVALID_FRUSTUM where the reference's perspective_matrix raises
+ * InvalidFrustumError (accumulate_fixation's per-call check, density.py:148-158). */
+int gm_fixation_check(const double* fixation, const void* consts);
+
 /* ellipse_intersection(gaze_dir, n, cone) (gaze.py:252-309) for the cone's
  * 4-sigma half-angle phi: out[18] = center_E[3], major_a, minor_b,
  * inclination_alpha, A0[3], A1[3], B0[3], B1[3]; GM_ERR_GAZE_OUTSIDE when

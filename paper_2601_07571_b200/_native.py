@@ -70,6 +70,8 @@ SIGNATURES = {
     "gm_layout": (ctypes.c_int, [ctypes.c_int, _D, ctypes.c_int64, ctypes.c_double, _I64, _I64, _I64, _I64]),
     "gm_sample_positions": (ctypes.c_int, [ctypes.c_int, _D, ctypes.c_int64, _I64, _I64, ctypes.c_int64, _D, _D]),
     "gm_normalize": (ctypes.c_int, [ctypes.c_int, _D, ctypes.c_int64, ctypes.c_double, _D]),
+    "gm_setup_consts": (None, [ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p]),
+    "gm_fixation_check": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p]),
     "gm_fixation_setup": (ctypes.c_int, [_D, ctypes.c_int64, ctypes.c_double, ctypes.c_int, ctypes.c_int, _D,
                                          ctypes.c_void_p, _I64]),
     "gm_plan_create": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(_VP)]),

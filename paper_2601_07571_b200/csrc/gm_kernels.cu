@@ -2161,6 +2161,17 @@ extern "C" int gm_fixation_setup(const double* fx, int64_t F, double theta, int 
     return GM_OK;
 }
 
+// One fixation's setup under precomputed constants (accumulate_fixation's
+// per-call InvalidFrustumError check): no allocation, no trig for the constants.
+extern "C" int gm_fixation_check(const double* fx, const GmSetupConsts* c) {
+    if (!fx || !c) return set_err(GM_ERR_ARG, "null argument");
+    GmFixExact ex;
+    GmFixCull cull;
+    if (gm_setup_batch(fx, 1, c, &ex, &cull, 1) >= 0)
+        return set_err(GM_ERR_INVALID_FRUSTUM, "degenerate frustum bounds (InvalidFrustumError)");
+    return GM_OK;
+}
+
 // Full W x H rasterization of the plan's occluders under the camera record
 // already in d_fix[0] / d_cull[0] (kernels.rasterize, kernels.py:140-192):
 // k_tri_setup (cull per d_cull[0]; cos_t = -3 disables it) into a segment

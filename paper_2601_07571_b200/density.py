@@ -533,28 +533,34 @@ def _config_key(config: GenerationConfig) -> tuple:
 
 
 class _SetupCheck:
-    """The host fixation setup of one fixation (gm_fixation_setup), with its
-    buffers and ctypes pointers built once: accumulate_fixation's per-call
-    check that the fixation's crop frustum is valid (the reference raises
-    InvalidFrustumError from perspective_matrix at that call)."""
+    """The host fixation setup of one fixation (gm_fixation_check) under the
+    config's constants, computed once: accumulate_fixation's per-call check
+    that the fixation's crop frustum is valid (the reference raises
+    InvalidFrustumError from perspective_matrix at that call).  The row buffer
+    and the raw function pointer are prebuilt; a call costs a few us."""
 
     def __init__(self, config: GenerationConfig):
-        self.lib = _native.load()
+        lib = _native.load()
+        self.consts = ctypes.create_string_buffer(256)  # GmSetupConsts (< 256 bytes)
+        res = int(config.zbuffer_resolution)
+        lib.gm_setup_consts(float(config.theta), int(bool(config.filtering_enabled)), res, res, self.consts)
         self.row = np.zeros(18)
-        self.ex = np.zeros(_native.FIX_EXACT_DOUBLES)
-        self.bad = np.zeros(1, np.int64)
-        self.args = (_native.dptr(self.row), 1, float(config.theta), int(bool(config.filtering_enabled)),
-                     int(config.zbuffer_resolution), _native.dptr(self.ex), None, _native.iptr(self.bad))
+        self.views = (self.row[2:5], self.row[5:9], self.row[9:15], self.row[15:18])
+        raw = ctypes.CDLL(str(lib._name)).gm_fixation_check  # no per-call argument conversion
+        raw.restype = ctypes.c_int
+        self.fn = raw
+        self.args = (ctypes.c_void_p(self.row.ctypes.data), ctypes.cast(self.consts, ctypes.c_void_p))
 
     def __call__(self, f) -> None:
         r = self.row
         r[0] = f.start_time
         r[1] = f.duration
-        r[2:5] = f.camera_position
-        r[5:9] = f.camera_rotation
-        r[9:15] = f.frustum
-        r[15:18] = f.gaze_dir
-        rc = self.lib.gm_fixation_setup(*self.args)
+        pos, rot, fr, gz = self.views
+        pos[...] = f.camera_position
+        rot[...] = f.camera_rotation
+        fr[...] = f.frustum
+        gz[...] = f.gaze_dir
+        rc = self.fn(*self.args)
         if rc:
             _native.check(rc, "fixation 0")
 
