@@ -7,6 +7,12 @@
 #ifndef TW_CAP
 #define TW_CAP 64  // triangles staged by the first pass (a multiple of 32); longer lists go to the crowded pass
 #endif
+#ifndef SECTOR_FILL
+#define SECTOR_FILL 0  // 1: write the unmarked texels of every touched 32-byte store sector (no DRAM RMW)
+#endif
+#ifndef RANK_CTA_MAX
+#define RANK_CTA_MAX 0  // crowded pass: lists up to this long are ordered by rank counting, not bitonic
+#endif
 #ifndef RANK_SORT_MAX
 #define RANK_SORT_MAX 16  // staged lists up to this long are ordered by rank counting, longer by bitonic sort
 #endif
@@ -248,7 +254,7 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
     };
 
     // texel of compact id q: (row, tile-local column)
-    auto texel_of = [&](int q, int& row, int& colo) {
+    auto texel_of = [&](int q, int& row, int& colo, uint32_t& w_row) {
         row = 0;
 #pragma unroll
         for (int step = TH / 2; step > 0; step >>= 1) {
@@ -256,7 +262,7 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
             const int pc = __shfl_sync(FULL, pref_ex, cand & 31);
             if (cand < TH && pc <= q) row = cand;
         }
-        const uint32_t w_row = __shfl_sync(FULL, wr, row);
+        w_row = __shfl_sync(FULL, wr, row);
         const int k_in_row = q - __shfl_sync(FULL, pref_ex, row);
         colo = q < total ? kth_set_bit(w_row, k_in_row) : 0;
     };
@@ -463,6 +469,27 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
     auto store = [&](int row, int colo, bool fast, float2 fb, double best, int bkey, int bwin) {
         store_at((int64_t)(yb + row) * W + xb + colo, fast, fb, best, bkey, bwin);
     };
+    // Texel-store writes are sparse (3x3 blocks): a 32-byte sector left partly written costs a
+    // DRAM read-modify-write when L2 evicts it.  The first marked texel of each sector (4 float2
+    // bounds, 8 writer ints) also writes the sector's unmarked texels -- no reader ever looks at
+    // an unmarked texel -- so every sector it touches is written whole.  (Generation batches,
+    // W a multiple of 8 so sectors do not straddle rows.)
+    const bool fill_sectors = !EXACT && (W & 7) == 0;
+    auto fill = [&](int row, int colo, uint32_t w_row) {
+        const int64_t rb = (int64_t)(yb + row) * W + xb;
+        const uint32_t s4 = (w_row >> (colo & ~3)) & 0xFu;
+        if ((s4 & ((1u << (colo & 3)) - 1u)) == 0u) {
+#pragma unroll
+            for (int k = 0; k < 4; k++)
+                if (!((s4 >> k) & 1u)) dep2[rb + (colo & ~3) + k] = make_float2(CUDART_INF_F, CUDART_INF_F);
+        }
+        const uint32_t s8 = (w_row >> (colo & ~7)) & 0xFFu;
+        if ((s8 & ((1u << (colo & 7)) - 1u)) == 0u) {
+#pragma unroll
+            for (int k = 0; k < 8; k++)
+                if (!((s8 >> k) & 1u)) win[rb + (colo & ~7) + k] = -1;
+        }
+    };
     if (!CROWDED) {
         auto defer = [&]() {  // to k_texels_crowded, which sorts the whole list (one CTA per tile)
             if (lane == 0) dv.crowd[atomicAdd(dv.crowd_count, 1)] = (int)item;
@@ -485,14 +512,18 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
                 const int q = r0 + lane;
                 const bool valid = q < total;
                 int row, colo;
-                texel_of(q, row, colo);
+                uint32_t w_row;
+                texel_of(q, row, colo, w_row);
                 float V = valid ? 0.0f : CUDART_INF_F;
                 double best = CUDART_INF;
                 int bkey = INT_MAX, bwin = -1;
                 float2 fb = make_float2(0.0f, 0.0f);
                 bool fast = false;
                 if (nsel > 0) fast = walk(nsel, valid, row, colo, V, best, bkey, bwin, !EXACT, fb);
-                if (valid) store(row, colo, fast, fb, best, bkey, bwin);
+                if (valid) {
+                    store(row, colo, fast, fb, best, bkey, bwin);
+                    if (SECTOR_FILL && fill_sectors) fill(row, colo, w_row);
+                }
             }
         }
     } else {
@@ -543,6 +574,27 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
                 __syncthreads();  // every thread has read the count before the next block adds to it
             }
             if (STATS) nsel_total += cnt;
+            int so = 0;  // the sorted list starts at SEL + so / KEY + so
+#if RANK_CTA_MAX > 0
+            if (cnt <= RANK_CTA_MAX && 2 * cnt <= sel_cap) {
+                // short list: every entry's rank by counting (broadcast reads), scattered into
+                // the upper half -- one barrier instead of a bitonic network's log^2 of them
+                so = sel_cap / 2;
+                for (int e = tid; e < cnt; e += nthr) {
+                    const float ke = KEY[e];
+                    const int se = SEL[e];
+                    int rank = 0;
+                    for (int j = 0; j < cnt; j++) {
+                        const float kj = KEY[j];
+                        rank += (kj < ke || (kj == ke && SEL[j] < se)) ? 1 : 0;
+                    }
+                    SEL[so + rank] = se;
+                    KEY[so + rank] = ke;
+                }
+                __syncthreads();
+            } else
+#endif
+            {
             int P = 32;
             while (P < cnt) P <<= 1;
             for (int k = cnt + tid; k < P; k += nthr) {
@@ -569,14 +621,16 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
                     __syncthreads();
                 }
             }
+            }
             const bool last = cursor >= n;
+            const int* SS = SEL + so;  // sorted segment indices
             // walk order: the sorted list, staged 32 records at a time into this warp's slice
             auto fetch = [&](int kk) -> const TriF32& {
                 if ((kk & 31) == 0) {
                     __syncwarp();
                     const int k = kk + lane;
                     if (k < cnt) {
-                        const uint4* from = reinterpret_cast<const uint4*>(segf + SEL[k]);
+                        const uint4* from = reinterpret_cast<const uint4*>(segf + SS[k]);
                         uint4* to = reinterpret_cast<uint4*>(&T32[lane]);
 #pragma unroll
                         for (int part = 0; part < 6; part++) to[part] = from[part];
@@ -585,12 +639,13 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
                 }
                 return T32[kk & 31];
             };
-            auto from_global = [&](int k) -> const TriF32& { return segf[SEL[k]]; };
+            auto from_global = [&](int k) -> const TriF32& { return segf[SS[k]]; };
             for (int r0 = warp * 32; r0 < total; r0 += nthr) {
                 const int q = r0 + lane;
                 const bool valid = q < total;
                 int row, colo;
-                texel_of(q, row, colo);
+                uint32_t w_row;
+                texel_of(q, row, colo, w_row);
                 const int64_t at = (int64_t)(yb + row) * W + xb + colo;
                 float V = valid ? (first ? 0.0f : vb[at]) : CUDART_INF_F;
                 double best = (valid && !first) ? carry[at] : CUDART_INF;
@@ -604,6 +659,7 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
                     fast = walk_with(cnt, fetch, from_global, valid, row, colo, V, best, bkey, bwin,
                                      !EXACT && first && last, fb);
                 if (valid) {
+                    if (SECTOR_FILL && fill_sectors && first) fill(row, colo, w_row);
                     if (last) {
                         store_at(at, fast, fb, best, bkey, bwin);
                     } else {

@@ -89,6 +89,8 @@ class DensityMap:
             link = self.__dict__.get("_device_link")
             if link is not None:  # a caller overwriting the map: settle the queued fixations first
                 link.expose(self)
+            if name == "values":
+                self.__dict__.pop("_zero", None)
         object.__setattr__(self, name, value)
 
     @classmethod

@@ -305,3 +305,21 @@ def test_integration_md_ctypes_stub_runs():
     assert got.global_max == want.global_max > 0
     for oid in want.values:
         np.testing.assert_array_equal(got.values[oid], want.values[oid])
+
+
+def test_accumulate_fixation_zero_map_replaced_values():
+    """A DensityMap.zeros whose values dict is replaced (or read and edited)
+    before the first call must be uploaded, not cleared on the device."""
+    scene, k, table = W.c1()
+    cfg = gm.GenerationConfig(k=k)
+    sampled = gm.build_sampled_meshes(scene, k)
+    fx = [gm.Fixation(r[0], r[1], r[2:5], r[5:9], tuple(r[9:15]), r[15:18]) for r in table[:6]]
+    base = gm.generate(scene, sampled, fx[:3], cfg)
+    dm = gm.DensityMap.zeros(sampled)
+    dm.values = {o: v.copy() for o, v in base.values.items()}
+    dm.global_max = base.global_max
+    for f in fx[3:]:
+        gm.accumulate_fixation(dm, scene, sampled, f, cfg)
+    full = gm.generate(scene, sampled, fx, cfg)
+    np.testing.assert_allclose(dm.values["icosphere"], full.values["icosphere"], rtol=1e-12, atol=0.0)
+    assert dm.global_max == pytest.approx(full.global_max, rel=1e-12)
