@@ -1443,8 +1443,9 @@ static void launch_texels_th(gm_plan* p, cudaStream_t s, const TriStore& ts, con
                              const CoarseBins& cb, int tiles_x, int tiles_per_fix, int64_t items,
                              const GmFixExact* fix, long long b0) {
     const int tiles_y = tiles_per_fix / tiles_x;
-    const dim3 grid((unsigned)tiles_x, (unsigned)((tiles_y + TW_WARPS - 1) / TW_WARPS), (unsigned)(items / tiles_per_fix));
-    k_texels<ATTRS, STATS, EXACT, TH><<<grid, TW_WARPS * 32, TX_DYN_SMEM, s>>>(ts, dv, cb, tiles_x, tiles_per_fix,
+    constexpr int nw = TexelWarps<TH>::n;
+    const dim3 grid((unsigned)tiles_x, (unsigned)((tiles_y + nw - 1) / nw), (unsigned)(items / tiles_per_fix));
+    k_texels<ATTRS, STATS, EXACT, TH><<<grid, nw * 32, nw * (int)sizeof(TexelWarpSmem), s>>>(ts, dv, cb, tiles_x, tiles_per_fix,
                                                                            tiles_y, fix, b0);
     if (dv.crowd_wide) {  // full-frustum batches and the raster API: few, long tiles
         k_texels_crowded<ATTRS, STATS, EXACT, HV_FULL_WARPS, HV_FULL_SEL, TH>

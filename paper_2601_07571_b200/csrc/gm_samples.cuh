@@ -236,22 +236,23 @@ __global__ void KM_BOUNDS k_mark(const float* __restrict__ pxf, const float* __r
                 const int bx0 = max(cxlo - 1, 0), bx1 = min(cxhi + 1, W - 1);
                 const int by0 = max(cylo - 1, 0), by1 = min(cyhi + 1, H - 1);
                 my_bits |= 1u << j;
-                uint32_t* m = dv.mask + (int64_t)f * H * dv.wwords;
                 const unsigned long long bits = ((1ull << (bx1 - bx0 + 1)) - 1ull) << (bx0 & 31);
-                const int w0 = bx0 >> 5;
-                for (int yy = by0; yy <= by1; yy++) {
-                    uint32_t* row = m + (int64_t)yy * dv.wwords + w0;
-                    if (dv.crowd_wide) {
-                        // full-frustum batches: bits are only ever set during the pass, so a (possibly
-                        // stale) read that already shows them proves the atomic redundant -- unfiltered
-                        // C2 mark 74 -> 61 ms; in crop-frustum batches the extra read costs more than
-                        // the atomics it saves (C2 +12%, C5 +42%)
-                        if ((__ldcg(row) & (uint32_t)bits) != (uint32_t)bits) atomicOr(row, (uint32_t)bits);
-                        if ((bits >> 32) && (__ldcg(row + 1) & (uint32_t)(bits >> 32)) != (uint32_t)(bits >> 32))
-                            atomicOr(row + 1, (uint32_t)(bits >> 32));
-                    } else {
-                        atomicOr(row, (uint32_t)bits);
-                        if (bits >> 32) atomicOr(row + 1, (uint32_t)(bits >> 32));
+                const uint32_t lo = (uint32_t)bits, hi = (uint32_t)(bits >> 32);
+                const int ww = dv.wwords;
+                uint32_t* row = dv.mask + ((int64_t)f * H + by0) * ww + (bx0 >> 5);
+                if (dv.crowd_wide) {
+                    // full-frustum batches: bits are only ever set during the pass, so a (possibly
+                    // stale) read that already shows them proves the atomic redundant -- unfiltered
+                    // C2 mark 74 -> 61 ms; in crop-frustum batches the extra read costs more than
+                    // the atomics it saves (C2 +12%, C5 +42%)
+                    for (int yy = by0; yy <= by1; yy++, row += ww) {
+                        if ((__ldcg(row) & lo) != lo) atomicOr(row, lo);
+                        if (hi && (__ldcg(row + 1) & hi) != hi) atomicOr(row + 1, hi);
+                    }
+                } else {
+                    for (int yy = by0; yy <= by1; yy++, row += ww) {
+                        atomicOr(row, lo);
+                        if (hi) atomicOr(row + 1, hi);
                     }
                 }
             }

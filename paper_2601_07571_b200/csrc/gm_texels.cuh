@@ -17,6 +17,9 @@
 #define RANK_SORT_MAX 16  // staged lists up to this long are ordered by rank counting, longer by bitonic sort
 #endif
 #define TW_SEL 128  // overlapping triangles remembered per tile (more: rescanned per round)
+#ifndef TW_WARPS_CROP
+#define TW_WARPS_CROP 1  // ... for the 32 x 32 tiles of crop-frustum batches (C2 -1%; 2 for the rest)
+#endif
 #ifndef TW_WARPS
 #define TW_WARPS 2  // warps (independent tile items) per k_texels CTA
 #endif
@@ -705,16 +708,22 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
     }
 }
 
-// First pass: grid (tiles_x, ceil(tiles_y / TW_WARPS), fixations); warp w of a
-// CTA takes tile row blockIdx.y * TW_WARPS + w.
+// Warps per first-pass CTA for a tile height (registers capped at 72 either way).
+template <int TH>
+struct TexelWarps {
+    static constexpr int n = TH == 32 ? TW_WARPS_CROP : TW_WARPS;
+};
+// First pass: grid (tiles_x, ceil(tiles_y / n), fixations); warp w of a CTA takes
+// tile row blockIdx.y * n + w.
 template <bool ATTRS, bool STATS, bool EXACT, int TH>
-__global__ void TX_BOUNDS k_texels(TriStore ts, DepthView dv, CoarseBins cb, int tiles_x,
+__global__ void __launch_bounds__(TexelWarps<TH>::n * 32, 28 / TexelWarps<TH>::n) k_texels(TriStore ts, DepthView dv,
+                                                                                    CoarseBins cb, int tiles_x,
                                    int tiles_per_fix, int tiles_y,
                                    const GmFixExact* __restrict__ fixes, long long b0) {
     extern __shared__ __align__(16) unsigned char tx_dyn[];
     const int warp = threadIdx.x >> 5;
     if (*ts.fail <= b0) return;
-    const int ty = blockIdx.y * TW_WARPS + warp;
+    const int ty = blockIdx.y * TexelWarps<TH>::n + warp;
     if (ty < tiles_y)
         texel_item<ATTRS, STATS, false, EXACT, TH>(reinterpret_cast<TexelWarpSmem*>(tx_dyn)[warp].t32,
                                                reinterpret_cast<TexelWarpSmem*>(tx_dyn)[warp].sel,
