@@ -7,6 +7,10 @@
 #ifndef TW_CAP
 #define TW_CAP 64  // triangles staged by the first pass (a multiple of 32); longer lists go to the crowded pass
 #endif
+#ifndef TEXEL_LIST
+#define TEXEL_LIST 1  // first pass: each round's texels read from a per-tile compact list in shared memory
+                      // (C2 -3%; the crowded pass keeps the search: a list there cost C5 +7%)
+#endif
 #ifndef SECTOR_FILL
 #define SECTOR_FILL 0  // 1: write the unmarked texels of every touched 32-byte store sector (no DRAM RMW)
 #endif
@@ -511,12 +515,41 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
         {
             // one staging serves every round, per-texel state in registers
             if (nsel > 0) stage(0, nsel);
+#if TEXEL_LIST
+            // the tile's marked texels as a compact (row << 5 | column) list in the gather
+            // area (free once staged): lane r writes row r's, one read per texel per round
+            // instead of a shuffle binary search + k-th set bit
+            uint16_t* tlist = reinterpret_cast<uint16_t*>(SEL);
+            constexpr int LCAP = (TW_SEL + 32) * 4;  // SEL + KEY, as 16-bit entries
+            __syncwarp();
+            if (lane < TH) {
+                uint32_t w = wr;
+                int at = pref_ex;
+                while (w && at < LCAP) {
+                    tlist[at++] = (uint16_t)((lane << 5) | (__ffs(w) - 1));
+                    w &= w - 1;
+                }
+            }
+            __syncwarp();
+#endif
             for (int r0 = 0; r0 < total; r0 += 32) {
                 const int q = r0 + lane;
                 const bool valid = q < total;
                 int row, colo;
                 uint32_t w_row;
+#if TEXEL_LIST
+                if (r0 + 32 <= LCAP) {
+                    const unsigned e = valid ? tlist[q] : 0u;
+                    row = (int)(e >> 5);
+                    colo = (int)(e & 31u);
+                    w_row = 0u;  // only the (disabled by default) sector fill reads it
+                    if (SECTOR_FILL) w_row = __shfl_sync(FULL, wr, row);
+                } else {
+                    texel_of(q, row, colo, w_row);
+                }
+#else
                 texel_of(q, row, colo, w_row);
+#endif
                 float V = valid ? 0.0f : CUDART_INF_F;
                 double best = CUDART_INF;
                 int bkey = INT_MAX, bwin = -1;
