@@ -346,6 +346,9 @@ struct TriStore {
 #ifndef TS_WARPS
 #define TS_WARPS 2  // warps (independent cluster groups) per k_tri_setup CTA
 #endif
+#ifndef TS_TOTAL_ATOMIC
+#define TS_TOTAL_ATOMIC 0  // 1: k_tri_setup counts screen triangles with one global atomic per cluster
+#endif                     // (0: k_coarse adds each fixation's count once -- no single-address hot spot)
 #ifndef TS_VEC_STORE
 #define TS_VEC_STORE 1  // TriF32 assembled in registers, six 16-byte stores (C5 cull 352 -> 258 ms)
 #endif
@@ -387,7 +390,9 @@ __global__ void __launch_bounds__(TS_WARPS * 32) k_tri_setup(const double* __res
         if (total == 0) continue;
         int base = 0;
         if (lane == 31) {
+#if TS_TOTAL_ATOMIC
             atomicAdd(ts.total, (unsigned long long)total);
+#endif
             base = atomicAdd(ts.count + f, total);
             if (base + total > ts.cap_seg) {
                 atomicMin(ts.fail, b0);
@@ -483,6 +488,9 @@ __global__ void __launch_bounds__(256) k_coarse(TriStore ts, CoarseBins cb, cons
     const int f = blockIdx.x;
     const int nbins = cb.ncx * cb.ncy;
     const int n = min(ts.count[f], (int)ts.cap_seg);
+#if !TS_TOTAL_ATOMIC
+    if (threadIdx.x == 0 && ts.total) atomicAdd(ts.total, (unsigned long long)ts.count[f]);  // statistics
+#endif
     const uint2* segb = ts.bbox + (int64_t)f * ts.cap_seg;
     for (int b = threadIdx.x; b < nbins; b += blockDim.x) s_cnt[b] = 0;
     __syncthreads();

@@ -500,12 +500,27 @@ class _DeviceLink:
         self.exposed = False
         self.call_key = None  # (scene, layout, config, device) of the calls feeding it
         self.check = None     # _SetupCheck of that config
+        self.rows = None      # the pending fixations' (F, 18) table rows, filled by the checks
+        self.overrides = False  # a pending fixation carries pose overrides (then the objects are needed)
+
+    def add(self, fixation) -> None:
+        """Queue a fixation whose row the check has just built."""
+        n = len(self.pending)
+        if self.rows is None:
+            self.rows = np.empty((self.PENDING_MAX, 18))
+        self.rows[n] = self.check.row
+        self.pending.append(fixation)
+        if getattr(fixation, "overrides", None):
+            self.overrides = True
 
     def flush(self) -> None:
         if not self.pending:
             return
         todo, self.pending = self.pending, []
-        self.plan.accumulate_log(todo, self.config, reset=False, timers=self.timers, _owner_ok=True)
+        # no overrides: the table the per-call checks built (no per-object conversion)
+        log = todo if self.overrides else self.rows[:len(todo)]
+        self.overrides = False
+        self.plan.accumulate_log(log, self.config, reset=False, timers=self.timers, _owner_ok=True)
         self.device_ahead = True
         dmap = self.dmap_ref()
         if dmap is not None and any(b > a for a, b in self.plan.slices.values()):
@@ -605,7 +620,7 @@ def accumulate_fixation(dmap: DensityMap, scene, sampled_meshes: dict, fixation,
     link.check(fixation)  # raises InvalidFrustumError here, as the reference does
     if timers is not None:
         link.timers = timers
-    link.pending.append(fixation)
+    link.add(fixation)
     if len(link.pending) >= link.PENDING_MAX:
         link.flush()
     return dmap
