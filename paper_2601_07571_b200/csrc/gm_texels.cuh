@@ -11,6 +11,9 @@
 #define TEXEL_LIST 1  // first pass: each round's texels read from a per-tile compact list in shared memory
                       // (C2 -3%; the crowded pass keeps the search: a list there cost C5 +7%)
 #endif
+#ifndef TL_QUAD
+#define TL_QUAD 1  // texel list in 16 x 16 quadrant order (else row order)
+#endif
 #ifndef SECTOR_FILL
 #define SECTOR_FILL 0  // 1: write the unmarked texels of every touched 32-byte store sector (no DRAM RMW)
 #endif
@@ -146,7 +149,6 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
     }
     const int xe = xb + TW - 1, ye = yb + TH - 1;
     unsigned long long c_pairs = 0, c_cov = 0, c_iter = 0, c_edge = 0;
-    bool chunked = false;  // STATS: the tile took the multi-chunk path
 
     // 1. triangles overlapping the tile -> S.sel (scan cursor resumes if > TW_SEL)
     auto gather = [&](int& cursor) {
@@ -522,7 +524,39 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
             uint16_t* tlist = reinterpret_cast<uint16_t*>(SEL);
             constexpr int LCAP = (TW_SEL + 32) * 4;  // SEL + KEY, as 16-bit entries
             __syncwarp();
-            if (lane < TH) {
+#if TL_QUAD
+            if (total <= LCAP) {
+                // 16 x 16 quadrants in turn (top left, top right, bottom left, bottom right):
+                // a round's 32 texels then span ~16 x 8 texels instead of 32 x 4, so fewer
+                // staged triangles reach any of its lanes (each texel's result does not depend
+                // on which round it is in: the walk state is per lane)
+                uint32_t lo = wr & 0xffffu, hi = wr >> 16;  // lanes >= TH hold 0
+                const int cl = __popc(lo), ch = __popc(hi);
+                int pl = cl, ph = ch;  // inclusive prefixes within each 16-row half
+#pragma unroll
+                for (int o = 1; o < 16; o <<= 1) {
+                    const int vl = __shfl_up_sync(FULL, pl, o), vh = __shfl_up_sync(FULL, ph, o);
+                    if ((lane & 15) >= o) {
+                        pl += vl;
+                        ph += vh;
+                    }
+                }
+                const int top_lo = __shfl_sync(FULL, pl, 15), top_hi = __shfl_sync(FULL, ph, 15);
+                const int bot_lo = __shfl_sync(FULL, pl, 31);
+                const int base_lo = lane < 16 ? 0 : top_lo + top_hi;
+                const int base_hi = lane < 16 ? top_lo : top_lo + top_hi + bot_lo;
+                int al = base_lo + pl - cl, ah = base_hi + ph - ch;
+                while (lo) {
+                    tlist[al++] = (uint16_t)((lane << 5) | (__ffs(lo) - 1));
+                    lo &= lo - 1;
+                }
+                while (hi) {
+                    tlist[ah++] = (uint16_t)((lane << 5) | (__ffs(hi) + 15));
+                    hi &= hi - 1;
+                }
+            } else
+#endif
+            if (lane < TH) {  // row order (the texel_of order, which rounds past LCAP use)
                 uint32_t w = wr;
                 int at = pref_ex;
                 while (w && at < LCAP) {
@@ -733,9 +767,6 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
         stat_add(dv.stats, GM_STAT_TX_LIST, t0 ? (unsigned long long)n : 0ull);
         stat_add(dv.stats, GM_STAT_TX_ITER, l0 ? c_iter : 0ull);
         stat_add(dv.stats, GM_STAT_PAIRS, c_pairs);
-        stat_add(dv.stats, GM_STAT_TX_CHUNKED, (l0 && chunked) ? 1ull : 0ull);
-        stat_add(dv.stats, GM_STAT_TX_CHUNKED_PAIRS, chunked ? c_pairs : 0ull);
-        stat_add(dv.stats, GM_STAT_TX_CHUNKED_TEXELS, (l0 && chunked) ? (unsigned long long)total : 0ull);
         stat_add(dv.stats, GM_STAT_COVERED, c_cov);
         stat_add(dv.stats, GM_STAT_TX_EDGE, c_edge);
     }
