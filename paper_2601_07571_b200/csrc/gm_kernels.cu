@@ -51,7 +51,10 @@
 #else
 #define TX_BOUNDS __launch_bounds__(TX_MAX_THREADS)
 #endif
-#ifdef KS_MINB
+#ifndef KS_MINB
+#define KS_MINB 4  // k_samples: 4 CTAs (32 warps) per SM, 64 registers (C5 accumulate 269 -> 245 ms;
+#endif             // uncapped: 80 registers, 3 CTAs)
+#if KS_MINB > 0
 #define KS_BOUNDS __launch_bounds__(256, KS_MINB)
 #else
 #define KS_BOUNDS __launch_bounds__(256)
@@ -1457,11 +1460,11 @@ static void launch_texels_th(gm_plan* p, cudaStream_t s, const TriStore& ts, con
                                                                            tiles_y, fix, b0);
     if (dv.crowd_wide) {  // full-frustum batches and the raster API: few, long tiles
         k_texels_crowded<ATTRS, STATS, EXACT, HV_FULL_WARPS, HV_FULL_SEL, TH>
-            <<<p->sms * (24 / HV_FULL_WARPS), HV_FULL_WARPS * 32, (int)sizeof(HeavySmem<HV_FULL_WARPS, HV_FULL_SEL>),
+            <<<p->sms * (HV_FULL_WARPS_SM / HV_FULL_WARPS), HV_FULL_WARPS * 32, (int)sizeof(HeavySmem<HV_FULL_WARPS, HV_FULL_SEL>),
                s>>>(ts, dv, cb, tiles_x, tiles_per_fix, fix, b0);
     } else {
         k_texels_crowded<ATTRS, STATS, EXACT, HV_CROP_WARPS, HV_CROP_SEL, TH>
-            <<<p->sms * (24 / HV_CROP_WARPS), HV_CROP_WARPS * 32, (int)sizeof(HeavySmem<HV_CROP_WARPS, HV_CROP_SEL>),
+            <<<p->sms * (HV_CROP_WARPS_SM / HV_CROP_WARPS), HV_CROP_WARPS * 32, (int)sizeof(HeavySmem<HV_CROP_WARPS, HV_CROP_SEL>),
                s>>>(ts, dv, cb, tiles_x, tiles_per_fix, fix, b0);
     }
 }

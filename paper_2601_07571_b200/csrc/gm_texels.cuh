@@ -11,6 +11,12 @@
 #define TEXEL_LIST 1  // first pass: each round's texels read from a per-tile compact list in shared memory
                       // (C2 -3%; the crowded pass keeps the search: a list there cost C5 +7%)
 #endif
+#ifndef TX_WARPS_SM
+#define TX_WARPS_SM 28  // first-pass warps per SM the register budget is sized for (32 x 16 tiles: 72 registers)
+#endif
+#ifndef TX_WARPS_SM_CROP
+#define TX_WARPS_SM_CROP 32  // ... 32 x 32 tiles (63 registers, no spills: C2 texels 154.1 -> 148.6 ms)
+#endif
 #ifndef TL_QUAD
 #define TL_QUAD 1  // texel list in 16 x 16 quadrant order (else row order)
 #endif
@@ -45,6 +51,15 @@ struct __align__(16) TexelWarpSmem {
 // long lists (up to ~3,000 triangles over distant props) made a few serial
 // tiles the whole launch; spreading a tile's rounds over 8 warps cut unfiltered
 // C2 texels 398 -> 105 ms.
+// crowded-pass warps per SM the register budget is sized for: 24 (80 registers) for the
+// 2-warp crop-frustum CTAs (32: C5 texels +4%, shared memory), 32 (64 registers) for the
+// 8-warp full-frustum ones (unfiltered C2 texels 105.5 -> 101.6 ms)
+#ifndef HV_CROP_WARPS_SM
+#define HV_CROP_WARPS_SM 24
+#endif
+#ifndef HV_FULL_WARPS_SM
+#define HV_FULL_WARPS_SM 32
+#endif
 #ifndef HV_CROP_WARPS
 #define HV_CROP_WARPS 2
 #endif
@@ -776,11 +791,12 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
 template <int TH>
 struct TexelWarps {
     static constexpr int n = TH == 32 ? TW_WARPS_CROP : TW_WARPS;
+    static constexpr int ctas = (TH == 32 ? TX_WARPS_SM_CROP : TX_WARPS_SM) / n;  // resident CTAs per SM
 };
 // First pass: grid (tiles_x, ceil(tiles_y / n), fixations); warp w of a CTA takes
 // tile row blockIdx.y * n + w.
 template <bool ATTRS, bool STATS, bool EXACT, int TH>
-__global__ void __launch_bounds__(TexelWarps<TH>::n * 32, 28 / TexelWarps<TH>::n) k_texels(TriStore ts, DepthView dv,
+__global__ void __launch_bounds__(TexelWarps<TH>::n * 32, TexelWarps<TH>::ctas) k_texels(TriStore ts, DepthView dv,
                                                                                     CoarseBins cb, int tiles_x,
                                    int tiles_per_fix, int tiles_y,
                                    const GmFixExact* __restrict__ fixes, long long b0) {
@@ -798,7 +814,7 @@ __global__ void __launch_bounds__(TexelWarps<TH>::n * 32, 28 / TexelWarps<TH>::n
 // Crowded pass: persistent CTAs of NW warps over the tiles the first pass
 // deferred, one tile per CTA at a time (texel_item, CROWDED branch).
 template <bool ATTRS, bool STATS, bool EXACT, int NW, int SELN, int TH>
-__global__ void __launch_bounds__(NW * 32, 24 / NW) k_texels_crowded(TriStore ts, DepthView dv, CoarseBins cb,
+__global__ void __launch_bounds__(NW * 32, (NW == HV_FULL_WARPS ? HV_FULL_WARPS_SM : HV_CROP_WARPS_SM) / NW) k_texels_crowded(TriStore ts, DepthView dv, CoarseBins cb,
                                                                      int tiles_x, int tiles_per_fix,
                                                                      const GmFixExact* __restrict__ fixes,
                                                                      long long b0) {
