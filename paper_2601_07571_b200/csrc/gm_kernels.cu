@@ -352,10 +352,18 @@ struct TriStore {
 #ifndef TS_TOTAL_ATOMIC
 #define TS_TOTAL_ATOMIC 0  // 1: k_tri_setup counts screen triangles with one global atomic per cluster
 #endif                     // (0: k_coarse adds each fixation's count once -- no single-address hot spot)
+#ifndef TS_MINB
+#define TS_MINB 16  // k_tri_setup register budget: 16 CTAs/SM, 64 registers (uncapped 76: C2 cull
+#endif              // 21.1 -> 19.2 ms, C5 222 -> 212.5 ms; 20 CTAs spill 172 B, C5 +2%)
+#if TS_MINB > 0
+#define TS_BOUNDS __launch_bounds__(TS_WARPS * 32, TS_MINB)
+#else
+#define TS_BOUNDS __launch_bounds__(TS_WARPS * 32)
+#endif
 #ifndef TS_VEC_STORE
 #define TS_VEC_STORE 1  // TriF32 assembled in registers, six 16-byte stores (C5 cull 352 -> 258 ms)
 #endif
-__global__ void __launch_bounds__(TS_WARPS * 32) k_tri_setup(const double* __restrict__ tw, int64_t T,
+__global__ void TS_BOUNDS k_tri_setup(const double* __restrict__ tw, int64_t T,
                                                    const float4* __restrict__ tsph, const float4* __restrict__ csph,
                                                    int64_t n_clu, const GmFixExact* __restrict__ fixes,
                                                    const GmFixCull* __restrict__ culls, int W, int H, TriStore ts,
