@@ -41,16 +41,8 @@
 #ifndef SAMPLE_GRID_MULT
 #define SAMPLE_GRID_MULT 1  // persistent sample-pass grid = resident CTAs x this
 #endif
-// launch bounds of the hot kernels; -DTX_MINB=n etc. (build variants) cap
-// their registers for n CTAs per SM
-#ifndef TX_MINB
-#define TX_MINB 14  // 64-thread CTAs: 72 registers (uncapped the first pass takes 88)
-#endif
-#if TX_MINB > 0
-#define TX_BOUNDS __launch_bounds__(TX_MAX_THREADS, TX_MINB)
-#else
-#define TX_BOUNDS __launch_bounds__(TX_MAX_THREADS)
-#endif
+// launch bounds of the hot kernels (k_texels / k_texels_crowded: TX_WARPS_SM* / HV_*_WARPS_SM in
+// gm_texels.cuh); -DKS_MINB=n etc. (build variants) re-size their register budgets
 #ifndef KS_MINB
 #define KS_MINB 4  // k_samples: 4 CTAs (32 warps) per SM, 64 registers (C5 accumulate 269 -> 245 ms;
 #endif             // uncapped: 80 registers, 3 CTAs)
