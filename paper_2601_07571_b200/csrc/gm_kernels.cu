@@ -272,6 +272,23 @@ __global__ void k_group_spheres(const float4* __restrict__ member, const double*
 // the float32 evaluation at any pixel centre of the bbox and the reference's
 // own float64 rounding (kernels.py:107-125): |e32 - e_ref| <= tol,
 // |invw32 - invw_ref| <= tolw.  Built once per screen triangle in k_tri_setup.
+#ifndef TRI80
+#define TRI80 1  // 80-byte TriF32 with one edge tolerance (the max of the three) instead of 96 bytes
+#endif
+#if TRI80
+struct __align__(16) TriF32 {
+    float inv_minw;                  // >= every inverse depth the triangle writes
+    float ox, oy;                    // frame origin = bbox corner (x0, y0), pixels
+    float wx;                        // bbox extent x1 - x0 + 1 (and wy): pixel centre c = (px + 0.5,
+    float wy;                        // py + 0.5) is in the bbox iff 0 < c - o < w (exact in float32)
+    int gidx;                        // index of the float64 record in the fixation's segment
+    float tol, tolw;                 // edge-function (all three edges) and inverse-depth bounds
+    float a[3], b[3], c[3];          // e_i = a x + b y + c
+    float A, B, C;                   // inverse depth
+};  // 80 B, every byte written
+static_assert(sizeof(TriF32) == 80, "TriF32 is five 16-byte words");
+#define TRI_TOL(t, i) ((t).tol)
+#else
 struct __align__(16) TriF32 {
     float a[3], b[3], c[3], tol[3];  // e_i = a x + b y + c
     float A, B, C, tolw;             // inverse depth
@@ -283,6 +300,9 @@ struct __align__(16) TriF32 {
     int pad[2];                      // (explicit: every byte of the 96 is written and copied)
 };  // 96 B
 static_assert(sizeof(TriF32) == 96, "TriF32 is six 16-byte words");
+#define TRI_TOL(t, i) ((t).tol[i])
+#endif
+constexpr int TRI_WORDS = (int)sizeof(TriF32) / 16;  // 16-byte words per record (staging copies)
 
 __device__ __forceinline__ void make_tri_f32(const GmScreenTri& T, int gidx, TriF32& o) {
     const double ox = T.x0, oy = T.y0;
@@ -290,6 +310,9 @@ __device__ __forceinline__ void make_tri_f32(const GmScreenTri& T, int gidx, Tri
     const double iw[3] = {T.iw0, T.iw1, T.iw2};
     const double xmax = (double)(T.x1 - T.x0 + 1), ymax = (double)(T.y1 - T.y0 + 1);
     double A = 0.0, B = 0.0, C = 0.0, Aab = 0.0, Bab = 0.0, Cab = 0.0;
+#if TRI80
+    double tol = 0.0;
+#endif
 #pragma unroll
     for (int i = 0; i < 3; i++) {
         // edge i runs from vertex (i+1)%3 to (i+2)%3: w_i = (bx-ax)(py-ay) - (by-ay)(px-ax)
@@ -302,7 +325,11 @@ __device__ __forceinline__ void make_tri_f32(const GmScreenTri& T, int gidx, Tri
         // float32 plane evaluation error <= ~4 * 2^-24 and the reference's float64
         // rounding <= ~4 * 2^-53 of |a|(|x|+|ax|) + |b|(|y|+|ay|); tol is >= 2x that
         const double mag = fabs(a) * (xmax + fabs(sx[ia])) + fabs(b) * (ymax + fabs(sy[ia]));
+#if TRI80
+        tol = fmax(tol, 4.8e-7 * mag + 1e-30);
+#else
         o.tol[i] = (float)(4.8e-7 * mag + 1e-30);
+#endif
         const double k = iw[i] * T.inv_area;  // l_i = w_i * inv_area, inv_w = sum l_i iw_i
         A += a * k;
         B += b * k;
@@ -321,7 +348,11 @@ __device__ __forceinline__ void make_tri_f32(const GmScreenTri& T, int gidx, Tri
     o.wx = (float)(T.x1 - T.x0 + 1);
     o.wy = (float)(T.y1 - T.y0 + 1);
     o.gidx = gidx;
+#if TRI80
+    o.tol = (float)tol;  // rounded to nearest: the 2x margin of each edge's bound covers it
+#else
     o.pad[0] = o.pad[1] = 0;
+#endif
 }
 
 struct TriStore {
@@ -353,7 +384,7 @@ struct TriStore {
 #define TS_BOUNDS __launch_bounds__(TS_WARPS * 32)
 #endif
 #ifndef TS_VEC_STORE
-#define TS_VEC_STORE 1  // TriF32 assembled in registers, six 16-byte stores (C5 cull 352 -> 258 ms)
+#define TS_VEC_STORE 1  // TriF32 assembled in registers, 16-byte stores (C5 cull 352 -> 258 ms)
 #endif
 __global__ void TS_BOUNDS k_tri_setup(const double* __restrict__ tw, int64_t T,
                                                    const float4* __restrict__ tsph, const float4* __restrict__ csph,
@@ -414,7 +445,7 @@ __global__ void TS_BOUNDS k_tri_setup(const double* __restrict__ tw, int64_t T,
                     uint4* dst = reinterpret_cast<uint4*>(&ts.t32[(int64_t)f * ts.cap_seg + at + q]);
                     const uint4* src = reinterpret_cast<const uint4*>(&tf);
 #pragma unroll
-                    for (int part = 0; part < 6; part++) dst[part] = src[part];
+                    for (int part = 0; part < TRI_WORDS; part++) dst[part] = src[part];
                 }
 #else
                 make_tri_f32(out[q], at + q, ts.t32[(int64_t)f * ts.cap_seg + at + q]);

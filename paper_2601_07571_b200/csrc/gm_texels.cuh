@@ -232,7 +232,7 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
                     const uint4* fr = reinterpret_cast<const uint4*>(segf + gm_[m]);
                     uint4* to = reinterpret_cast<uint4*>(&T32[rk[m]]);
 #pragma unroll
-                    for (int part = 0; part < 6; part++) to[part] = fr[part];
+                    for (int part = 0; part < TRI_WORDS; part++) to[part] = fr[part];
                 }
             }
             __syncwarp();
@@ -272,7 +272,7 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
             const uint4* from = reinterpret_cast<const uint4*>(segf + src);
             uint4* to = reinterpret_cast<uint4*>(&T32[dst]);
 #pragma unroll
-            for (int part = 0; part < 6; part++) to[part] = from[part];
+            for (int part = 0; part < TRI_WORDS; part++) to[part] = from[part];
         }
         __syncwarp();
     };
@@ -343,8 +343,8 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
 #pragma unroll
             for (int i = 0; i < 3; i++) {
                 const float e = __fmaf_rn(t.a[i], fx, __fmaf_rn(t.b[i], fy, t.c[i]));
-                maybe = maybe && (e >= -t.tol[i]);
-                certain = certain && (e > t.tol[i]);
+                maybe = maybe && (e >= -TRI_TOL(t, i));
+                certain = certain && (e > TRI_TOL(t, i));
             }
             if (!maybe) continue;
             const float iwv = __fmaf_rn(t.A, fx, __fmaf_rn(t.B, fy, t.C));
@@ -718,7 +718,7 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
                         const uint4* from = reinterpret_cast<const uint4*>(segf + SS[k]);
                         uint4* to = reinterpret_cast<uint4*>(&T32[lane]);
 #pragma unroll
-                        for (int part = 0; part < 6; part++) to[part] = from[part];
+                        for (int part = 0; part < TRI_WORDS; part++) to[part] = from[part];
                     }
                     __syncwarp();
                 }
