@@ -72,6 +72,9 @@ struct __align__(16) TexelWarpSmem {
 #ifndef HV_FULL_SEL
 #define HV_FULL_SEL 2048
 #endif
+#ifndef WALK_SLOTS2
+#define WALK_SLOTS2 1  // walk candidate slots: empty = -inf upper bound, "certainly written" in the lower bound's sign
+#endif
 #ifndef SORT_WARP
 #define SORT_WARP 1  // crowded pass: bitonic sizes 2..32 by warp shuffles (C5 -0.6%; strides <= 16 of
 #endif               // the larger sizes in registers too: C5 +5%)
@@ -332,9 +335,16 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
         const int px = xb + colo, py = yb + row;
         const float pxc = (float)px + 0.5f, pyc = (float)py + 0.5f;  // pixel centre
         int cs0 = -1, cs1 = -1;  // exact candidates (global record index) and their bounds
+#if WALK_SLOTS2
+        // a slot is live while its inverse-depth upper bound is >= V (empty: -inf); cl = the
+        // lower bound when the triangle is certainly written there (> 0), else -1
+        float ch0 = -CUDART_INF_F, ch1 = -CUDART_INF_F;
+        float cl0 = -1.0f, cl1 = -1.0f;
+#else
         float ch0 = 0.0f, ch1 = 0.0f;
         float cl0 = 0.0f, cl1 = 0.0f;   // their lower inverse-depth bounds
         bool ce0 = false, ce1 = false;  // certainly covering and written
+#endif
         bool overflow = false;
         for (int kk = 0; kk < kend; kk++) {
             const TriF32& t = fetch(kk);
@@ -362,6 +372,22 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
             if (!(hi > 0.0f) || lo > inv_near_hi || hi < inv_far_lo) continue;  // certainly not written
             const bool cw = certain && lo > 0.0f && hi <= inv_near_lo && lo >= inv_far_hi;
             if (cw && lo * (1.0f - 1e-6f) > V) V = lo * (1.0f - 1e-6f);
+#if WALK_SLOTS2
+            if (hi >= V) {  // an empty or stale slot takes it (a stale one can never win again)
+                const float clv = cw ? lo : -1.0f;
+                if (ch0 < V) {
+                    cs0 = t.gidx;
+                    ch0 = hi;
+                    cl0 = clv;
+                } else if (ch1 < V) {
+                    cs1 = t.gidx;
+                    ch1 = hi;
+                    cl1 = clv;
+                } else {
+                    overflow = true;
+                }
+            }
+#else
             if (hi >= V) {
                 if (cs0 < 0) {
                     cs0 = t.gidx;
@@ -387,10 +413,16 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
                     overflow = true;
                 }
             }
+#endif
         }
         if (!valid) return false;
+#if WALK_SLOTS2
+        const bool live0 = ch0 >= V, live1 = ch1 >= V;
+        if (allow_fast && !overflow && live0 != live1 && (live0 ? cl0 : cl1) > 0.0f) {
+#else
         const bool live0 = cs0 >= 0 && ch0 >= V, live1 = cs1 >= 0 && ch1 >= V;
         if (allow_fast && !overflow && live0 != live1 && (live0 ? ce0 : ce1)) {
+#endif
             // the only candidate left is certainly written and every other triangle is
             // provably farther (inverse depth < V <= its own lower bound)
             bwin = live0 ? cs0 : cs1;
