@@ -72,6 +72,9 @@ struct __align__(16) TexelWarpSmem {
 #ifndef HV_FULL_SEL
 #define HV_FULL_SEL 2048
 #endif
+#ifndef EDGE_MIN
+#define EDGE_MIN 1  // walk edge test as one min over the three edge functions (80-byte TriF32)
+#endif
 #ifndef WALK_SLOTS2
 #define WALK_SLOTS2 1  // walk candidate slots: empty = -inf upper bound, "certainly written" in the lower bound's sign
 #endif
@@ -359,6 +362,15 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
             const bool in = (inv_minw >= V) & (fx > 0.0f) & (fx < hd.w) & (fy > 0.0f) & (fy < wy);
             if (!in) continue;
             if (STATS) c_edge++;
+#if TRI80 && EDGE_MIN
+            // one tolerance for the three edges: all e_i >= -tol  <=>  min e_i >= -tol (the
+            // planes and the bbox-local centre are finite, so no NaN reaches the min)
+            const float em = fminf(fminf(__fmaf_rn(t.a[0], fx, __fmaf_rn(t.b[0], fy, t.c[0])),
+                                         __fmaf_rn(t.a[1], fx, __fmaf_rn(t.b[1], fy, t.c[1]))),
+                                   __fmaf_rn(t.a[2], fx, __fmaf_rn(t.b[2], fy, t.c[2])));
+            if (!(em >= -t.tol)) continue;
+            const bool certain = em > t.tol;
+#else
             bool maybe = true, certain = true;
 #pragma unroll
             for (int i = 0; i < 3; i++) {
@@ -367,6 +379,7 @@ __device__ __forceinline__ void texel_item(TriF32* __restrict__ T32, int* __rest
                 certain = certain && (e > TRI_TOL(t, i));
             }
             if (!maybe) continue;
+#endif
             const float iwv = __fmaf_rn(t.A, fx, __fmaf_rn(t.B, fy, t.C));
             const float lo = iwv - t.tolw, hi = iwv + t.tolw;
             if (!(hi > 0.0f) || lo > inv_near_hi || hi < inv_far_lo) continue;  // certainly not written
